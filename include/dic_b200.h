@@ -1,0 +1,231 @@
+/*
+ * dic_b200.h — C ABI of the B200-native DIC bitmap support count.
+ *
+ * This is the drop-in boundary for the hot path of the reference `dicmine`
+ * package (Python + NumPy; /root/reference/pkg/src/dicmine).  The reference
+ * has no FFI of its own: its operator seam is the module-global kernel
+ * `_count_block(arr, first, last, mask) -> int` (engine.py:43-58) selected by
+ * `count_support_interval` (engine.py:176-223), plus the bitmap builder
+ * `encode_transaction` / `BitDatabase` (bitops.py:24-37, database.py:13-86).
+ * Each entry point below names the reference function it replaces.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; every data pointer is a DEVICE pointer
+ *     unless the comment says "host"; `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream);
+ *   - return 0 on success or a negative DIC_E* code; the message for the last
+ *     failure on the calling thread is available from dic_last_error();
+ *   - argument errors are detected on the host before any launch; data errors
+ *     (item id outside [0, m), table overflow) are reported through device
+ *     status words that the caller reads after synchronising — kernels never
+ *     trap on data;
+ *   - everything is asynchronous on `stream` except functions documented as
+ *     synchronising.
+ *
+ * Bit layouts (shared by all kernels):
+ *   rows   : uint64 [n][W], W = ceil(m/64); item p of row j is bit (p & 63)
+ *            of word (p >> 6) — the reference's single-word layout
+ *            (bitops.py:36) extended LSW-first to W words.
+ *   tids   : uint32 [m][ld], the item-major bit-sliced ("vertical") copy:
+ *            bit b of tids[i*ld + g] is set iff row 32*g + b holds item i.
+ *            ld is a multiple of 32 (128-byte rows), words past n are zero.
+ *   items  : uint16 [C][k], the k ascending item ids of each candidate of a
+ *            size-k bucket (candidates of one launch share k).
+ */
+#ifndef DIC_B200_H
+#define DIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    DIC_OK = 0,
+    DIC_EINVAL = -1,   /* bad argument (mirrors the reference's ValueError)   */
+    DIC_ECUDA = -2,    /* CUDA launch / runtime failure                        */
+    DIC_ENOMEM = -3,   /* device allocation failed                             */
+    DIC_EDATA = -4,    /* input data error (e.g. ItemOutOfRange)               */
+    DIC_ESTATE = -5    /* engine used out of order                             */
+};
+
+#define DIC_ABI_VERSION 1
+
+/* Library / error plumbing --------------------------------------------- */
+int dic_abi_version(void);
+const char* dic_last_error(void);
+/* Number of SMs of the current device (for grid sizing by callers).       */
+int dic_device_sm_count(void);
+
+/* Encoder: CSR item lists -> row bitmap ---------------------------------
+ * Replaces encode_transaction (bitops.py:24-37) applied per row, i.e.
+ * database_from_transactions (database.py:89-93) / as_bit_database's ragged
+ * branch (_validation.py:56).  Duplicates collapse into one bit.
+ * rows must hold n*W words; it is fully overwritten.
+ * status (device, int64[4], caller-zeroed NOT required — the call resets it):
+ *   status[0] = number of duplicate ids collapsed (sum over rows of
+ *               len - popcount), the LoadReport dedup figure (datasets.py:160-194)
+ *   status[1] = flat CSR position of the FIRST out-of-range id in row-major
+ *               order (the one encode_transaction would raise on), or -1
+ *   status[2] = its row, or -1
+ * The caller reads status after synchronising; status[1] >= 0 maps to
+ * ItemOutOfRange(indices[status[1]], line=row). */
+int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int64_t n,
+                   int32_t m, uint64_t* rows, int64_t* status, void* stream);
+
+/* Row bitmap -> item-major bit-sliced copy (tids, layout above).
+ * tids must hold m*ld words, ld >= ceil(n/32) and ld % 32 == 0.          */
+int dic_rows_to_tids(const uint64_t* rows, int64_t n, int32_t m,
+                     uint32_t* tids, int64_t ld, void* stream);
+/* Helper: the ld dic_rows_to_tids expects for n rows (host function).     */
+int64_t dic_tids_ld(int64_t n);
+
+/* First pass: per-item supports -----------------------------------------
+ * Replaces first_pass's singleton counting (engine.py:132-154): for every
+ * item i < m, counts[i] += #{ j in [first, last] : row j holds i }.
+ * counts is ACCUMULATED into (int64), so multi-GPU shards can sum locally. */
+int dic_item_support(const uint32_t* tids, int64_t ld, int32_t m,
+                     int64_t first, int64_t last, int64_t* counts,
+                     void* stream);
+
+/* THE hot kernel: candidate support over one chunk ----------------------
+ * Replaces _count_block (engine.py:43-58) as called by
+ * count_support_interval (engine.py:176-223) for every dashed itemset:
+ *   support_inc[c] += #{ j in [first, last] : (rows[j] & I_c) == I_c }
+ * computed on the bit-sliced copy as sum_g popc(AND_{i in I_c} tids[i][g]),
+ * 0 <= first <= last < n (the caller checks the reference's range rule and
+ * raises ValueError; this entry returns DIC_EINVAL on violation).
+ * Candidates are one size bucket: items[c*k .. c*k+k-1], 1 <= k <= m.
+ * support_inc is accumulated into (uint64 counts).                         */
+int dic_count_support(const uint32_t* tids, int64_t ld, int32_t m,
+                      int64_t first, int64_t last,
+                      const uint16_t* items, int32_t k, int64_t C,
+                      uint64_t* support_inc, void* stream);
+
+/* The same count on the row bitmap, the literal `(T & I) == I` form of
+ * _count_block (engine.py:54-56) for C multi-word masks [C][W].  Used as an
+ * independent second kernel for parity checks and for callers that only
+ * hold the row bitmap.  support_inc is accumulated into.                  */
+int dic_count_support_rows(const uint64_t* rows, int32_t W,
+                           int64_t first, int64_t last,
+                           const uint64_t* masks, int64_t C,
+                           uint64_t* support_inc, void* stream);
+
+/* Candidate generation + subset pruning ---------------------------------
+ * Replaces make_candidates' join/admission loop (engine.py:320-369) for the
+ * API-level call on a host catalog.  `box_masks` [B][W] is the set of masks
+ * currently known with a box shape, `known_masks` [K][W] every known mask
+ * (any shape).  For every (s, l) with s < S, l < L:
+ *   cand = src_masks[s] | (1 << level1[l]);
+ *   admit[s*L + l] = cand != src && cand not in known && every immediate
+ *                    subset of cand is in box_masks.
+ * The caller applies the reference's first-occurrence dedup in (s, l) order.
+ * Synchronising (builds a temporary device hash set).                     */
+int dic_candidate_admission(const uint64_t* src_masks, int64_t S,
+                            const int32_t* level1, int64_t L, int32_t W,
+                            const uint64_t* known_masks, int64_t K,
+                            const uint64_t* box_masks, int64_t B,
+                            uint8_t* admit, void* stream);
+
+/* Device-resident DIC engine ---------------------------------------------
+ * The checkpoint loop of _run (engine.py:398-458) with the catalog
+ * (itemsets.py:88-136) held on the device as structure-of-arrays plus a
+ * hash index of every mask ever created (`known`).  One engine per rank;
+ * each rank holds the LOCAL rows of its shard (chunk-sliced
+ * sharding), the state machine is replicated on every rank.             */
+typedef struct dic_engine dic_engine;
+
+typedef struct dic_stop_status {
+    int64_t dashed_at_start;  /* |dashed| counted at this stop (interval_counts) */
+    int64_t promoted;         /* DASHED_CIRCLE -> DASHED_BOX (prune, :296-298)  */
+    int64_t pruned;           /* DASHED_CIRCLE -> NIL by the bound (:299-310)    */
+    int64_t inserted;         /* new candidates (make_candidates, :366-369)      */
+    int64_t dashed_peak;      /* |dashed| after make_candidates (peak, :440)     */
+    int64_t finalized;        /* dashed -> solid (check_full_pass, :372-390)     */
+    int64_t dashed_at_end;    /* |dashed| after compaction (loop test, :423)     */
+    int64_t records;          /* itemsets ever created (|known|)                 */
+} dic_stop_status;
+
+/* tids/ld/n_local: this rank's bit-sliced rows (owned by the caller, must
+ * outlive the engine).  need = ceil(minsup*n) (params.py:17-19),
+ * interval = M, stop_max = ceil(n/M) over the GLOBAL n.                   */
+int dic_engine_create(const uint32_t* tids, int64_t ld, int64_t n_local,
+                      int32_t m, int64_t need, int64_t interval,
+                      int64_t stop_max, int32_t prune_bound, void* stream,
+                      dic_engine** out);
+int dic_engine_destroy(dic_engine* e);
+/* first_pass (engine.py:105-173), step 1: local per-item counts into
+ * counts[m] (device int64, overwritten).  Multi-GPU callers sum-allreduce
+ * counts before step 2.                                                   */
+int dic_engine_item_counts(dic_engine* e, int64_t* counts);
+/* step 2: singleton records (SOLID_BOX / SOLID_CIRCLE, intervals=stop_max),
+ * level1, and every frequent pair seeded as DASHED_CIRCLE.  Synchronising;
+ * returns |level1| and the number of pairs seeded.                        */
+int dic_engine_seed(dic_engine* e, const int64_t* counts,
+                    int64_t* n_level1, int64_t* n_pairs);
+/* Per stop, step 1: count every dashed candidate over LOCAL rows
+ * [lfirst, llast] into the delta buffer (zeroed here).  lfirst > llast
+ * (an empty local slice) is allowed and counts nothing.                  */
+int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast);
+/* The delta buffer (device uint64/int64 [*len]) for the per-stop
+ * sum-allreduce across ranks; valid until the next checkpoint.           */
+int dic_engine_delta(dic_engine* e, void** ptr, int64_t* len);
+/* Per stop, step 2: support += delta, intervals += 1, prune, make
+ * candidates, check_full_pass, compact.  Synchronising; fills *st.       */
+int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st);
+/* Results: number of SOLID_BOX records, then copy them out to HOST arrays
+ * masks[F][W] (uint64), sizes[F], supports[F] (unsorted).  Synchronising. */
+int dic_engine_num_frequent(dic_engine* e, int64_t* F);
+int dic_engine_frequent(dic_engine* e, uint64_t* masks_host,
+                        int32_t* sizes_host, int64_t* supports_host,
+                        int64_t F);
+/* Words per mask of this engine (W = ceil(m/64)).                        */
+int dic_engine_words(dic_engine* e);
+
+/* Synthetic generators (host, multithreaded, counter-based RNG) ---------
+ * Seeded restatements of BASELINE.json's config generators (DESIGN.md
+ * §Inputs).  Rows are generated for the GLOBAL row ranges
+ * [range_begin[i], range_begin[i] + range_len[i]) concatenated in order, so a
+ * rank can generate exactly its shard; output is identical for any thread
+ * count and any range split.  The result is an opaque host CSR.          */
+typedef struct dic_csr dic_csr;
+int dic_synth_zipf(const int64_t* range_begin, const int64_t* range_len,
+                   int nranges, int32_t m, double s, double mean_len,
+                   uint64_t seed, int threads, dic_csr** out);
+int dic_synth_quest(const int64_t* range_begin, const int64_t* range_len,
+                    int nranges, int32_t m, int32_t n_patterns,
+                    double pattern_len, double mean_len, uint64_t seed,
+                    int threads, dic_csr** out);
+int dic_synth_dense(const int64_t* range_begin, const int64_t* range_len,
+                    int nranges, int32_t m, int32_t groups,
+                    int32_t group_size, double group_p, uint64_t seed,
+                    int threads, dic_csr** out);
+int dic_csr_info(const dic_csr* c, int64_t* n, int64_t* nnz);
+/* host arrays: indptr[n+1], indices[nnz]                                  */
+int dic_csr_export(const dic_csr* c, int64_t* indptr, int32_t* indices);
+void dic_csr_free(dic_csr* c);
+/* cfg5: row bitmap rows[n][W] of i.i.d. Bernoulli(p) bits, generated on the
+ * device; and C candidates (host arrays) with k ~ U{kmin..kmax} items drawn
+ * uniformly without replacement: cand_k[C], cand_items[C][kmax] ascending,
+ * unused slots 0xFFFF.                                                    */
+int dic_synth_bernoulli_rows(int64_t n, int32_t m, double p, uint64_t seed,
+                             uint64_t* rows, void* stream);
+int dic_synth_candidates(int64_t C, int32_t m, int32_t kmin, int32_t kmax,
+                         uint64_t seed, int32_t* cand_k, uint16_t* cand_items);
+
+/* Peak probes (for the roofline denominators) ---------------------------
+ * Runs `iters` iterations of an unrolled LOP3 (op=0), POPC (op=1) or IADD
+ * (op=2) chain on every thread of blocks x threads; *sink is written only
+ * under a data-dependent (practically false) condition so nothing is dead.
+ * Synchronising; returns the lane-ops issued and the CUDA-event time.     */
+int dic_probe_int_pipe(int op, int blocks, int threads, int64_t iters,
+                       uint32_t* sink, double* lane_ops, float* ms,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIC_B200_H */

@@ -1,0 +1,88 @@
+// common.cuh — shared plumbing for the DIC B200 kernels: error reporting,
+// launch checking and small device helpers.  Internal to libdicb200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include <algorithm>
+
+#include "../../include/dic_b200.h"
+
+namespace dic {
+
+// Thread-local message for dic_last_error().
+void set_error(const char* fmt, ...);
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? DIC_ENOMEM : DIC_ECUDA;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+#define DIC_CHECK_LAUNCH(what)                                   \
+    do {                                                         \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return ::dic::cuda_fail(_e, what); \
+    } while (0)
+
+#define DIC_CUDA(call)                                           \
+    do {                                                         \
+        cudaError_t _e = (call);                                 \
+        if (_e != cudaSuccess) return ::dic::cuda_fail(_e, #call); \
+    } while (0)
+
+#define DIC_REQUIRE(cond, ...)                                   \
+    do {                                                         \
+        if (!(cond)) { ::dic::set_error(__VA_ARGS__); return DIC_EINVAL; } \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// Chunk geometry on the bit-sliced layout.  Row j lives in group j>>5, bit
+// j&31.  A chunk [first, last] (inclusive, the reference's convention,
+// params.py:67-75) touches groups g_first..g_last with partial masks at the
+// two ends.
+struct ChunkGeom {
+    int64_t g_first, g_last;   // inclusive group range
+    uint32_t first_mask;       // bits of g_first inside the chunk
+    uint32_t last_mask;        // bits of g_last inside the chunk
+};
+
+__host__ __device__ inline ChunkGeom chunk_geom(int64_t first, int64_t last) {
+    ChunkGeom c;
+    c.g_first = first >> 5;
+    c.g_last = last >> 5;
+    c.first_mask = 0xFFFFFFFFu << (uint32_t)(first & 31);
+    uint32_t lb = (uint32_t)(last & 31);
+    c.last_mask = lb == 31 ? 0xFFFFFFFFu : ((1u << (lb + 1)) - 1u);
+    return c;
+}
+
+// Mask of the rows of group g that lie inside the chunk.
+__device__ __forceinline__ uint32_t group_mask(const ChunkGeom& c, int64_t g) {
+    uint32_t mk = (g < c.g_first || g > c.g_last) ? 0u : 0xFFFFFFFFu;
+    if (g == c.g_first) mk &= c.first_mask;
+    if (g == c.g_last) mk &= c.last_mask;
+    return mk;
+}
+
+// 64-bit mixer (SplitMix64 finalizer, the constants of datasets.py:44-53's
+// generator family).  Used for hashing masks and for counter-based RNG.
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__host__ __device__ inline uint64_t hash_words(const uint64_t* w, int W) {
+    uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(W + 1);
+    for (int i = 0; i < W; ++i) h = mix64(h ^ (w[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1)));
+    return h;
+}
+
+}  // namespace dic

@@ -1,0 +1,136 @@
+"""Kernel-level parity on the GPU: encoder, bit-sliced transform, item support,
+the hot support-count kernel and the row-form count, each against a plain
+numpy restatement of the reference's `(T & I) == I` count (engine.py:43-58)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1812_10959_b200 import device as D
+
+pytestmark = pytest.mark.gpu
+
+
+def np_count(rows: np.ndarray, first: int, last: int, masks: np.ndarray) -> np.ndarray:
+    blk = rows[first : last + 1]
+    out = np.empty(masks.shape[0], dtype=np.int64)
+    for c in range(masks.shape[0]):
+        out[c] = int(np.count_nonzero(np.all((blk & masks[c]) == masks[c], axis=1)))
+    return out
+
+
+def random_rows(rng, n, m, density):
+    W = D.words_for(m)
+    bits = rng.random((n, W * 64)) < density
+    bits[:, m:] = False
+    rows = np.packbits(bits.reshape(n, W, 64)[:, :, ::-1], axis=2, bitorder="big")
+    return np.ascontiguousarray(rows.view(">u8").reshape(n, W).astype(np.uint64))
+
+
+def items_to_masks(items: np.ndarray, W: int) -> np.ndarray:
+    out = np.zeros((items.shape[0], W), dtype=np.uint64)
+    for c, row in enumerate(items):
+        for it in row:
+            out[c, it >> 6] |= np.uint64(1) << np.uint64(it & 63)
+    return out
+
+
+def to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("m", [1, 7, 64, 65, 128, 300, 1000])
+def test_encode_and_transpose(m):
+    rng = np.random.default_rng(m)
+    n = 2500
+    lens = rng.integers(0, min(m, 12) + 1, size=n)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(lens)
+    indices = rng.integers(0, m, size=int(indptr[-1])).astype(np.int32)  # duplicates on purpose
+    rows, status = D.encode_csr(to_dev(indptr), to_dev(indices), n, m)
+    W = D.words_for(m)
+    want = np.zeros((n, W), dtype=np.uint64)
+    dedup = 0
+    for r in range(n):
+        s = set(indices[indptr[r] : indptr[r + 1]].tolist())
+        dedup += lens[r] - len(s)
+        for it in s:
+            want[r, it >> 6] |= np.uint64(1) << np.uint64(it & 63)
+    got = rows.cpu().numpy()
+    assert np.array_equal(got, want)
+    st = status.cpu().numpy()
+    assert st[0] == dedup and st[1] == -1 and st[2] == -1
+    tids, ld = D.rows_to_tids(rows, n, m)
+    t = tids.cpu().numpy().view(np.uint32)
+    for i in range(m):
+        col = (want[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1)
+        padded = np.zeros(ld * 32, dtype=np.uint64)
+        padded[:n] = col
+        words = (padded.reshape(ld, 32) << np.arange(32, dtype=np.uint64)).sum(axis=1).astype(np.uint32)
+        assert np.array_equal(t[i], words), f"item {i}"
+
+
+def test_encode_reports_first_bad_item():
+    indptr = np.array([0, 2, 2, 5, 6], dtype=np.int64)
+    indices = np.array([1, 3, 0, 70, 99, 64], dtype=np.int32)  # m=64: 70 at pos 3 (row 2) first
+    rows, status = D.encode_csr(to_dev(indptr), to_dev(indices), 4, 64)
+    st = status.cpu().numpy()
+    assert st[1] == 3 and st[2] == 2
+
+
+@pytest.mark.parametrize("m,n,first,last", [
+    (64, 4000, 0, 3999), (64, 4000, 17, 2049), (130, 3001, 5, 5), (1000, 10000, 999, 8190),
+    (512, 70000, 123, 69999), (33, 1, 0, 0)])
+def test_item_support(m, n, first, last):
+    rng = np.random.default_rng(n + m)
+    rows = random_rows(rng, n, m, 0.3)
+    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
+    got = D.item_support(tids, ld, m, first, last).cpu().numpy()
+    blk = rows[first : last + 1]
+    want = np.array([np.count_nonzero((blk[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1)) for i in range(m)])
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m,n,k,C,density,first,last", [
+    (64, 5000, 2, 700, 0.4, 0, 4999),
+    (64, 5000, 3, 300, 0.5, 31, 1031),       # unaligned both ends
+    (128, 20000, 1, 128, 0.3, 1, 19998),
+    (1000, 30000, 2, 5000, 0.05, 100, 29000),
+    (512, 40000, 5, 2000, 0.5, 64, 39999),
+    (200, 9000, 8, 500, 0.7, 0, 8999),
+    (200, 9000, 11, 300, 0.8, 3, 8000),       # generic-k path
+    (70, 100, 4, 50, 0.6, 40, 40),            # single-row chunk
+])
+def test_count_support_matches_numpy(m, n, k, C, density, first, last):
+    rng = np.random.default_rng(m * 7 + k)
+    rows = random_rows(rng, n, m, density)
+    items = np.sort(np.stack([rng.choice(m, size=k, replace=False) for _ in range(C)]), axis=1).astype(np.uint16)
+    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
+    got = D.count_support(tids, ld, m, first, last, to_dev(items.view(np.int16))).cpu().numpy()
+    want = np_count(rows, first, last, items_to_masks(items, D.words_for(m)))
+    assert np.array_equal(got, want)
+    # the literal row-form kernel agrees too
+    got_rows = D.count_support_rows(to_dev(rows), first, last, to_dev(items_to_masks(items, D.words_for(m)))).cpu().numpy()
+    assert np.array_equal(got_rows, want)
+
+
+def test_count_support_accumulates():
+    rng = np.random.default_rng(5)
+    m, n = 96, 3000
+    rows = random_rows(rng, n, m, 0.5)
+    items = np.array([[1, 2], [5, 90], [0, 95]], dtype=np.uint16)
+    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
+    out = torch.full((3,), 7, dtype=torch.int64, device="cuda")
+    D.count_support(tids, ld, m, 0, 999, to_dev(items.view(np.int16)), out)
+    D.count_support(tids, ld, m, 1000, n - 1, to_dev(items.view(np.int16)), out)
+    want = np_count(rows, 0, n - 1, items_to_masks(items, 2)) + 7
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_bad_chunk_rejected():
+    rows = to_dev(np.array([[1], [2]], dtype=np.uint64))
+    tids, ld = D.rows_to_tids(rows, 2, 2)
+    with pytest.raises(D._abi.DicError):
+        D.count_support(tids, ld, 2, 1, 0, to_dev(np.array([[0]], dtype=np.int16)))
