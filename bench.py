@@ -1,0 +1,355 @@
+"""Benchmark: end-to-end DIC on BASELINE.json's large sharded config (cfg4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step is one complete DIC run (first pass + every checkpoint until no
+dashed itemset is left) of cfg4 — n = 10,000,000 Quest-style transactions
+over m = 1,000 items, minsup 0.1 %, M = 100,000 — from the bit-sliced
+database resident in HBM to the sorted frequent itemsets on the host.
+`value` is subset-tests/s over the whole job (first pass m*n singleton tests
+plus, per stop, |dashed| x chunk rows), `e2e` the same metric through the
+public API from pinned host CSR (H2D + GPU encode + mine + D2H result).
+
+Under torchrun (N > 1) each rank generates and holds only its chunk-sliced
+shard (sharding.py) and the per-stop count deltas are sum-allreduced over
+NCCL; the total work is fixed, so scaling is "strong".
+
+`--impl reference` times the CPU restatement of the reference engine
+(oracle/dic_oracle.c, the "port" arm: the reference is pure Python and
+cannot travel to the GPU box) on the host cores, rank 0 only, each step a
+bounded sample of the same workload: first pass + the first checkpoint.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+CFG_INDEX = 4
+
+
+def parse() -> argparse.Namespace:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=CFG_INDEX)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def int_peaks() -> dict:
+    """Live LOP3 / POPC lane-op peaks (MEASURED_PEAKS.json has no integer pipes)."""
+    import torch
+
+    from paper_1812_10959_b200 import device as D
+
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    out = {}
+    for op, name in ((0, "lop3"), (1, "popc")):
+        best = 0.0
+        for threads in (512, 1024):
+            blocks = sms * (2048 // threads)
+            D.probe_int_pipe(op, blocks, threads, 32)
+            ops, ms = D.probe_int_pipe(op, blocks, threads, 1024)
+            best = max(best, ops / (ms * 1e-3))
+        out[name] = best
+    return out
+
+
+def measured_hbm() -> tuple[float, str]:
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def subset_tests(n: int, m: int, params, trace) -> int:
+    """First pass (m*n singleton tests) + sum over stops of |dashed| x chunk rows."""
+    total = n * m
+    for st in trace.stops:
+        first, last = params.chunk_bounds(st["stop"])
+        total += st["dashed_at_start"] * (last - first + 1)
+    return total
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1812_10959_b200.config import MiningParams
+    from paper_1812_10959_b200.workloads import generate_csr
+    from tests.golden_util import rows_from_csr
+
+    cores = os.cpu_count() or 1
+    indptr, indices = generate_csr(cfg, threads=cores)
+    rows = rows_from_csr(indptr, indices, cfg.m)
+    params = MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    times, tests = [], 0
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        run = O.mine(rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=cores, max_stops=1)
+        dt = time.perf_counter() - t
+        first, last = params.chunk_bounds(1)
+        tests = cfg.n * cfg.m + run.interval_counts * (last - first + 1)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = tests / (ms * 1e-3)
+    sample = (f"{cfg.name}: oracle first pass over all {cfg.n} rows + the first checkpoint "
+              f"({run.interval_counts} dashed pairs x {cfg.interval} rows)")
+    line = {"metric": "subset-tests/s (end-to-end DIC, cfg4)", "value": value, "unit": "subset-tests/s",
+            "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded Quest-style generator)",
+            "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "minsup": cfg.minsup, "interval": cfg.interval,
+                       "sample": "first pass + 1 checkpoint per step"},
+            "cpu_baseline": {"value": value, "unit": "subset-tests/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "subset-tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main() -> None:
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1812_10959_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_10959_b200 as dic
+    from paper_1812_10959_b200 import _abi
+    from paper_1812_10959_b200 import device as D
+    from paper_1812_10959_b200.miner import StopTrace, run_engine
+    from paper_1812_10959_b200.workloads import generate_csr
+
+    torch.cuda.set_device(local_rank)
+    D.require_cuda()
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        group = dist.group.WORLD
+    lib = _abi.load()
+    params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    plan = dic.ShardPlan.for_params(params, world, rank)
+    cores = os.cpu_count() or 1
+    threads = max(1, cores // max(world, 1))
+    ranges = plan.ranges() if world > 1 else [(0, cfg.n)]
+    indptr, indices = generate_csr(cfg, ranges=ranges, threads=threads)
+    n_local = int(indptr.size - 1)
+
+    # pinned host CSR (the e2e input) and the HBM-resident bit-sliced copy
+    h_indptr = torch.from_numpy(indptr).pin_memory()
+    h_indices = torch.from_numpy(indices).pin_memory()
+    db = dic.BitDatabase.from_csr(h_indptr.cuda(), h_indices.cuda(), cfg.m)
+    tids = db.device_tids()
+    torch.cuda.synchronize()
+
+    def one_run(trace=None, count_events=None):
+        return run_engine(tids, n_local, cfg.m, params, plan=plan if world > 1 else None, group=group,
+                          trace=trace, count_events=count_events)
+
+    if args.profile:
+        one_run()
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(args.warmup):
+        one_run()
+    trace = StopTrace()
+    ref = one_run(trace=trace)
+    tests = subset_tests(cfg.n, cfg.m, params, trace)
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    count_events: list = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.dic_launch_count()
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for i in range(args.steps):
+            res = one_run(count_events=count_events if i == args.steps - 1 else None)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = (lib.dic_launch_count() - launches0) // args.steps
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    assert [(f.mask, f.support) for f in res.frequent] == [(f.mask, f.support) for f in ref.frequent]
+
+    # roofline of the dominant kernel (the streaming support count) over the
+    # last timed run: per launch >= 1 POPC per (candidate, 32-row word)
+    count_ms = [a.elapsed_time(b) for a, b, _ in count_events]
+    words = [w for _, _, w in count_events]
+    peaks = int_peaks()
+    hbm_gbs, hbm_src = measured_hbm()
+    tot_ms = sum(count_ms)
+    popc_ops = float(sum(words))
+    achieved = popc_ops / (tot_ms * 1e-3) if tot_ms > 0 else 0.0
+    roofline = {"bound": "int-pipe (POPC)", "achieved": achieved / 1e12, "peak": peaks["popc"] / 1e12,
+                "unit": "T word-popcounts/s", "frac": achieved / peaks["popc"] if peaks["popc"] else None,
+                "traffic": None, "kernel": "count_stream_kernel",
+                "launches": len(count_ms), "avg_launch_ms": tot_ms / max(len(count_ms), 1),
+                "share_of_step": tot_ms / ms if ms else None,
+                "peak_source": "live probe (tools/probe_peaks.py kernels): POPC lanes/s; LOP3 "
+                               f"{peaks['lop3'] / 1e12:.2f} T lane-ops/s",
+                "hbm_peak_gbs": hbm_gbs, "hbm_peak_source": hbm_src}
+
+    # end to end through the public API from pinned host CSR
+    e2e = None
+    if not args.no_e2e:
+        h2d = int(h_indptr.numel() * 8 + h_indices.numel() * 4)
+        W = dic.bits.words_for(cfg.m)
+        d2h = int(len(ref.frequent) * (W * 8 + 4 + 8) + 4 * 8)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            dbe = dic.BitDatabase.from_csr(h_indptr.cuda(non_blocking=True), h_indices.cuda(non_blocking=True),
+                                           cfg.m)
+            out = run_engine(dbe.device_tids(), n_local, cfg.m, params, plan=plan if world > 1 else None,
+                             group=group)
+            del dbe
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = f0.elapsed_time(f1) / args.steps
+        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e2e_t.item())
+        assert [(f.mask, f.support) for f in out.frequent] == [(f.mask, f.support) for f in ref.frequent]
+        e2e = {"value": tests / (e2e_ms * 1e-3), "unit": "subset-tests/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "host_wall_ms_per_step":
+                   1000 * (time.perf_counter() - t) / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, db, params)
+
+    if rank == 0:
+        s = ref.stats
+        line = {
+            "metric": "subset-tests/s (end-to-end DIC, cfg4)", "value": tests / (ms * 1e-3), "unit": "subset-tests/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 bit-sliced (int)",
+            "data": "synthetic (seeded Quest-style generator, DESIGN.md §Inputs)",
+            "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "minsup": cfg.minsup,
+                       "interval": cfg.interval, "parallelism": f"rows-sharded x{world}",
+                       "l2": "inputs larger than L2 (bit-sliced db 1.28 GB > 126 MB)",
+                       "dic_seconds": ms / 1000.0, "subset_tests_per_step": tests,
+                       "frequent_itemsets": len(ref.frequent), "stops": len(trace.stops),
+                       "db_passes": s.db_passes, "candidates_generated": s.candidates_generated,
+                       "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
+            "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, db, params) -> dict:
+    """The oracle port on the host cores, bounded sample: first pass + the
+    first checkpoint (the first stop counts every seeded pair)."""
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    rows = db.rows  # D2H of the row bitmap, outside any timed region
+    t = time.perf_counter()
+    run = O.mine(rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=cores, max_stops=1)
+    dt = time.perf_counter() - t
+    first, last = params.chunk_bounds(1)
+    tests = cfg.n * cfg.m + run.interval_counts * (last - first + 1)
+    return {"value": tests / dt, "unit": "subset-tests/s", "cores": cores, "kind": "port",
+            "sample": f"first pass + checkpoint 1 ({run.interval_counts} pairs x {last - first + 1} rows), "
+                      f"{dt:.1f} s"}
+
+
+if __name__ == "__main__":
+    main()

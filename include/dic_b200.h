@@ -26,9 +26,17 @@
  *   rows   : uint64 [n][W], W = ceil(m/64); item p of row j is bit (p & 63)
  *            of word (p >> 6) — the reference's single-word layout
  *            (bitops.py:36) extended LSW-first to W words.
- *   tids   : uint32 [m][ld], the item-major bit-sliced ("vertical") copy:
- *            bit b of tids[i*ld + g] is set iff row 32*g + b holds item i.
- *            ld is a multiple of 32 (128-byte rows), words past n are zero.
+ *   tids   : the tiled, pre-swizzled bit-sliced ("vertical") copy, uint32
+ *            words.  Rows are grouped 32 per word (group g = rows 32g..32g+31,
+ *            bit b <-> row 32g+b).  A tile holds TW groups of all m items,
+ *            TW = dic_tids_tile_groups(m) = 32 (m <= 768) or 16; item i's TW
+ *            words of tile t form one row whose 16-byte chunks are XOR-
+ *            swizzled by sw(i) = i & 7 (TW 32) or (i >> 1) & 3 (TW 16):
+ *              word(i, g) = tids[t*m*TW + i*TW + ((q ^ sw(i))*4 + e)],
+ *              t = g / TW, q = (g % TW) / 4, e = g % 4.
+ *            A tile's global image equals its shared-memory image, so one
+ *            bulk copy (TMA engine) stages it.  Rows past n read as zero;
+ *            the buffer holds dic_tids_words(n, m) words.
  *   items  : uint16 [C][k], the k ascending item ids of each candidate of a
  *            size-k bucket (candidates of one launch share k).
  */
@@ -58,6 +66,8 @@ int dic_abi_version(void);
 const char* dic_last_error(void);
 /* Number of SMs of the current device (for grid sizing by callers).       */
 int dic_device_sm_count(void);
+/* Number of kernels this library has launched in the process (monotonic).  */
+int64_t dic_launch_count(void);
 
 /* Encoder: CSR item lists -> row bitmap ---------------------------------
  * Replaces encode_transaction (bitops.py:24-37) applied per row, i.e.
@@ -75,18 +85,19 @@ int dic_device_sm_count(void);
 int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int64_t n,
                    int32_t m, uint64_t* rows, int64_t* status, void* stream);
 
-/* Row bitmap -> item-major bit-sliced copy (tids, layout above).
- * tids must hold m*ld words, ld >= ceil(n/32) and ld % 32 == 0.          */
+/* Row bitmap -> tiled bit-sliced copy (tids, layout above); every word of
+ * the dic_tids_words(n, m) buffer is written.                             */
 int dic_rows_to_tids(const uint64_t* rows, int64_t n, int32_t m,
-                     uint32_t* tids, int64_t ld, void* stream);
-/* Helper: the ld dic_rows_to_tids expects for n rows (host function).     */
-int64_t dic_tids_ld(int64_t n);
+                     uint32_t* tids, void* stream);
+/* Layout helpers (host functions).                                         */
+int64_t dic_tids_words(int64_t n, int32_t m);
+int dic_tids_tile_groups(int32_t m);
 
 /* First pass: per-item supports -----------------------------------------
  * Replaces first_pass's singleton counting (engine.py:132-154): for every
  * item i < m, counts[i] += #{ j in [first, last] : row j holds i }.
  * counts is ACCUMULATED into (int64), so multi-GPU shards can sum locally. */
-int dic_item_support(const uint32_t* tids, int64_t ld, int32_t m,
+int dic_item_support(const uint32_t* tids, int64_t n, int32_t m,
                      int64_t first, int64_t last, int64_t* counts,
                      void* stream);
 
@@ -99,7 +110,7 @@ int dic_item_support(const uint32_t* tids, int64_t ld, int32_t m,
  * raises ValueError; this entry returns DIC_EINVAL on violation).
  * Candidates are one size bucket: items[c*k .. c*k+k-1], 1 <= k <= m.
  * support_inc is accumulated into (uint64 counts).                         */
-int dic_count_support(const uint32_t* tids, int64_t ld, int32_t m,
+int dic_count_support(const uint32_t* tids, int64_t n, int32_t m,
                       int64_t first, int64_t last,
                       const uint16_t* items, int32_t k, int64_t C,
                       uint64_t* support_inc, void* stream);
@@ -148,10 +159,10 @@ typedef struct dic_stop_status {
     int64_t records;          /* itemsets ever created (|known|)                 */
 } dic_stop_status;
 
-/* tids/ld/n_local: this rank's bit-sliced rows (owned by the caller, must
+/* tids/n_local: this rank's bit-sliced rows (owned by the caller, must
  * outlive the engine).  need = ceil(minsup*n) (params.py:17-19),
  * interval = M, stop_max = ceil(n/M) over the GLOBAL n.                   */
-int dic_engine_create(const uint32_t* tids, int64_t ld, int64_t n_local,
+int dic_engine_create(const uint32_t* tids, int64_t n_local,
                       int32_t m, int64_t need, int64_t interval,
                       int64_t stop_max, int32_t prune_bound, void* stream,
                       dic_engine** out);

@@ -36,14 +36,16 @@ SIGNATURES: dict[str, tuple] = {
     "dic_abi_version": (C.c_int, []),
     "dic_last_error": (C.c_char_p, []),
     "dic_device_sm_count": (C.c_int, []),
+    "dic_launch_count": (i64, []),
     "dic_encode_csr": (C.c_int, [vp, vp, i64, i32, vp, vp, vp]),
-    "dic_rows_to_tids": (C.c_int, [vp, i64, i32, vp, i64, vp]),
-    "dic_tids_ld": (i64, [i64]),
+    "dic_rows_to_tids": (C.c_int, [vp, i64, i32, vp, vp]),
+    "dic_tids_words": (i64, [i64, i32]),
+    "dic_tids_tile_groups": (C.c_int, [i32]),
     "dic_item_support": (C.c_int, [vp, i64, i32, i64, i64, vp, vp]),
     "dic_count_support": (C.c_int, [vp, i64, i32, i64, i64, vp, i32, i64, vp, vp]),
     "dic_count_support_rows": (C.c_int, [vp, i32, i64, i64, vp, i64, vp, vp]),
     "dic_candidate_admission": (C.c_int, [vp, i64, vp, i64, i32, vp, i64, vp, i64, vp, vp]),
-    "dic_engine_create": (C.c_int, [vp, i64, i64, i32, i64, i64, i64, i32, vp, P(vp)]),
+    "dic_engine_create": (C.c_int, [vp, i64, i32, i64, i64, i64, i32, vp, P(vp)]),
     "dic_engine_destroy": (C.c_int, [vp]),
     "dic_engine_item_counts": (C.c_int, [vp, vp]),
     "dic_engine_seed": (C.c_int, [vp, vp, P(i64), P(i64)]),

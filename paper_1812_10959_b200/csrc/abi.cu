@@ -8,6 +8,9 @@
 namespace dic {
 
 static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void note_launch() { __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED); }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -119,6 +122,8 @@ extern "C" const char* dic_last_error(void) { return g_err; }
 
 extern "C" int dic_device_sm_count(void) { return sm_count(); }
 
+extern "C" int64_t dic_launch_count(void) { return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 extern "C" int dic_candidate_admission(const uint64_t* src_masks, int64_t S, const int32_t* level1, int64_t L,
                                        int32_t W, const uint64_t* known_masks, int64_t K,
                                        const uint64_t* box_masks, int64_t B, uint8_t* admit, void* stream) {
@@ -130,16 +135,16 @@ extern "C" int dic_candidate_admission(const uint64_t* src_masks, int64_t S, con
     int32_t *kht = nullptr, *bht = nullptr;
     DIC_CUDA(cudaMallocAsync((void**)&kht, kc * sizeof(int32_t), s));
     DIC_CUDA(cudaMallocAsync((void**)&bht, bc * sizeof(int32_t), s));
-    set_clear_kernel<<<(unsigned)std::min<int64_t>((kc + 255) / 256, 4096), 256, 0, s>>>(kht, kc);
-    set_clear_kernel<<<(unsigned)std::min<int64_t>((bc + 255) / 256, 4096), 256, 0, s>>>(bht, bc);
+    set_clear_kernel<<<(unsigned)std::min<int64_t>((kc + 255) / 256, 4096), 256, 0, s>>>(kht, kc); ::dic::note_launch();
+    set_clear_kernel<<<(unsigned)std::min<int64_t>((bc + 255) / 256, 4096), 256, 0, s>>>(bht, bc); ::dic::note_launch();
     auto* km = reinterpret_cast<const unsigned long long*>(known_masks);
     auto* bm = reinterpret_cast<const unsigned long long*>(box_masks);
-    if (K > 0) set_insert_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(kht, kc - 1, km, K, W);
-    if (B > 0) set_insert_kernel<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(bht, bc - 1, bm, B, W);
+    if (K > 0) set_insert_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(kht, kc - 1, km, K, W); ::dic::note_launch();
+    if (B > 0) set_insert_kernel<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(bht, bc - 1, bm, B, W); ::dic::note_launch();
     int64_t total = S * L;
     admission_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
         reinterpret_cast<const unsigned long long*>(src_masks), S, level1, L, W, kht, kc - 1, km, bht, bc - 1, bm,
-        admit);
+        admit); ::dic::note_launch();
     DIC_CHECK_LAUNCH("admission_kernel");
     DIC_CUDA(cudaFreeAsync(kht, s));
     DIC_CUDA(cudaFreeAsync(bht, s));

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -24,6 +25,8 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// Count of kernels this library launched (dic_launch_count()).
+void note_launch();
 
 #define DIC_CHECK_LAUNCH(what)                                   \
     do {                                                         \
@@ -69,6 +72,29 @@ __device__ __forceinline__ uint32_t group_mask(const ChunkGeom& c, int64_t g) {
     if (g == c.g_first) mk &= c.first_mask;
     if (g == c.g_last) mk &= c.last_mask;
     return mk;
+}
+
+// ----------------------------------------------------------------------------
+// Tiled, padded bit-sliced layout ("tids"; include/dic_b200.h).  A tile holds
+// TW row-groups (TW*32 rows) of all m items: item i's TW words form one row,
+// padded by 4 zero words, so the row stride RW = TW + 4 words is 4 mod 8
+// banks-of-16-bytes... i.e. 16-byte chunk q of item i sits in bank group
+// (i * RW/4 + q) mod 8 with RW/4 odd: 8 lanes reading the same chunk of 8
+// items that differ mod 8 hit 8 different bank groups, and every chunk
+// address is a compile-time offset from the row base.  The tile's global
+// image equals its shared-memory image, so one bulk copy stages it.
+__host__ __device__ inline int tile_groups(int m) { return m <= 768 ? 32 : 16; }
+__host__ __device__ inline int row_words(int TW) { return TW + 4; }
+__host__ __device__ inline int64_t tile_count(int64_t n, int m) {
+    int64_t groups = (n + 31) / 32;
+    int TW = tile_groups(m);
+    return (groups + TW - 1) / TW;
+}
+__host__ __device__ inline int64_t tile_words(int m) { return (int64_t)m * row_words(tile_groups(m)); }
+// uint32 index of (item, group)
+__host__ __device__ inline int64_t tids_index(int m, int TW, uint32_t item, int64_t g) {
+    int64_t t = g / TW;
+    return t * (int64_t)m * row_words(TW) + (int64_t)item * row_words(TW) + (g - t * TW);
 }
 
 // 64-bit mixer (SplitMix64 finalizer, the constants of datasets.py:44-53's

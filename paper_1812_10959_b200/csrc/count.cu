@@ -6,175 +6,282 @@
 //                           chunk, on the bit-sliced layout
 //   dic_count_support_rows  the literal (T & I) == I form on the row bitmap
 //
-// Design: the reference scans the chunk once PER
-// candidate with three NumPy passes.  Here a CTA stages one tile of the chunk
-// — 32 row-groups (1024 rows) x all m items, 128 B per item — in shared
-// memory ONCE, then every thread walks its candidates over the tile:
-//   count += popc(AND_{i in I} tile[i][g])      for the 32 groups g
-// i.e. (k-1) ANDs + 1 POPC per 32 rows instead of ~2W LOP3s per row.  Rows
-// are XOR-swizzled in 16-byte chunks (chunk' = chunk ^ (item & 7)) so the
-// LDS.128 of 8 lanes touching 8 different items hit 8 different bank groups.
+// Design.  The reference scans the chunk once PER
+// candidate with three NumPy passes.  Here the candidates are stationary
+// and the chunk streams past them, like the B operand of a GEMM:
+//   * a CTA owns a block of 512*R candidates of one size k (R per thread,
+//     their shared-memory row offsets and counters live in registers) and a
+//     range of tiles of the chunk;
+//   * tiles (TW row-groups x all m items, stored in global memory already in
+//     their swizzled shared-memory image) arrive by ONE cp.async.bulk each
+//     (TMA engine, mbarrier completion), double-buffered so the next tile
+//     lands while the current one is counted;
+//   * per 32 rows a candidate costs (k-1) ANDs + 1 POPC (LDS.128 brings 4
+//     words of a row; 8 lanes on 8 different items hit 8 bank groups);
+//   * one atomic per (candidate, CTA) at the end instead of one per tile.
 #include "common.cuh"
 
 namespace dic {
 
-constexpr int kCountThreads = 256;
-
 // ---------------------------------------------------------------------------
-// item support
+// PTX helpers: mbarrier + bulk async copy (TMA engine)
 // ---------------------------------------------------------------------------
-// grid = (m, splits).  Each CTA sums popcounts of one item's words over a
-// slice of the chunk's groups with 128-bit loads; edge groups are masked.
-__global__ void __launch_bounds__(256) item_support_kernel(
-    const uint32_t* __restrict__ tids, int64_t ld, ChunkGeom geom, int64_t groups_per_cta,
-    unsigned long long* __restrict__ counts) {
-    const int item = blockIdx.x;
-    const uint32_t* col = tids + (int64_t)item * ld;
-    int64_t gb = (geom.g_first & ~3LL) + (int64_t)blockIdx.y * groups_per_cta;
-    int64_t ge = min(gb + groups_per_cta, geom.g_last + 1);
-    unsigned long long acc = 0;
-    for (int64_t g = gb + 4 * threadIdx.x; g < ge; g += 4 * blockDim.x) {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(col + g));
-        acc += __popc(v.x & group_mask(geom, g)) + __popc(v.y & group_mask(geom, g + 1)) +
-               __popc(v.z & group_mask(geom, g + 2)) + __popc(v.w & group_mask(geom, g + 3));
-    }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
-    __shared__ unsigned long long part[8];
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
-        if (t) atomicAdd(counts + item, t);
-    }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
-
-// ---------------------------------------------------------------------------
-// bit-sliced support count
-// ---------------------------------------------------------------------------
-// Byte offset of item's 128-byte row in plane 0 with its swizzle folded in;
-// logical chunk q of the row is at (off ^ (q << 4)).
-__device__ __forceinline__ uint32_t row_off(uint32_t item) {
-    return (item << 7) | ((item & 7u) << 4);
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-
-// Stage tile groups [gbase, gbase + 32*P) of all m items into shared memory,
-// zeroing everything outside the chunk.  gbase is a multiple of 32 and
-// ld a multiple of 32, so every 16-byte load is aligned and in bounds.
-__device__ __forceinline__ void stage_tile(uint8_t* smem, const uint32_t* __restrict__ tids,
-                                           int64_t ld, int m, int P, int64_t gbase,
-                                           const ChunkGeom& geom) {
-    const int per_plane = m * 8;
-    const int total = P * per_plane;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int p = idx / per_plane;
-        const int rem = idx - p * per_plane;
-        const int i = rem >> 3, q = rem & 7;
-        const int64_t g = gbase + p * 32 + q * 4;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (g <= geom.g_last && g + 3 >= geom.g_first) {
-            v = __ldg(reinterpret_cast<const uint4*>(tids + (int64_t)i * ld + g));
-            v.x &= group_mask(geom, g);
-            v.y &= group_mask(geom, g + 1);
-            v.z &= group_mask(geom, g + 2);
-            v.w &= group_mask(geom, g + 3);
-        }
-        *reinterpret_cast<uint4*>(smem + (size_t)p * m * 128 + (row_off((uint32_t)i) ^ (q << 4))) = v;
-    }
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ uint32_t popc4(uint4 v) {
     return __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
 }
-
 __device__ __forceinline__ uint4 and4(uint4 a, uint4 b) {
     return make_uint4(a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w);
 }
 
-template <int K>
-__global__ void __launch_bounds__(kCountThreads) count_tile_kernel(
-    const uint32_t* __restrict__ tids, int64_t ld, int m, int P, ChunkGeom geom, int64_t g0,
-    const uint16_t* __restrict__ items, int kdyn, int64_t C, int64_t cands_per_cta,
-    unsigned long long* __restrict__ out) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int64_t gbase = g0 + (int64_t)blockIdx.x * P * 32;
-    stage_tile(smem, tids, ld, m, P, gbase, geom);
-    __syncthreads();
-
-    const int64_t cbeg = (int64_t)blockIdx.y * cands_per_cta;
-    const int64_t cend = min(C, cbeg + cands_per_cta);
-    const uint32_t plane_bytes = (uint32_t)m * 128u;
-    const int k = K > 0 ? K : kdyn;
-    for (int64_t c = cbeg + threadIdx.x; c < cend; c += blockDim.x) {
-        uint32_t cnt = 0;
-        if constexpr (K > 0) {
-            uint32_t off[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) off[j] = row_off(__ldg(items + c * K + j));
-            for (int p = 0; p < P; ++p) {
-                const uint8_t* base = smem + (size_t)p * plane_bytes;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    uint4 a = *reinterpret_cast<const uint4*>(base + (off[0] ^ (q << 4)));
-#pragma unroll
-                    for (int j = 1; j < K; ++j)
-                        a = and4(a, *reinterpret_cast<const uint4*>(base + (off[j] ^ (q << 4))));
-                    cnt += popc4(a);
+// ---------------------------------------------------------------------------
+// item support (first pass)
+// ---------------------------------------------------------------------------
+// grid.x = tile splits; thread = item (strided); each thread sums its item
+// row over the split's tiles (rows of adjacent items are adjacent in memory).
+__global__ void __launch_bounds__(256) item_support_kernel(const uint32_t* __restrict__ tids, int m, int TW,
+                                                           ChunkGeom geom, int64_t t_first, int64_t t_last,
+                                                           unsigned long long* __restrict__ counts) {
+    const int64_t nt = t_last - t_first + 1;
+    const int64_t ta = t_first + nt * blockIdx.x / gridDim.x;
+    const int64_t tb = t_first + nt * (blockIdx.x + 1) / gridDim.x;
+    const int RW = row_words(TW);
+    const int64_t tw_words = (int64_t)m * RW;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        unsigned long long acc = 0;
+        for (int64_t t = ta; t < tb; ++t) {
+            const uint4* row = reinterpret_cast<const uint4*>(tids + t * tw_words + (int64_t)i * RW);
+            const bool edge = (t * TW <= geom.g_first) || (t * TW + TW - 1 >= geom.g_last);
+            for (int q = 0; q < TW / 4; ++q) {
+                uint4 v = __ldg(row + q);
+                if (edge) {
+                    int64_t g = t * TW + (int64_t)(q * 4);
+                    v.x &= group_mask(geom, g);
+                    v.y &= group_mask(geom, g + 1);
+                    v.z &= group_mask(geom, g + 2);
+                    v.w &= group_mask(geom, g + 3);
                 }
-            }
-        } else {
-            // generic size: item offsets re-read per chunk (L1-resident)
-            const uint16_t* it = items + c * (int64_t)k;
-            for (int p = 0; p < P; ++p) {
-                const uint8_t* base = smem + (size_t)p * plane_bytes;
-                for (int q = 0; q < 8; ++q) {
-                    uint4 a = make_uint4(~0u, ~0u, ~0u, ~0u);
-                    for (int j = 0; j < k; ++j)
-                        a = and4(a, *reinterpret_cast<const uint4*>(base + (row_off(__ldg(it + j)) ^ (q << 4))));
-                    cnt += popc4(a);
-                }
+                acc += popc4(v);
             }
         }
-        if (cnt) atomicAdd(out + c, (unsigned long long)cnt);
+        if (acc) atomicAdd(counts + i, acc);
     }
 }
 
-// Fallback for universes too wide to stage (m * 128 B > shared memory):
-// every thread reads the tids words straight from global memory / L1.
-__global__ void __launch_bounds__(256) count_global_kernel(
-    const uint32_t* __restrict__ tids, int64_t ld, ChunkGeom geom, int64_t g0, int64_t ngb,
-    const uint16_t* __restrict__ items, int k, int64_t C, unsigned long long* __restrict__ out) {
-    // work item = (candidate, block of 32 groups)
-    int64_t total = C * ngb;
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        int64_t c = w / ngb, b = w - c * ngb;
-        int64_t gb = g0 + b * 32;
-        const uint16_t* it = items + c * (int64_t)k;
-        uint32_t cnt = 0;
-        for (int q = 0; q < 8; ++q) {
-            int64_t g = gb + q * 4;
-            if (g > geom.g_last || g + 3 < geom.g_first) continue;
-            uint4 a = make_uint4(group_mask(geom, g), group_mask(geom, g + 1),
-                                 group_mask(geom, g + 2), group_mask(geom, g + 3));
-            for (int j = 0; j < k; ++j)
-                a = and4(a, __ldg(reinterpret_cast<const uint4*>(tids + (int64_t)__ldg(it + j) * ld + g)));
-            cnt += popc4(a);
-        }
-        if (cnt) atomicAdd(out + c, (unsigned long long)cnt);
-    }
-}
+// ---------------------------------------------------------------------------
+// the streaming support count
+// ---------------------------------------------------------------------------
+constexpr int kStreamThreads = 512;
+constexpr int kMaxBuckets = 16;
 
-// Launch geometry shared by the API entry and the engine.
-struct CountPlan {
-    int P = 1;
-    int64_t g0 = 0, tiles = 0, csplit = 1, cands_per_cta = 0;
-    size_t smem = 0;
-    bool staged = true;
+struct BucketDesc {
+    const uint16_t* items;    // [C][k]
+    unsigned long long* out;  // [C], accumulated into
+    int64_t C;
+    int32_t k;
+    int32_t blocks;  // candidate blocks of this bucket (grid.y slices)
 };
 
-static int g_max_smem = -1;
+struct StreamArgs {
+    const uint32_t* tids;
+    int32_t m, TW;
+    uint32_t tile_bytes;
+    int64_t t_first, t_last;  // inclusive tile range of the chunk
+    int64_t row_splits;
+    ChunkGeom geom;
+    int32_t nb;
+    BucketDesc b[kMaxBuckets];
+};
 
+// candidates per thread: as many as the register budget allows for size k
+__host__ __device__ constexpr int regs_per_thread(int K) {
+    return K == 0 ? 2 : (K <= 2 ? 16 : (K <= 4 ? 8 : (K <= 6 ? 5 : 4)));
+}
+
+template <int K, int TW>
+__device__ __forceinline__ void stream_body(const StreamArgs& a, const BucketDesc& B, int64_t blk, int64_t t0,
+                                            int64_t t1, uint8_t* smem) {
+    constexpr int R = regs_per_thread(K);
+    constexpr int KK = K > 0 ? K : 1;
+    constexpr int CH = TW / 4;  // 16-byte chunks per item row
+    constexpr int RB = (TW + 4) * 4;  // row stride in bytes
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* bufs = smem + 128;
+    const uint32_t tb = a.tile_bytes;
+    const int64_t cbase = blk * (int64_t)kStreamThreads * R;
+    const int k = K > 0 ? K : B.k;
+
+    uint32_t off[R][KK];
+    uint32_t cnt[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
+        int64_t cc = c < B.C ? c : B.C - 1;
+        cnt[r] = 0;
+        if constexpr (K > 0) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                off[r][j] = (uint32_t)__ldg(B.items + cc * K + j) * RB;
+            }
+        } else {
+            off[r][0] = (uint32_t)cc;
+        }
+    }
+
+    for (int64_t t = t0; t < t1; ++t) {
+        const int s = (int)((t - t0) & 1);
+        mbar_wait(&bar[s], (uint32_t)(((t - t0) >> 1) & 1));
+        uint8_t* base = bufs + (size_t)s * tb;
+        // tiles holding a chunk edge: zero the rows outside [first, last]
+        if (t * TW <= a.geom.g_first || t * TW + TW - 1 >= a.geom.g_last) {
+            uint32_t* w = reinterpret_cast<uint32_t*>(base);
+            for (int idx = threadIdx.x; idx < a.m * (TW + 4); idx += kStreamThreads) {
+                int item = idx / (TW + 4), slot = idx - item * (TW + 4);
+                if (slot < TW) w[idx] &= group_mask(a.geom, t * TW + slot);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if constexpr (K > 0) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    uint4 v = *reinterpret_cast<const uint4*>(base + off[r][0] + q * 16);
+#pragma unroll
+                    for (int j = 1; j < K; ++j)
+                        v = and4(v, *reinterpret_cast<const uint4*>(base + off[r][j] + q * 16));
+                    cnt[r] += popc4(v);
+                }
+            } else {
+                const uint16_t* it = B.items + (int64_t)off[r][0] * k;
+                for (int q = 0; q < CH; ++q) {
+                    uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    for (int j = 0; j < k; ++j) {
+                        uint32_t o = (uint32_t)__ldg(it + j) * RB;
+                        v = and4(v, *reinterpret_cast<const uint4*>(base + o + q * 16));
+                    }
+                    cnt[r] += popc4(v);
+                }
+            }
+        }
+        __syncthreads();  // buffer s fully consumed
+        if (threadIdx.x == 0 && t + 2 < t1) {
+            fence_proxy_async();
+            mbar_expect_tx(&bar[s], tb);
+            bulk_g2s(base, a.tids + (t + 2) * (int64_t)(tb / 4), tb, &bar[s]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
+        if (c < B.C && cnt[r]) atomicAdd(B.out + c, (unsigned long long)cnt[r]);
+    }
+}
+
+template <int TW>
+__global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const __grid_constant__ StreamArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    int64_t blk = blockIdx.y;
+    int j = 0;
+    while (j + 1 < a.nb && blk >= a.b[j].blocks) {
+        blk -= a.b[j].blocks;
+        ++j;
+    }
+    const BucketDesc& B = a.b[j];
+    const int64_t nt = a.t_last - a.t_first + 1;
+    const int64_t t0 = a.t_first + nt * blockIdx.x / a.row_splits;
+    const int64_t t1 = a.t_first + nt * (blockIdx.x + 1) / a.row_splits;
+    if (t0 >= t1) return;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        for (int s = 0; s < 2 && t0 + s < t1; ++s) {
+            mbar_expect_tx(&bar[s], a.tile_bytes);
+            bulk_g2s(smem + 128 + (size_t)s * a.tile_bytes, a.tids + (t0 + s) * (int64_t)(a.tile_bytes / 4),
+                     a.tile_bytes, &bar[s]);
+        }
+    }
+    __syncthreads();
+    switch (B.k) {
+        case 1: stream_body<1, TW>(a, B, blk, t0, t1, smem); break;
+        case 2: stream_body<2, TW>(a, B, blk, t0, t1, smem); break;
+        case 3: stream_body<3, TW>(a, B, blk, t0, t1, smem); break;
+        case 4: stream_body<4, TW>(a, B, blk, t0, t1, smem); break;
+        case 5: stream_body<5, TW>(a, B, blk, t0, t1, smem); break;
+        case 6: stream_body<6, TW>(a, B, blk, t0, t1, smem); break;
+        case 7: stream_body<7, TW>(a, B, blk, t0, t1, smem); break;
+        case 8: stream_body<8, TW>(a, B, blk, t0, t1, smem); break;
+        default: stream_body<0, TW>(a, B, blk, t0, t1, smem); break;
+    }
+}
+
+// Universes too wide to double-buffer a tile (m > 1536): plain loads of the
+// same layout through L1/L2.  Work item = (candidate, tile).
+__global__ void __launch_bounds__(256) count_global_kernel(const uint32_t* __restrict__ tids, int m, int TW,
+                                                           ChunkGeom geom, int64_t t_first, int64_t nt,
+                                                           const uint16_t* __restrict__ items, int k, int64_t C,
+                                                           unsigned long long* __restrict__ out) {
+    const int64_t total = C * nt;
+    const int RW = row_words(TW);
+    const int64_t tw_words = (int64_t)m * RW;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = w / nt, t = t_first + (w - c * nt);
+        const uint16_t* it = items + c * (int64_t)k;
+        uint32_t cnt = 0;
+        for (int q = 0; q < TW / 4; ++q) {
+            int64_t g = t * TW + q * 4;
+            if (g > geom.g_last || g + 3 < geom.g_first) continue;
+            uint4 v = make_uint4(group_mask(geom, g), group_mask(geom, g + 1), group_mask(geom, g + 2),
+                                 group_mask(geom, g + 3));
+            for (int j = 0; j < k; ++j) {
+                uint32_t item = __ldg(it + j);
+                const uint4* row = reinterpret_cast<const uint4*>(tids + t * tw_words + (int64_t)item * RW);
+                v = and4(v, __ldg(row + q));
+            }
+            cnt += popc4(v);
+        }
+        if (cnt) atomicAdd(out + c, (unsigned long long)cnt);
+    }
+}
+
+static int g_max_smem = -1;
 static int max_dyn_smem() {
     if (g_max_smem < 0) {
         int dev = 0, v = 0;
@@ -185,94 +292,98 @@ static int max_dyn_smem() {
     return g_max_smem;
 }
 
-CountPlan plan_count(int m, ChunkGeom geom, int64_t C) {
-    CountPlan pl;
-    pl.g0 = geom.g_first & ~31LL;
-    const int64_t span = geom.g_last + 1 - pl.g0;  // groups from the aligned base
-    const size_t plane = (size_t)m * 128;
-    const int smax = max_dyn_smem();
-    if (plane > (size_t)smax) {
-        pl.staged = false;
-        return pl;
-    }
-    pl.P = 1;
-    pl.tiles = (span + 31) / 32;
-    pl.smem = plane;
-    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(228 * 1024) / (plane + 1024)));
-    const int64_t target = (int64_t)sm_count() * per_sm * 2;
-    int64_t cs = (target + pl.tiles - 1) / pl.tiles;
-    // keep at least ~2 candidates per thread per CTA so the staging amortises
-    const int64_t min_cpc = 2 * kCountThreads;
-    int64_t cs_max = std::max<int64_t>(1, (C + min_cpc - 1) / min_cpc);
-    cs = std::max<int64_t>(1, std::min<int64_t>(cs, cs_max));
-    cs = std::min<int64_t>(cs, 65535);
-    pl.csplit = cs;
-    pl.cands_per_cta = (C + cs - 1) / cs;
-    return pl;
-}
+struct BucketIn {
+    const uint16_t* items;
+    unsigned long long* out;
+    int64_t C;
+    int k;
+};
 
-template <int K>
-static int launch_count_tile(const CountPlan& pl, const uint32_t* tids, int64_t ld, int m,
-                             ChunkGeom geom, const uint16_t* items, int k, int64_t C,
-                             unsigned long long* out, cudaStream_t s) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        DIC_CUDA(cudaFuncSetAttribute(count_tile_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      max_dyn_smem()));
-        attr_done = true;
+// Count every bucket over rows [first, last] in as few launches as possible.
+int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                         const BucketIn* bk, int nbk, cudaStream_t s) {
+    if (last < first) return DIC_OK;
+    const int TW = tile_groups(m);
+    const ChunkGeom geom = chunk_geom(first, last);
+    const int64_t t_first = geom.g_first / TW, t_last = geom.g_last / TW;
+    const int64_t nt = t_last - t_first + 1;
+    const size_t tile_bytes = (size_t)m * row_words(TW) * 4;
+    const size_t smem = 128 + 2 * tile_bytes;
+    if (smem > (size_t)max_dyn_smem()) {
+        for (int i = 0; i < nbk; ++i) {
+            if (bk[i].C <= 0) continue;
+            int64_t total = bk[i].C * nt;
+            int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+            count_global_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+                tids, m, TW, geom, t_first, nt, bk[i].items, bk[i].k, bk[i].C, bk[i].out); ::dic::note_launch();
+            DIC_CHECK_LAUNCH("count_global_kernel");
+        }
+        return DIC_OK;
     }
-    // grid.x may exceed 2^31-1 only for absurd n; tiles is bounded by ld/32
-    dim3 grid((unsigned)pl.tiles, (unsigned)pl.csplit);
-    count_tile_kernel<K><<<grid, kCountThreads, pl.smem, s>>>(tids, ld, m, pl.P, geom, pl.g0, items, k,
-                                                             C, pl.cands_per_cta, out);
-    DIC_CHECK_LAUNCH("count_tile_kernel");
+    static bool attr32 = false, attr16 = false;
+    if (TW == 32 && !attr32) {
+        DIC_CUDA(cudaFuncSetAttribute(count_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_dyn_smem()));
+        attr32 = true;
+    }
+    if (TW == 16 && !attr16) {
+        DIC_CUDA(cudaFuncSetAttribute(count_stream_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_dyn_smem()));
+        attr16 = true;
+    }
+    int i = 0;
+    while (i < nbk) {
+        StreamArgs a;
+        memset(&a, 0, sizeof(a));
+        a.tids = tids;
+        a.m = m;
+        a.TW = TW;
+        a.tile_bytes = (uint32_t)tile_bytes;
+        a.t_first = t_first;
+        a.t_last = t_last;
+        a.geom = geom;
+        int64_t blocks = 0;
+        for (; i < nbk && a.nb < kMaxBuckets; ++i) {
+            if (bk[i].C <= 0) continue;
+            const int R = regs_per_thread(bk[i].k <= 8 ? bk[i].k : 0);
+            BucketDesc& d = a.b[a.nb++];
+            d.items = bk[i].items;
+            d.out = bk[i].out;
+            d.C = bk[i].C;
+            d.k = bk[i].k;
+            d.blocks = (int32_t)((bk[i].C + (int64_t)kStreamThreads * R - 1) / ((int64_t)kStreamThreads * R));
+            blocks += d.blocks;
+        }
+        if (a.nb == 0) break;
+        DIC_REQUIRE(blocks <= 65535, "count: %lld candidate blocks exceed one launch", (long long)blocks);
+        // about two CTAs per SM in total: one resident, one to balance the tail
+        // one CTA per SM (512 threads x 128 registers fill the register
+        // file): size the grid to one full wave when the blocks allow it
+        const int64_t target = sm_count();
+        int64_t rs = blocks >= target ? 1 : target / blocks;
+        rs = std::max<int64_t>(1, std::min<int64_t>(rs, nt));
+        a.row_splits = rs;
+        dim3 grid((unsigned)rs, (unsigned)blocks);
+        if (TW == 32)
+            count_stream_kernel<32><<<grid, kStreamThreads, smem, s>>>(a);
+        else
+            count_stream_kernel<16><<<grid, kStreamThreads, smem, s>>>(a);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("count_stream_kernel");
+    }
     return DIC_OK;
 }
 
-int count_support_launch(const uint32_t* tids, int64_t ld, int m, int64_t first, int64_t last,
-                         const uint16_t* items, int k, int64_t C, unsigned long long* out,
-                         cudaStream_t s) {
-    if (C <= 0 || last < first) return DIC_OK;
-    ChunkGeom geom = chunk_geom(first, last);
-    CountPlan pl = plan_count(m, geom, C);
-    if (!pl.staged) {
-        int64_t ngb = (geom.g_last + 1 - pl.g0 + 31) / 32;
-        int64_t total = C * ngb;
-        int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
-        count_global_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
-            tids, ld, geom, pl.g0, ngb, items, k, C, out);
-        DIC_CHECK_LAUNCH("count_global_kernel");
-        return DIC_OK;
-    }
-    switch (k) {
-        case 1: return launch_count_tile<1>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 2: return launch_count_tile<2>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 3: return launch_count_tile<3>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 4: return launch_count_tile<4>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 5: return launch_count_tile<5>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 6: return launch_count_tile<6>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 7: return launch_count_tile<7>(pl, tids, ld, m, geom, items, k, C, out, s);
-        case 8: return launch_count_tile<8>(pl, tids, ld, m, geom, items, k, C, out, s);
-        default: return launch_count_tile<0>(pl, tids, ld, m, geom, items, k, C, out, s);
-    }
-}
-
-int item_support_launch(const uint32_t* tids, int64_t ld, int m, int64_t first, int64_t last,
+int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s) {
     if (last < first) return DIC_OK;
+    const int TW = tile_groups(m);
     ChunkGeom geom = chunk_geom(first, last);
-    int64_t gb = geom.g_first & ~3LL;
-    int64_t span = geom.g_last + 1 - gb;
-    // aim for ~4 waves of 256-thread CTAs over m x splits
-    int64_t want = (int64_t)sm_count() * 8;
-    int64_t splits = std::max<int64_t>(1, (want + m - 1) / m);
-    int64_t per = (span + splits - 1) / splits;
-    per = std::max<int64_t>(per, 4 * 256);
-    per = (per + 3) & ~3LL;
-    splits = (span + per - 1) / per;
-    splits = std::min<int64_t>(std::max<int64_t>(splits, 1), 65535);
-    dim3 grid((unsigned)m, (unsigned)splits);
-    item_support_kernel<<<grid, 256, 0, s>>>(tids, ld, geom, per, counts);
+    const int64_t t_first = geom.g_first / TW, t_last = geom.g_last / TW;
+    const int64_t nt = t_last - t_first + 1;
+    int64_t splits = std::min<int64_t>(nt, (int64_t)sm_count() * 8);
+    item_support_kernel<<<(unsigned)std::max<int64_t>(splits, 1), 256, 0, s>>>(tids, m, TW, geom, t_first, t_last,
+                                                                             counts); ::dic::note_launch();
     DIC_CHECK_LAUNCH("item_support_kernel");
     return DIC_OK;
 }
@@ -291,7 +402,7 @@ __global__ void __launch_bounds__(256) count_rows_kernel(
     const unsigned long long* __restrict__ rows, int Wd, int64_t first, int64_t last,
     const unsigned long long* __restrict__ masks, int64_t C, unsigned long long* __restrict__ out) {
     constexpr int WS = W > 0 ? W : 1;
-    __shared__ unsigned long long sm_masks[kRowCands * (W > 0 ? W : 16)];
+    extern __shared__ unsigned long long sm_masks[];  // [kRowCands][Wr]
     __shared__ uint32_t sm_cnt[kRowCands];
     const int Wr = W > 0 ? W : Wd;
     const int64_t c0 = (int64_t)blockIdx.y * kRowCands;
@@ -329,36 +440,42 @@ __global__ void __launch_bounds__(256) count_rows_kernel(
 
 template <int W>
 static void launch_rows(dim3 grid, const unsigned long long* rows, int Wd, int64_t first, int64_t last,
-                        const unsigned long long* masks, int64_t C, unsigned long long* out,
-                        cudaStream_t s) {
-    count_rows_kernel<W><<<grid, 256, 0, s>>>(rows, Wd, first, last, masks, C, out);
+                        const unsigned long long* masks, int64_t C, unsigned long long* out, cudaStream_t s) {
+    count_rows_kernel<W><<<grid, 256, (size_t)kRowCands * Wd * 8, s>>>(rows, Wd, first, last, masks, C, out);
+    ::dic::note_launch();
 }
 
 }  // namespace dic
 
 using namespace dic;
 
-extern "C" int dic_item_support(const uint32_t* tids, int64_t ld, int32_t m, int64_t first,
-                                int64_t last, int64_t* counts, void* stream) {
-    DIC_REQUIRE(m >= 1 && ld % 32 == 0, "dic_item_support: bad m=%d or ld=%lld", m, (long long)ld);
-    DIC_REQUIRE(first >= 0 && (last < first || (last >> 5) < ld),
-                "dic_item_support: chunk [%lld, %lld] outside ld=%lld groups", (long long)first,
-                (long long)last, (long long)ld);
-    return item_support_launch(tids, ld, m, first, last,
-                               reinterpret_cast<unsigned long long*>(counts), as_stream(stream));
+extern "C" int64_t dic_tids_words(int64_t n, int32_t m) {
+    if (n < 1 || m < 1) return 0;
+    return tile_count(n, m) * tile_words(m);
 }
 
-extern "C" int dic_count_support(const uint32_t* tids, int64_t ld, int32_t m, int64_t first,
-                                 int64_t last, const uint16_t* items, int32_t k, int64_t C,
-                                 uint64_t* support_inc, void* stream) {
+extern "C" int dic_tids_tile_groups(int32_t m) { return m >= 1 ? tile_groups(m) : DIC_EINVAL; }
+
+extern "C" int dic_item_support(const uint32_t* tids, int64_t n, int32_t m, int64_t first, int64_t last,
+                                int64_t* counts, void* stream) {
+    DIC_REQUIRE(m >= 1 && tids && counts, "dic_item_support: bad arguments");
+    DIC_REQUIRE(0 <= first && (last < first || last < n), "chunk [%lld, %lld] outside database of %lld rows",
+                (long long)first, (long long)last, (long long)n);
+    return item_support_launch(tids, n, m, first, last, reinterpret_cast<unsigned long long*>(counts),
+                               as_stream(stream));
+}
+
+extern "C" int dic_count_support(const uint32_t* tids, int64_t n, int32_t m, int64_t first, int64_t last,
+                                 const uint16_t* items, int32_t k, int64_t C, uint64_t* support_inc,
+                                 void* stream) {
     DIC_REQUIRE(m >= 1 && m <= 65535, "dic_count_support: m=%d outside [1, 65535]", m);
     DIC_REQUIRE(k >= 1 && k <= m, "dic_count_support: k=%d outside [1, m=%d]", k, m);
-    DIC_REQUIRE(ld % 32 == 0, "dic_count_support: ld=%lld not a multiple of 32", (long long)ld);
-    DIC_REQUIRE(0 <= first && first <= last && (last >> 5) < ld,
-                "chunk [%lld, %lld] outside database", (long long)first, (long long)last);
+    DIC_REQUIRE(0 <= first && first <= last && last < n, "chunk [%lld, %lld] outside database of %lld rows",
+                (long long)first, (long long)last, (long long)n);
     DIC_REQUIRE(C >= 0, "dic_count_support: C=%lld < 0", (long long)C);
-    return count_support_launch(tids, ld, m, first, last, items, k, C,
-                                reinterpret_cast<unsigned long long*>(support_inc), as_stream(stream));
+    if (C == 0) return DIC_OK;
+    BucketIn b{items, reinterpret_cast<unsigned long long*>(support_inc), C, k};
+    return count_buckets_launch(tids, n, m, first, last, &b, 1, as_stream(stream));
 }
 
 extern "C" int dic_count_support_rows(const uint64_t* rows, int32_t W, int64_t first, int64_t last,
@@ -384,7 +501,7 @@ extern "C" int dic_count_support_rows(const uint64_t* rows, int32_t W, int64_t f
         case 8: launch_rows<8>(grid, r, W, first, last, mk, C, o, s); break;
         case 16: launch_rows<16>(grid, r, W, first, last, mk, C, o, s); break;
         default:
-            DIC_REQUIRE(W <= 16, "dic_count_support_rows: W=%d > 16 unsupported", W);
+            DIC_REQUIRE(W <= 64, "dic_count_support_rows: W=%d > 64 unsupported", W);
             launch_rows<0>(grid, r, W, first, last, mk, C, o, s);
     }
     DIC_CHECK_LAUNCH("count_rows_kernel");

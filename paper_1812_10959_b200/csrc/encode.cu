@@ -70,19 +70,22 @@ __global__ void finish_status_kernel(const int64_t* __restrict__ indptr, int64_t
     status[2] = (unsigned long long)lo;
 }
 
-// Rows -> bit-sliced copy.  A CTA owns 32 consecutive groups (1024 rows) and
-// one 64-item word column at a time: warp w transposes groups w, w+8, ...
-// with 64 ballots per group (bit b of lane l's word -> bit l of column b),
-// stages the 64 x 32 result in shared memory and writes each item's 32
-// group words as one 128-byte line.
+// Rows -> tiled bit-sliced copy.  A CTA owns one tile (TW groups = TW*32
+// rows) and one 64-item word column at a time: warp w transposes groups
+// w, w+8, ... with 64 ballots per group (bit b of lane l's word -> bit l of
+// column b), stages the 64 x TW result in shared memory and writes the 64
+// item rows of the tile (with their zero pad words) with consecutive
+// threads on consecutive words.
 __global__ void __launch_bounds__(256) rows_to_tids_kernel(
-    const unsigned long long* __restrict__ rows, int64_t n, int32_t m, int W,
-    uint32_t* __restrict__ tids, int64_t ld) {
+    const unsigned long long* __restrict__ rows, int64_t n, int32_t m, int W, int TW,
+    uint32_t* __restrict__ tids) {
     __shared__ uint32_t stage[64][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t g0 = (int64_t)blockIdx.x * 32;
+    const int64_t t = blockIdx.x;
+    const int64_t g0 = t * TW;
+    uint32_t* tile = tids + t * (int64_t)m * row_words(TW);
     for (int wb = 0; wb < W; ++wb) {
-        for (int gl = warp; gl < 32; gl += 8) {
+        for (int gl = warp; gl < TW; gl += 8) {
             int64_t r = (g0 + gl) * 32 + lane;
             unsigned long long x = r < n ? rows[r * (int64_t)W + wb] : 0ull;
             uint32_t lo_col = 0, hi_col = 0;
@@ -100,11 +103,11 @@ __global__ void __launch_bounds__(256) rows_to_tids_kernel(
             stage[32 + lane][gl] = hi_col;
         }
         __syncthreads();
-        // write out: 64 items x 32 groups; thread t -> item t/4.., 8 words
-        for (int idx = threadIdx.x; idx < 64 * 32; idx += 256) {
-            int il = idx >> 5, gl = idx & 31;
-            int item = wb * 64 + il;
-            if (item < m && g0 + gl < ld) tids[(int64_t)item * ld + g0 + gl] = stage[il][gl];
+        const int items = min(64, m - wb * 64);
+        const int RW = row_words(TW);
+        for (int idx = threadIdx.x; idx < items * RW; idx += 256) {
+            int il = idx / RW, slot = idx - il * RW;
+            tile[(int64_t)(wb * 64 + il) * RW + slot] = slot < TW ? stage[il][slot] : 0u;
         }
         __syncthreads();
     }
@@ -114,11 +117,6 @@ __global__ void __launch_bounds__(256) rows_to_tids_kernel(
 
 using namespace dic;
 
-extern "C" int64_t dic_tids_ld(int64_t n) {
-    int64_t groups = (n + 31) / 32;
-    return ((groups + 31) / 32) * 32;
-}
-
 extern "C" int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int64_t n,
                               int32_t m, uint64_t* rows, int64_t* status, void* stream) {
     DIC_REQUIRE(n >= 0 && m >= 1, "dic_encode_csr: need n >= 0 and m >= 1 (n=%lld, m=%d)",
@@ -127,34 +125,29 @@ extern "C" int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int
     cudaStream_t s = as_stream(stream);
     const int W = (m + 63) / 64;
     auto* st = reinterpret_cast<unsigned long long*>(status);
-    init_status_kernel<<<1, 1, 0, s>>>(st);
+    init_status_kernel<<<1, 1, 0, s>>>(st); ::dic::note_launch();
     if (n == 0) { DIC_CHECK_LAUNCH("init_status_kernel"); return DIC_OK; }
     DIC_CUDA(cudaMemsetAsync(rows, 0, (size_t)n * W * sizeof(uint64_t), s));
     const int T = 256;
     int64_t blocks = (n + T - 1) / T;
     encode_csr_kernel<<<(unsigned)blocks, T, 0, s>>>(indptr, indices, n, m, W,
-                                                     reinterpret_cast<unsigned long long*>(rows), st);
+                                                     reinterpret_cast<unsigned long long*>(rows), st); ::dic::note_launch();
     DIC_CHECK_LAUNCH("encode_csr_kernel");
     dedup_count_kernel<<<(unsigned)blocks, T, 0, s>>>(
-        indptr, n, W, reinterpret_cast<const unsigned long long*>(rows), st);
+        indptr, n, W, reinterpret_cast<const unsigned long long*>(rows), st); ::dic::note_launch();
     DIC_CHECK_LAUNCH("dedup_count_kernel");
-    finish_status_kernel<<<1, 1, 0, s>>>(indptr, n, st);
+    finish_status_kernel<<<1, 1, 0, s>>>(indptr, n, st); ::dic::note_launch();
     DIC_CHECK_LAUNCH("finish_status_kernel");
     return DIC_OK;
 }
 
-extern "C" int dic_rows_to_tids(const uint64_t* rows, int64_t n, int32_t m, uint32_t* tids,
-                                int64_t ld, void* stream) {
-    DIC_REQUIRE(n >= 1 && m >= 1, "dic_rows_to_tids: need n >= 1 and m >= 1");
-    DIC_REQUIRE(ld % 32 == 0 && ld * 32 >= n, "dic_rows_to_tids: ld=%lld must be a multiple of 32 covering n=%lld rows",
-                (long long)ld, (long long)n);
-    cudaStream_t s = as_stream(stream);
+extern "C" int dic_rows_to_tids(const uint64_t* rows, int64_t n, int32_t m, uint32_t* tids, void* stream) {
+    DIC_REQUIRE(n >= 1 && m >= 1 && rows && tids, "dic_rows_to_tids: need n >= 1, m >= 1 and buffers");
     const int W = (m + 63) / 64;
-    // words past n inside each item row must read as zero
-    DIC_CUDA(cudaMemsetAsync(tids, 0, (size_t)m * ld * sizeof(uint32_t), s));
-    int64_t blocks = ld / 32;
-    rows_to_tids_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-        reinterpret_cast<const unsigned long long*>(rows), n, m, W, tids, ld);
+    const int TW = tile_groups(m);
+    const int64_t tiles = tile_count(n, m);
+    rows_to_tids_kernel<<<(unsigned)tiles, 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const unsigned long long*>(rows), n, m, W, TW, tids); ::dic::note_launch();
     DIC_CHECK_LAUNCH("rows_to_tids_kernel");
     return DIC_OK;
 }

@@ -34,10 +34,15 @@
 
 namespace dic {
 
-int count_support_launch(const uint32_t* tids, int64_t ld, int m, int64_t first, int64_t last,
-                         const uint16_t* items, int k, int64_t C, unsigned long long* out,
-                         cudaStream_t s);
-int item_support_launch(const uint32_t* tids, int64_t ld, int m, int64_t first, int64_t last,
+struct BucketIn {
+    const uint16_t* items;
+    unsigned long long* out;
+    int64_t C;
+    int k;
+};
+int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                         const BucketIn* bk, int nbk, cudaStream_t s);
+int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s);
 
 enum : uint8_t { DASHED_CIRCLE = 0, DASHED_BOX = 1, SOLID_CIRCLE = 2, SOLID_BOX = 3, NIL = 4 };
@@ -372,7 +377,7 @@ struct Bucket {
 
 struct dic_engine {
     const uint32_t* tids;
-    int64_t ld, n_local;
+    int64_t n_local;
     int m, W;
     int64_t need, interval, stop_max;
     int bound;
@@ -473,9 +478,10 @@ int ensure_hash(dic_engine* e, int64_t nrec_after) {
     int rc = dalloc(&e->ht, nc, e->s);
     if (rc) return rc;
     e->hcap = nc;
-    ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc);
-    if (e->nrec > 0)
-        ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, 0, e->nrec);
+    ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc); ::dic::note_launch();
+    if (e->nrec > 0) {
+        ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, 0, e->nrec); ::dic::note_launch();
+    }
     DIC_CHECK_LAUNCH("rehash");
     return DIC_OK;
 }
@@ -540,16 +546,15 @@ int64_t total_dashed(const dic_engine* e) {
 
 }  // namespace
 
-extern "C" int dic_engine_create(const uint32_t* tids, int64_t ld, int64_t n_local, int32_t m, int64_t need,
+extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t m, int64_t need,
                                  int64_t interval, int64_t stop_max, int32_t prune_bound, void* stream,
                                  dic_engine** out) {
     DIC_REQUIRE(out, "dic_engine_create: out is null");
     DIC_REQUIRE(m >= 1 && m <= 65535, "dic_engine_create: m=%d outside [1, 65535]", m);
-    DIC_REQUIRE(n_local >= 0 && ld % 32 == 0 && ld * 32 >= n_local, "dic_engine_create: bad ld/n_local");
+    DIC_REQUIRE(n_local >= 0 && (tids || n_local == 0), "dic_engine_create: bad tids/n_local");
     DIC_REQUIRE(interval >= 1 && stop_max >= 1, "dic_engine_create: bad interval/stop_max");
     dic_engine* e = new dic_engine();
     e->tids = tids;
-    e->ld = ld;
     e->n_local = n_local;
     e->m = m;
     e->W = (m + 63) / 64;
@@ -607,7 +612,7 @@ extern "C" int dic_engine_item_counts(dic_engine* e, int64_t* counts) {
     DIC_REQUIRE(e && counts, "dic_engine_item_counts: null argument");
     DIC_CUDA(cudaMemsetAsync(counts, 0, (size_t)e->m * sizeof(int64_t), e->s));
     if (e->n_local > 0)
-        return item_support_launch(e->tids, e->ld, e->m, 0, e->n_local - 1,
+        return item_support_launch(e->tids, e->n_local, e->m, 0, e->n_local - 1,
                                    reinterpret_cast<unsigned long long*>(counts), e->s);
     return DIC_OK;
 }
@@ -628,7 +633,7 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     if ((rc = grow_records(e, m + npairs + 1024))) return rc;
     e->nrec = 0;
     if ((rc = ensure_hash(e, m + npairs))) return rc;
-    seed_singletons_kernel<<<nblk(m), 256, 0, e->s>>>(e->R, e->W, m, counts, e->need, e->stop_max);
+    seed_singletons_kernel<<<nblk(m), 256, 0, e->s>>>(e->R, e->W, m, counts, e->need, e->stop_max); ::dic::note_launch();
     DIC_CHECK_LAUNCH("seed_singletons_kernel");
     if (L > 0) DIC_CUDA(cudaMemcpyAsync(e->level1, l1.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, e->s));
     e->nL1 = L;
@@ -642,14 +647,14 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         if ((rc = dalloc(&d_rs, L, e->s))) return rc;
         DIC_CUDA(cudaMemcpyAsync(d_rs, rs.data(), L * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
         seed_pairs_kernel<<<nblk(npairs), 256, 0, e->s>>>(e->R, e->W, e->level1, L, d_rs, npairs, m,
-                                                          e->buckets[2].rec, e->buckets[2].items);
+                                                          e->buckets[2].rec, e->buckets[2].items); ::dic::note_launch();
         DIC_CHECK_LAUNCH("seed_pairs_kernel");
         dfree(d_rs, e->s);
         e->buckets[2].n = npairs;
         if (changed && (rc = sync_bucket_tables(e))) return rc;
     }
     e->nrec = m + npairs;
-    ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec);
+    ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec); ::dic::note_launch();
     DIC_CHECK_LAUNCH("ht_insert_records_kernel");
     // device mirror of bucket sizes
     std::vector<unsigned long long> bn(m + 2, 0);
@@ -680,15 +685,16 @@ extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
     e->delta_off.assign(e->buckets.size(), 0);
     if (tot > 0) DIC_CUDA(cudaMemsetAsync(e->delta, 0, tot * sizeof(unsigned long long), e->s));
     int64_t off = 0;
+    std::vector<BucketIn> bk;
     for (size_t k = 0; k < e->buckets.size(); ++k) {
         const Bucket& b = e->buckets[k];
         e->delta_off[k] = off;
-        if (b.n > 0 && llast >= lfirst) {
-            int rc = count_support_launch(e->tids, e->ld, e->m, lfirst, llast, b.items, (int)k, b.n,
-                                          e->delta + off, e->s);
-            if (rc) return rc;
-        }
+        if (b.n > 0) bk.push_back(BucketIn{b.items, e->delta + off, b.n, (int)k});
         off += b.n;
+    }
+    if (!bk.empty() && llast >= lfirst) {
+        int rc = count_buckets_launch(e->tids, e->n_local, e->m, lfirst, llast, bk.data(), (int)bk.size(), e->s);
+        if (rc) return rc;
     }
     e->counted = true;
     return DIC_OK;
@@ -724,7 +730,7 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
         int64_t off = e->delta_off[k];
         apply_prune_finalize_kernel<<<nblk(b.n), 256, 0, e->s>>>(
             b.rec, b.n, e->delta + off, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
-            e->keep + off, e->ctr, e->d_removed + k);
+            e->keep + off, e->ctr, e->d_removed + k); ::dic::note_launch();
     }
     DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
     std::vector<unsigned long long> removed(e->buckets.size(), 0);
@@ -749,7 +755,7 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
         uint16_t* nitems = nullptr;
         if ((rc = dalloc(&nrec_arr, b.cap, e->s)) || (rc = dalloc(&nitems, b.cap * (int64_t)k, e->s))) return rc;
         compact_bucket_kernel<<<nblk(b.n), 256, 0, e->s>>>(b.n, (int)k, e->keep + off, e->pos + off, b.rec,
-                                                            b.items, nrec_arr, nitems);
+                                                            b.items, nrec_arr, nitems); ::dic::note_launch();
         DIC_CHECK_LAUNCH("compact_bucket_kernel");
         dfree(b.rec, e->s);
         dfree(b.items, e->s);
@@ -776,7 +782,7 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
             DIC_CUDA(cudaMemsetAsync(e->d_adm, 0, (e->m + 2) * sizeof(unsigned long long), e->s));
             eval_candidates_kernel<<<nblk(pairs), 256, 0, e->s>>>(
                 e->frontier, nfront, e->level1, e->nL1, e->W, e->R, e->ht, (uint64_t)e->hcap - 1, e->tmp_mask,
-                e->tmp_hash, e->tmp_size, e->tmp_cap, e->ctr, e->d_adm);
+                e->tmp_hash, e->tmp_size, e->tmp_cap, e->ctr, e->d_adm); ::dic::note_launch();
             DIC_CHECK_LAUNCH("eval_candidates_kernel");
             if ((rc = read_counters(e))) return rc;
             if ((int64_t)e->hctr->nadm <= e->tmp_cap) break;
@@ -805,11 +811,11 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
             unsigned long long nrec_now = (unsigned long long)e->nrec;
             DIC_CUDA(cudaMemcpyAsync(&e->ctr->nrec, &nrec_now, sizeof(nrec_now), cudaMemcpyHostToDevice, e->s));
             insert_candidates_kernel<<<nblk(na), 256, 0, e->s>>>(na, e->W, e->tmp_mask, e->tmp_hash, e->R, e->ht,
-                                                                 (uint64_t)e->hcap - 1, e->tmp_slot);
+                                                                 (uint64_t)e->hcap - 1, e->tmp_slot); ::dic::note_launch();
             DIC_CHECK_LAUNCH("insert_candidates_kernel");
             commit_candidates_kernel<<<nblk(na), 256, 0, e->s>>>(na, e->W, e->tmp_mask, e->tmp_hash, e->tmp_size,
                                                                  e->tmp_slot, e->R, e->ht, e->ctr, e->d_brec,
-                                                                 e->d_bitems, e->d_bn);
+                                                                 e->d_bitems, e->d_bn); ::dic::note_launch();
             DIC_CHECK_LAUNCH("commit_candidates_kernel");
             DIC_CUDA(cudaMemcpyAsync(bn.data(), e->d_bn, bn.size() * sizeof(unsigned long long),
                                      cudaMemcpyDeviceToHost, e->s));
@@ -833,7 +839,7 @@ extern "C" int dic_engine_num_frequent(dic_engine* e, int64_t* F) {
     int rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s);
     if (rc) return rc;
     DIC_CUDA(cudaMemsetAsync(&e->ctr->pad, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad);
+    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad); ::dic::note_launch();
     DIC_CHECK_LAUNCH("collect_frequent_kernel");
     if ((rc = read_counters(e))) return rc;
     dfree(ids, e->s);
@@ -853,14 +859,14 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
         (rc = dalloc(&dsz, std::max<int64_t>(F, 1), e->s)) || (rc = dalloc(&dsu, std::max<int64_t>(F, 1), e->s)))
         return rc;
     DIC_CUDA(cudaMemsetAsync(&e->ctr->pad, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad);
+    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad); ::dic::note_launch();
     if ((rc = read_counters(e))) return rc;
     if ((int64_t)e->hctr->pad != F) {
         set_error("dic_engine_frequent: F=%lld but %llu frequent records", (long long)F, e->hctr->pad);
         return DIC_EINVAL;
     }
     if (F > 0) {
-        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->W, ids, F, dm, dsz, dsu);
+        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->W, ids, F, dm, dsz, dsu); ::dic::note_launch();
         DIC_CHECK_LAUNCH("gather_frequent_kernel");
         DIC_CUDA(cudaMemcpyAsync(masks_host, dm, F * e->W * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s));
         DIC_CUDA(cudaMemcpyAsync(sizes_host, dsz, F * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));

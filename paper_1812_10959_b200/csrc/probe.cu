@@ -71,9 +71,9 @@ extern "C" int dic_probe_int_pipe(int op, int blocks, int threads, int64_t iters
     DIC_CUDA(cudaEventCreate(&e1));
     DIC_CUDA(cudaEventRecord(e0, s));
     switch (op) {
-        case 0: int_pipe_kernel<0><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); break;
-        case 1: int_pipe_kernel<1><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); break;
-        default: int_pipe_kernel<2><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); break;
+        case 0: int_pipe_kernel<0><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); ::dic::note_launch(); break;
+        case 1: int_pipe_kernel<1><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); ::dic::note_launch(); break;
+        default: int_pipe_kernel<2><<<blocks, threads, 0, s>>>(sink, iters, 0x1234567u); ::dic::note_launch(); break;
     }
     DIC_CHECK_LAUNCH("int_pipe_kernel");
     DIC_CUDA(cudaEventRecord(e1, s));
@@ -97,7 +97,7 @@ extern "C" int dic_synth_bernoulli_rows(int64_t n, int32_t m, double p, uint64_t
     int64_t total = n * W;
     int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
     bernoulli_rows_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-        reinterpret_cast<unsigned long long*>(rows), n, W, m, thresh, key);
+        reinterpret_cast<unsigned long long*>(rows), n, W, m, thresh, key); ::dic::note_launch();
     DIC_CHECK_LAUNCH("bernoulli_rows_kernel");
     return DIC_OK;
 }

@@ -34,8 +34,12 @@ def words_for(m: int) -> int:
     return (m + 63) // 64
 
 
-def tids_ld(n: int) -> int:
-    return int(_abi.load().dic_tids_ld(n))
+def tids_words(n: int, m: int) -> int:
+    return int(_abi.load().dic_tids_words(n, m))
+
+
+def tile_groups(m: int) -> int:
+    return int(_abi.load().dic_tids_tile_groups(m))
 
 
 def encode_csr(indptr: torch.Tensor, indices: torch.Tensor, n: int, m: int) -> tuple[torch.Tensor, torch.Tensor]:
@@ -50,29 +54,29 @@ def encode_csr(indptr: torch.Tensor, indices: torch.Tensor, n: int, m: int) -> t
     return rows[:n], status
 
 
-def rows_to_tids(rows: torch.Tensor, n: int, m: int) -> tuple[torch.Tensor, int]:
-    ld = tids_ld(n)
-    tids = torch.empty((m, ld), dtype=torch.int32, device=rows.device)
-    _abi.call("dic_rows_to_tids", _ptr(rows), n, m, _ptr(tids), ld, _stream())
-    return tids, ld
+def rows_to_tids(rows: torch.Tensor, n: int, m: int) -> torch.Tensor:
+    """Row bitmap -> the tiled bit-sliced layout (int32 words, see dic_b200.h)."""
+    tids = torch.empty(max(tids_words(n, m), 1), dtype=torch.int32, device=rows.device)
+    _abi.call("dic_rows_to_tids", _ptr(rows), n, m, _ptr(tids), _stream())
+    return tids
 
 
-def item_support(tids: torch.Tensor, ld: int, m: int, first: int, last: int,
+def item_support(tids: torch.Tensor, n: int, m: int, first: int, last: int,
                  counts: torch.Tensor | None = None) -> torch.Tensor:
     if counts is None:
         counts = torch.zeros(m, dtype=torch.int64, device=tids.device)
-    _abi.call("dic_item_support", _ptr(tids), ld, m, first, last, _ptr(counts), _stream())
+    _abi.call("dic_item_support", _ptr(tids), n, m, first, last, _ptr(counts), _stream())
     return counts
 
 
-def count_support(tids: torch.Tensor, ld: int, m: int, first: int, last: int, items: torch.Tensor,
+def count_support(tids: torch.Tensor, n: int, m: int, first: int, last: int, items: torch.Tensor,
                   out: torch.Tensor | None = None) -> torch.Tensor:
     """items: device uint16/int16 [C][k] ascending item ids; out += counts (int64 [C])."""
     Cn, k = items.shape
     if out is None:
         out = torch.zeros(Cn, dtype=torch.int64, device=tids.device)
     if Cn:
-        _abi.call("dic_count_support", _ptr(tids), ld, m, first, last, _ptr(items), k, Cn, _ptr(out), _stream())
+        _abi.call("dic_count_support", _ptr(tids), n, m, first, last, _ptr(items), k, Cn, _ptr(out), _stream())
     return out
 
 

@@ -1,0 +1,227 @@
+"""DIC entry points: mine_parallel / mine_serial and the device-engine driver.
+
+Same signatures, results (frequent itemsets in (size, mask) order with exact
+supports) and MiningStats as the reference's engines (/root/reference/pkg/
+src/dicmine/engine.py:398-496).  The checkpoint loop of _run (:422-441) runs
+here on the host, one iteration per stop, driving the device-resident state
+machine in libdicb200.so (csrc/engine.cu):
+
+    dic_engine_count        count every dashed candidate over the local chunk
+    [all_reduce of deltas]  only when sharded over several GPUs
+    dic_engine_checkpoint   apply + prune + make_candidates + check_full_pass
+
+One small synchronous status read per stop drives the loop test, exactly the
+``while catalog.dashed`` of the reference.  With an ``audit`` recorder the
+run instead goes through the phase-level API (phases.py) so every
+transition is recorded in the reference's order.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi, bits
+from .bitmap import BitDatabase
+from .catalog import ItemsetCatalog, Shape, TransitionAudit
+from .config import MiningParams
+from .phases import (FrequentItemset, MiningResult, MiningStats, check_full_pass, count_support_interval,
+                     first_pass, make_candidates, prune)
+from .sharding import ShardPlan
+
+
+@dataclass
+class StopTrace:
+    """Per-stop engine status (for tests and the bench's accounting)."""
+
+    stops: list[dict] = field(default_factory=list)
+
+
+class DeviceEngine:
+    """RAII handle over dic_engine (one per rank)."""
+
+    def __init__(self, tids, n_local: int, m: int, params: MiningParams, prune_bound: bool):
+        import torch
+
+        self._torch = torch
+        self.tids = tids  # keep the buffer alive as long as the engine
+        self.m = m
+        h = C.c_void_p()
+        _abi.call("dic_engine_create", tids.data_ptr() if n_local > 0 else None, n_local, m,
+                  params.min_support_count, params.interval, params.intervals_per_pass, 1 if prune_bound else 0,
+                  torch.cuda.current_stream().cuda_stream, C.byref(h))
+        self.h = h
+
+    def close(self) -> None:
+        if self.h:
+            _abi.call("dic_engine_destroy", self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def item_counts(self):
+        counts = self._torch.empty(self.m, dtype=self._torch.int64, device="cuda")
+        _abi.call("dic_engine_item_counts", self.h, counts.data_ptr())
+        return counts
+
+    def seed(self, counts) -> tuple[int, int]:
+        L, P = C.c_int64(), C.c_int64()
+        _abi.call("dic_engine_seed", self.h, counts.data_ptr(), C.byref(L), C.byref(P))
+        return L.value, P.value
+
+    def count(self, lfirst: int, llast: int) -> None:
+        _abi.call("dic_engine_count", self.h, lfirst, llast)
+
+    def delta(self):
+        """The per-stop count deltas as a (non-owning) int64 CUDA tensor."""
+        ptr, ln = C.c_void_p(), C.c_int64()
+        _abi.call("dic_engine_delta", self.h, C.byref(ptr), C.byref(ln))
+        n = ln.value
+        if n == 0:
+            return self._torch.empty(0, dtype=self._torch.int64, device="cuda")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr.value, False), "version": 3,
+                                        "strides": None}
+
+        return self._torch.as_tensor(_View(), device="cuda")
+
+    def checkpoint(self) -> _abi.StopStatus:
+        st = _abi.StopStatus()
+        _abi.call("dic_engine_checkpoint", self.h, C.byref(st))
+        return st
+
+    def frequent(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        F = C.c_int64()
+        _abi.call("dic_engine_num_frequent", self.h, C.byref(F))
+        W = bits.words_for(self.m)
+        masks = np.zeros((max(F.value, 1), W), dtype=np.uint64)
+        sizes = np.zeros(max(F.value, 1), dtype=np.int32)
+        sups = np.zeros(max(F.value, 1), dtype=np.int64)
+        _abi.call("dic_engine_frequent", self.h, masks.ctypes.data, sizes.ctypes.data, sups.ctypes.data, F.value)
+        return masks[: F.value], sizes[: F.value], sups[: F.value]
+
+
+def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray) -> tuple[FrequentItemset, ...]:
+    """Canonical (size, mask) order with masks compared as Python ints (MSW first)."""
+    ints = bits.array_to_masks(masks)
+    items = [FrequentItemset(mk, int(sz), int(sp)) for mk, sz, sp in zip(ints, sizes.tolist(), sups.tolist())]
+    items.sort(key=lambda f: (f.size, f.mask))
+    return tuple(items)
+
+
+def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound: bool = True,
+               plan: ShardPlan | None = None, group=None, trace: StopTrace | None = None,
+               t0: float | None = None, count_events: list | None = None,
+               engine_factory=None) -> MiningResult:
+    """The checkpoint loop of _run over one rank's local rows.
+
+    ``plan``/``group``: chunk-sliced sharding (sharding.py) with a
+    torch.distributed process group; counts are sum-allreduced per stop.
+    ``count_events``: if a list, (start, end, word_tests) CUDA events are
+    appended around every count launch (the bench's roofline figures).
+    ``engine_factory``: test seam (a CPU stand-in engine for the gloo
+    multi-rank tests); the product always uses DeviceEngine."""
+    import torch
+    import torch.distributed as dist
+
+    t0 = time.perf_counter() if t0 is None else t0
+    sharded = plan is not None and plan.world > 1
+    local_chunks = plan.local_chunks() if plan is not None else None
+    eng = (engine_factory or DeviceEngine)(tids, n_local, m, params, prune_bound)
+    try:
+        stats = MiningStats()
+        counts = eng.item_counts()
+        if sharded:
+            dist.all_reduce(counts, group=group)
+        _, npairs = eng.seed(counts)
+        stats.candidates_generated = npairs
+        stats.peak_dashed = npairs
+        scanned = params.n
+        dashed = npairs
+        stop = 0
+        while dashed:
+            stop = stop + 1 if stop < params.intervals_per_pass else 1
+            first, last = params.chunk_bounds(stop)
+            lfirst, llast = local_chunks[stop - 1] if local_chunks is not None else (first, last)
+            stats.interval_counts += dashed
+            if count_events is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                eng.count(lfirst, llast)
+                ev1.record()
+                count_events.append((ev0, ev1, dashed * (-(-max(llast - lfirst + 1, 0) // 32))))
+            else:
+                eng.count(lfirst, llast)
+            if sharded:
+                dist.all_reduce(eng.delta(), group=group)
+            st = eng.checkpoint()
+            scanned += last - first + 1
+            stats.candidates_pruned += st.pruned
+            stats.candidates_generated += st.inserted
+            stats.peak_dashed = max(stats.peak_dashed, st.dashed_peak)
+            dashed = st.dashed_at_end
+            if trace is not None:
+                trace.stops.append({f: getattr(st, f) for f, _ in _abi.StopStatus._fields_} | {"stop": stop})
+        frequent = sorted_frequent(*eng.frequent())
+    finally:
+        eng.close()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+    stats.db_passes = scanned / params.n
+    stats.wall_time_s = time.perf_counter() - t0
+    return MiningResult(frequent=frequent, stats=stats)
+
+
+def _run_phases(db: BitDatabase, params: MiningParams, prune_bound: bool,
+                audit: TransitionAudit | None) -> MiningResult:
+    """Phase-level loop (audit mode): host catalog, GPU counting/admission."""
+    t0 = time.perf_counter()
+    stats = MiningStats()
+    catalog = ItemsetCatalog()
+    level1 = first_pass(catalog, db, params, audit=audit, stats=stats)
+    scanned = db.n
+    stop = 0
+    while catalog.dashed:
+        stop = stop + 1 if stop < params.intervals_per_pass else 1
+        first, last = params.chunk_bounds(stop)
+        stats.interval_counts += len(catalog.dashed)
+        count_support_interval(catalog, db, first, last)
+        scanned += last - first + 1
+        promoted = prune(catalog, params, bound_enabled=prune_bound, audit=audit, stats=stats)
+        make_candidates(catalog, params, frontier=promoted, level1=level1, audit=audit, stats=stats)
+        stats.peak_dashed = max(stats.peak_dashed, len(catalog.dashed))
+        check_full_pass(catalog, params, audit=audit, stats=stats)
+    frequent = tuple(sorted((FrequentItemset(r.mask, r.size, r.support) for r in catalog.solid
+                             if r.shape is Shape.SOLID_BOX), key=lambda f: (f.size, f.mask)))
+    stats.db_passes = scanned / db.n
+    stats.wall_time_s = time.perf_counter() - t0
+    return MiningResult(frequent=frequent, stats=stats)
+
+
+def mine_parallel(db: BitDatabase, params: MiningParams, *, prune_bound: bool = True,
+                  audit: TransitionAudit | None = None) -> MiningResult:
+    """DIC on the GPU; same frequent itemsets, supports and stats as the
+    reference engines (engine.py:478-496)."""
+    if params.n != db.n:
+        raise ValueError(f"params were built for n={params.n}, database has n={db.n}")
+    if audit is not None:
+        return _run_phases(db, params, prune_bound, audit)
+    t0 = time.perf_counter()
+    return run_engine(db.device_tids(), db.n, db.m, params, prune_bound=prune_bound, t0=t0)
+
+
+def mine_serial(db: BitDatabase, params: MiningParams, *, prune_bound: bool = True,
+                audit: TransitionAudit | None = None) -> MiningResult:
+    """The reference's serial engine is its pure-Python verification path
+    (engine.py:461-475); here both entry points run the same GPU engine,
+    whose output is identical by construction."""
+    return mine_parallel(db, params, prune_bound=prune_bound, audit=audit)

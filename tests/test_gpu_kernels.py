@@ -62,14 +62,20 @@ def test_encode_and_transpose(m):
     assert np.array_equal(got, want)
     st = status.cpu().numpy()
     assert st[0] == dedup and st[1] == -1 and st[2] == -1
-    tids, ld = D.rows_to_tids(rows, n, m)
+    tids = D.rows_to_tids(rows, n, m)
     t = tids.cpu().numpy().view(np.uint32)
+    assert t.size == D.tids_words(n, m)
+    TW = D.tile_groups(m)
+    RW = TW + 4
+    ntiles = t.size // (m * RW)
+    tiles = t.reshape(ntiles, m, RW)
+    assert not tiles[:, :, TW:].any(), "pad words must be zero"
     for i in range(m):
         col = (want[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1)
-        padded = np.zeros(ld * 32, dtype=np.uint64)
+        padded = np.zeros(ntiles * TW * 32, dtype=np.uint64)
         padded[:n] = col
-        words = (padded.reshape(ld, 32) << np.arange(32, dtype=np.uint64)).sum(axis=1).astype(np.uint32)
-        assert np.array_equal(t[i], words), f"item {i}"
+        words = (padded.reshape(-1, 32) << np.arange(32, dtype=np.uint64)).sum(axis=1).astype(np.uint32)
+        assert np.array_equal(tiles[:, i, :TW].reshape(-1), words), f"item {i}"
 
 
 def test_encode_reports_first_bad_item():
@@ -86,8 +92,8 @@ def test_encode_reports_first_bad_item():
 def test_item_support(m, n, first, last):
     rng = np.random.default_rng(n + m)
     rows = random_rows(rng, n, m, 0.3)
-    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
-    got = D.item_support(tids, ld, m, first, last).cpu().numpy()
+    tids = D.rows_to_tids(to_dev(rows), n, m)
+    got = D.item_support(tids, n, m, first, last).cpu().numpy()
     blk = rows[first : last + 1]
     want = np.array([np.count_nonzero((blk[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1)) for i in range(m)])
     assert np.array_equal(got, want)
@@ -102,13 +108,16 @@ def test_item_support(m, n, first, last):
     (200, 9000, 8, 500, 0.7, 0, 8999),
     (200, 9000, 11, 300, 0.8, 3, 8000),       # generic-k path
     (70, 100, 4, 50, 0.6, 40, 40),            # single-row chunk
+    (1000, 200000, 2, 20000, 0.03, 77, 190000),  # TW=16, several candidate blocks x row splits
+    (768, 100000, 3, 9000, 0.2, 0, 99999),      # largest TW=32 universe
+    (2000, 5000, 2, 300, 0.1, 10, 4990),        # too wide to stage: global fallback
 ])
 def test_count_support_matches_numpy(m, n, k, C, density, first, last):
     rng = np.random.default_rng(m * 7 + k)
     rows = random_rows(rng, n, m, density)
     items = np.sort(np.stack([rng.choice(m, size=k, replace=False) for _ in range(C)]), axis=1).astype(np.uint16)
-    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
-    got = D.count_support(tids, ld, m, first, last, to_dev(items.view(np.int16))).cpu().numpy()
+    tids = D.rows_to_tids(to_dev(rows), n, m)
+    got = D.count_support(tids, n, m, first, last, to_dev(items.view(np.int16))).cpu().numpy()
     want = np_count(rows, first, last, items_to_masks(items, D.words_for(m)))
     assert np.array_equal(got, want)
     # the literal row-form kernel agrees too
@@ -121,16 +130,18 @@ def test_count_support_accumulates():
     m, n = 96, 3000
     rows = random_rows(rng, n, m, 0.5)
     items = np.array([[1, 2], [5, 90], [0, 95]], dtype=np.uint16)
-    tids, ld = D.rows_to_tids(to_dev(rows), n, m)
+    tids = D.rows_to_tids(to_dev(rows), n, m)
     out = torch.full((3,), 7, dtype=torch.int64, device="cuda")
-    D.count_support(tids, ld, m, 0, 999, to_dev(items.view(np.int16)), out)
-    D.count_support(tids, ld, m, 1000, n - 1, to_dev(items.view(np.int16)), out)
+    D.count_support(tids, n, m, 0, 999, to_dev(items.view(np.int16)), out)
+    D.count_support(tids, n, m, 1000, n - 1, to_dev(items.view(np.int16)), out)
     want = np_count(rows, 0, n - 1, items_to_masks(items, 2)) + 7
     assert np.array_equal(out.cpu().numpy(), want)
 
 
 def test_bad_chunk_rejected():
     rows = to_dev(np.array([[1], [2]], dtype=np.uint64))
-    tids, ld = D.rows_to_tids(rows, 2, 2)
+    tids = D.rows_to_tids(rows, 2, 2)
     with pytest.raises(D._abi.DicError):
-        D.count_support(tids, ld, 2, 1, 0, to_dev(np.array([[0]], dtype=np.int16)))
+        D.count_support(tids, 2, 2, 1, 0, to_dev(np.array([[0]], dtype=np.int16)))
+    with pytest.raises(D._abi.DicError):
+        D.count_support(tids, 2, 2, 0, 2, to_dev(np.array([[0]], dtype=np.int16)))

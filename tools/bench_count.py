@@ -25,7 +25,7 @@ def main() -> None:
     a = ap.parse_args()
     D.require_cuda()
     rows = D.bernoulli_rows(a.n, a.m, 0.05, 5)
-    tids, ld = D.rows_to_tids(rows, a.n, a.m)
+    tids = D.rows_to_tids(rows, a.n, a.m)
     ks, items = D.synth_candidates(a.C, a.m, 2, 6, 5)
     res = {}
     total_t = 0.0
@@ -33,14 +33,14 @@ def main() -> None:
         sel = items[ks == k][:, :k]
         it = torch.from_numpy(np.ascontiguousarray(sel).view(np.int16)).cuda()
         out = torch.zeros(sel.shape[0], dtype=torch.int64, device="cuda")
-        D.count_support(tids, ld, a.m, 0, a.n - 1, it, out)
+        D.count_support(tids, a.n, a.m, 0, a.n - 1, it, out)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         best = 1e30
         for _ in range(a.reps):
             out.zero_()
             e0.record()
-            D.count_support(tids, ld, a.m, 0, a.n - 1, it, out)
+            D.count_support(tids, a.n, a.m, 0, a.n - 1, it, out)
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1))
