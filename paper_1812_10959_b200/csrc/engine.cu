@@ -18,8 +18,15 @@
 //             (itemsets.py:130-132).
 //   frontier  record ids promoted to DASHED_BOX at this stop (prune's return).
 //
-// Phase fusion (exactness argued in DESIGN.md §Engine): check_full_pass runs
-// in the same kernel as prune because finalisation never changes box-ness
+// One host synchronisation per stop: every kernel of a checkpoint reads its
+// sizes from device memory (grid-stride loops), capacities are checked on
+// the device (an overflow skips the state change and the host grows and
+// replays the candidate step), and entries that leave the dashed vector stay
+// in their bucket as dead slots — skipped by the apply kernel — until the
+// next checkpoint compacts that bucket.
+//
+// Phase fusion (exactness argued in DESIGN.md §4): check_full_pass runs in
+// the same kernel as prune because finalisation never changes box-ness
 // (DASHED_BOX->SOLID_BOX, DASHED_CIRCLE->SOLID_CIRCLE) and freshly inserted
 // candidates have intervals_counted == 0 < stop_max, so make_candidates sees
 // the same admissions and check_full_pass the same records either way.
@@ -57,17 +64,21 @@ __host__ __device__ inline uint64_t zob(uint32_t item) {
 constexpr int32_t kEmpty = -1;
 constexpr int32_t kTempFlag = 0x40000000;
 
-// Device counters (one struct, read back with a single copy).
-struct Counters {
-    unsigned long long nfront;
-    unsigned long long npruned;
-    unsigned long long nfinal;
-    unsigned long long survivors;  // non-NIL dashed after prune (incl. finalised)
-    unsigned long long nadm;       // admissible joins found by eval (pre-dedup)
-    unsigned long long ninserted;  // distinct new candidates committed
-    unsigned long long nrec;       // records
-    unsigned long long pad;
+// Status words (device, one contiguous u64 array; the host reads a prefix
+// of each section once per stop).
+enum : int {
+    S_NFRONT = 0,    // promoted DASHED_CIRCLE -> DASHED_BOX
+    S_NPRUNED = 1,   // DASHED_CIRCLE -> NIL by the bound
+    S_NFINAL = 2,    // dashed -> solid
+    S_SURV = 3,      // live dashed entries after prune (before finalisation)
+    S_NADM = 4,      // admissible joins (before dedup)
+    S_NINS = 5,      // distinct new candidates committed
+    S_OVERFLOW = 6,  // a capacity check failed: candidate step not applied
+    S_NREC = 7,      // records (persistent across stops)
+    S_HEAD = 8
 };
+// followed by: removed[KS] (slots not kept this stop), adm[KS] (admitted
+// joins by size), bn[KS] (bucket fill, persistent), KS = m + 2.
 
 struct Records {
     unsigned long long* mask = nullptr;  // [cap][W]
@@ -97,8 +108,8 @@ __device__ __forceinline__ bool mask_eq(const unsigned long long* a, const MaskV
     return true;
 }
 
-__device__ __forceinline__ int32_t ht_lookup(const int32_t* __restrict__ ht, uint64_t hmask,
-                                             const Records& R, int W, uint64_t h, const MaskView& v) {
+__device__ __forceinline__ int32_t ht_lookup(const int32_t* __restrict__ ht, uint64_t hmask, const Records& R,
+                                             int W, uint64_t h, const MaskView& v) {
     uint64_t slot = mix64(h) & hmask;
     while (true) {
         int32_t e = ht[slot];
@@ -112,8 +123,7 @@ __device__ __forceinline__ int32_t ht_lookup(const int32_t* __restrict__ ht, uin
 // seeding / rehash
 // ---------------------------------------------------------------------------
 __global__ void ht_clear_kernel(int32_t* ht, int64_t cap) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
-         i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
         ht[i] = kEmpty;
 }
 
@@ -126,8 +136,8 @@ __global__ void ht_insert_records_kernel(int32_t* ht, uint64_t hmask, Records R,
 }
 
 // Singletons: record i = item i (first_pass, engine.py:125-163).
-__global__ void seed_singletons_kernel(Records R, int W, int m, const int64_t* __restrict__ counts,
-                                       int64_t need, int64_t stop_max) {
+__global__ void seed_singletons_kernel(Records R, int W, int m, const int64_t* __restrict__ counts, int64_t need,
+                                       int64_t stop_max) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     for (int w = 0; w < W; ++w) R.mask[(int64_t)i * W + w] = (w == (i >> 6)) ? (1ull << (i & 63)) : 0ull;
@@ -145,7 +155,6 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
                                   int32_t* __restrict__ b_rec, uint16_t* __restrict__ b_items) {
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= npairs) return;
-    // row_start[a] = index of the first pair with first element a
     int64_t lo = 0, hi = L - 2;
     while (lo < hi) {
         int64_t mid = (lo + hi + 1) >> 1;
@@ -173,178 +182,230 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
 // ---------------------------------------------------------------------------
 // per stop
 // ---------------------------------------------------------------------------
+constexpr int kMaxApply = 16;
+struct ApplyArgs {
+    int nb;
+    int32_t k[kMaxApply];
+    const int32_t* rec[kMaxApply];
+    int64_t off[kMaxApply];  // slot offset of bucket i within this launch
+    int64_t total;
+};
+
 // support += delta, intervals += 1 (count_support_interval), then prune
-// (engine.py:292-310) and check_full_pass (:380-388).  keep[c] = still dashed.
-__global__ void apply_prune_finalize_kernel(const int32_t* __restrict__ b_rec, int64_t nb,
-                                            const unsigned long long* __restrict__ delta, Records R,
-                                            int64_t need, int64_t interval, int64_t stop_max, int bound,
+// (engine.py:292-310) and check_full_pass (:380-388).  Slots already dead
+// (left the dashed vector at an earlier stop, compaction pending) are only
+// marked not-kept.  keep[c] = still dashed.
+__global__ void apply_prune_finalize_kernel(const __grid_constant__ ApplyArgs a,
+                                            const unsigned long long* __restrict__ delta, Records R, int64_t need,
+                                            int64_t interval, int64_t stop_max, int bound,
                                             int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
-                                            Counters* ctr, unsigned long long* removed_k) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool promoted = false, pruned = false, fin = false, surv = false, kept = false;
-    if (c < nb) {
-        int32_t r = b_rec[c];
-        int64_t s = R.support[r] + (int64_t)delta[c];
-        int64_t iv = R.intervals[r] + 1;
-        R.support[r] = s;
-        R.intervals[r] = iv;
+                                            unsigned long long* __restrict__ stat) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool pruned = false, fin = false, surv = false, gone = false;
+    int bk = 0;
+    if (g < a.total) {
+        while (bk + 1 < a.nb && g >= a.off[bk + 1]) ++bk;
+        const int64_t c = g - a.off[bk];
+        const int32_t r = a.rec[bk][c];
         uint8_t sh = R.shape[r];
-        if (sh == DASHED_CIRCLE) {
-            if (s >= need) {
-                sh = DASHED_BOX;
-                promoted = true;
-            } else if (bound && iv < stop_max) {
-                int64_t remaining = stop_max - iv;
-                if (s + interval * remaining < need) {
+        bool kept = false;
+        if (is_dashed(sh)) {
+            const int64_t s = R.support[r] + (int64_t)delta[g];
+            const int64_t iv = R.intervals[r] + 1;
+            R.support[r] = s;
+            R.intervals[r] = iv;
+            if (sh == DASHED_CIRCLE) {
+                if (s >= need) {
+                    sh = DASHED_BOX;
+                    // order among promoted records is irrelevant to results and stats
+                    frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r;
+                } else if (bound && iv < stop_max && s + interval * (stop_max - iv) < need) {
                     sh = NIL;
                     pruned = true;
                 }
             }
-        }
-        if (is_dashed(sh)) {
-            surv = true;
-            if (iv == stop_max) {
-                sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
-                fin = true;
+            if (is_dashed(sh)) {
+                surv = true;
+                if (iv == stop_max) {
+                    sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
+                    fin = true;
+                }
             }
+            R.shape[r] = sh;
+            kept = is_dashed(sh);
         }
-        R.shape[r] = sh;
-        kept = is_dashed(sh);
-        keep[c] = kept ? 1 : 0;
-        if (promoted) {
-            // order among promoted records is irrelevant to results and stats
-            unsigned long long pos = atomicAdd(&ctr->nfront, 1ull);
-            frontier[pos] = r;
-        }
+        keep[g] = kept ? 1 : 0;
+        gone = !kept;
     }
-    // warp-aggregated counters
-    unsigned pr = __ballot_sync(0xFFFFFFFFu, pruned), fi = __ballot_sync(0xFFFFFFFFu, fin);
-    unsigned su = __ballot_sync(0xFFFFFFFFu, surv), rm = __ballot_sync(0xFFFFFFFFu, c < nb && !kept);
+    const unsigned full = 0xFFFFFFFFu;
+    unsigned pr = __ballot_sync(full, pruned), fi = __ballot_sync(full, fin), su = __ballot_sync(full, surv);
     if ((threadIdx.x & 31) == 0) {
-        if (pr) atomicAdd(&ctr->npruned, (unsigned long long)__popc(pr));
-        if (fi) atomicAdd(&ctr->nfinal, (unsigned long long)__popc(fi));
-        if (su) atomicAdd(&ctr->survivors, (unsigned long long)__popc(su));
-        if (rm) atomicAdd(removed_k, (unsigned long long)__popc(rm));
+        if (pr) atomicAdd(&stat[S_NPRUNED], (unsigned long long)__popc(pr));
+        if (fi) atomicAdd(&stat[S_NFINAL], (unsigned long long)__popc(fi));
+        if (su) atomicAdd(&stat[S_SURV], (unsigned long long)__popc(su));
+    }
+    if (gone) atomicAdd(&stat[S_HEAD + a.k[bk]], 1ull);  // removed[k]
+}
+
+// Order-preserving compaction of bucket k: scatter the kept slots into
+// scratch (pos = exclusive scan of keep), then copy back; bn[k] = kept.
+__global__ void compact_scatter_kernel(int64_t nb, int k, const int32_t* __restrict__ keep,
+                                       const int32_t* __restrict__ pos, const int32_t* __restrict__ rec_in,
+                                       const uint16_t* __restrict__ items_in, int32_t* __restrict__ rec_out,
+                                       uint16_t* __restrict__ items_out, unsigned long long* bn_k) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nb) return;
+    if (c == nb - 1) *bn_k = (unsigned long long)(pos[c] + keep[c]);
+    if (!keep[c]) return;
+    int64_t d = pos[c];
+    rec_out[d] = rec_in[c];
+    for (int j = 0; j < k; ++j) items_out[d * k + j] = items_in[c * k + j];
+}
+
+__global__ void compact_copyback_kernel(int k, const unsigned long long* __restrict__ bn_k, int64_t nb,
+                                        const int32_t* __restrict__ rec_s, const uint16_t* __restrict__ items_s,
+                                        int32_t* __restrict__ rec, uint16_t* __restrict__ items) {
+    const int64_t n = (int64_t)*bn_k;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n && c < nb;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        rec[c] = rec_s[c];
+        for (int j = 0; j < k; ++j) items[c * k + j] = items_s[c * k + j];
     }
 }
 
-// make_candidates (engine.py:320-369), evaluation: thread per (frontier f,
-// level1 item j).  Admission needs cand not in known and every immediate
-// subset known with a box shape; the subset equal to src is a box by
-// construction (it was just promoted) and is skipped.
-__global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, int64_t nf,
-                                       const int32_t* __restrict__ level1, int64_t L, int W, Records R,
-                                       const int32_t* __restrict__ ht, uint64_t hmask,
+// make_candidates (engine.py:320-369), evaluation: grid-stride over
+// (frontier f, level1 item j) pairs, sizes read from the status words.
+// Admission needs cand not in known and every immediate subset known with a
+// box shape; the subset equal to src is a box by construction (it was just
+// promoted) and is skipped.
+__global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, const int32_t* __restrict__ level1,
+                                       int64_t L, int W, Records R, const int32_t* __restrict__ ht, uint64_t hmask,
                                        unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
-                                       int32_t* __restrict__ tmp_size, int64_t tmp_cap, Counters* ctr,
-                                       unsigned long long* adm_by_size) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nf * L) return;
-    int64_t f = t / L, j = t - f * L;
-    int32_t src = frontier[f];
-    int l = level1[j];
-    const unsigned long long* sm = R.mask + (int64_t)src * W;
-    if ((sm[l >> 6] >> (l & 63)) & 1ull) return;  // cand == base
-    uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
-    MaskView cand{sm, l, -1};
-    if (ht_lookup(ht, hmask, R, W, hc, cand) >= 0) return;  // already known
-    for (int w = 0; w < W; ++w) {
-        unsigned long long x = cand.word(w);
-        while (x) {
-            int b = __ffsll((long long)x) - 1;
-            x &= x - 1;
-            int bit = w * 64 + b;
-            if (bit == l) continue;
-            MaskView sub{sm, l, bit};
-            int32_t e = ht_lookup(ht, hmask, R, W, hc ^ zob((uint32_t)bit), sub);
-            if (e < 0 || !is_box(R.shape[e])) return;
+                                       int32_t* __restrict__ tmp_size, int64_t tmp_cap,
+                                       unsigned long long* __restrict__ stat, int KS) {
+    const int64_t total = (int64_t)stat[S_NFRONT] * L;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = t / L, j = t - f * L;
+        const int32_t src = frontier[f];
+        const int l = level1[j];
+        const unsigned long long* sm = R.mask + (int64_t)src * W;
+        if ((sm[l >> 6] >> (l & 63)) & 1ull) continue;  // cand == base
+        const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
+        const MaskView cand{sm, l, -1};
+        if (ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
+        bool ok = true;
+        for (int w = 0; w < W && ok; ++w) {
+            unsigned long long x = cand.word(w);
+            while (x) {
+                const int bit = w * 64 + __ffsll((long long)x) - 1;
+                x &= x - 1;
+                if (bit == l) continue;
+                const MaskView sub{sm, l, bit};
+                const int32_t e = ht_lookup(ht, hmask, R, W, hc ^ zob((uint32_t)bit), sub);
+                if (e < 0 || !is_box(R.shape[e])) {
+                    ok = false;
+                    break;
+                }
+            }
+        }
+        if (!ok) continue;
+        const unsigned long long pos = atomicAdd(&stat[S_NADM], 1ull);
+        const int sz = R.size[src] + 1;
+        atomicAdd(&stat[S_HEAD + KS + sz], 1ull);  // adm[sz]
+        if ((int64_t)pos < tmp_cap) {
+            for (int w = 0; w < W; ++w) tmp_mask[(int64_t)pos * W + w] = cand.word(w);
+            tmp_hash[pos] = hc;
+            tmp_size[pos] = sz;
         }
     }
-    unsigned long long pos = atomicAdd(&ctr->nadm, 1ull);
-    int sz = R.size[src] + 1;
-    atomicAdd(adm_by_size + sz, 1ull);
-    if ((int64_t)pos < tmp_cap) {
-        for (int w = 0; w < W; ++w) tmp_mask[(int64_t)pos * W + w] = cand.word(w);
-        tmp_hash[pos] = hc;
-        tmp_size[pos] = sz;
+}
+
+// All-or-nothing capacity check for the candidate step.
+__global__ void check_capacity_kernel(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap,
+                                      int64_t hcap, const int64_t* __restrict__ bcap) {
+    __shared__ int over;
+    if (threadIdx.x == 0) {
+        const unsigned long long na = stat[S_NADM];
+        over = (int64_t)na > tmp_cap || (int64_t)(stat[S_NREC] + na) > rec_cap ||
+               (int64_t)(stat[S_NREC] + na) * 2 > hcap;
     }
+    __syncthreads();
+    const unsigned long long* adm = stat + S_HEAD + KS;
+    const unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    for (int k = threadIdx.x; k < KS; k += blockDim.x)
+        if (adm[k] && (int64_t)(bn[k] + adm[k]) > bcap[k]) over = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) stat[S_OVERFLOW] = over ? 1ull : 0ull;
 }
 
 // Dedup the admissible joins: claim a hash slot per distinct mask.  Slots
 // hold either a record id or kTempFlag | tmp index (resolved by commit).
-__global__ void insert_candidates_kernel(int64_t na, int W, const unsigned long long* __restrict__ tmp_mask,
+__global__ void insert_candidates_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
                                          const uint64_t* __restrict__ tmp_hash, Records R, int32_t* ht,
-                                         uint64_t hmask, int64_t* __restrict__ tmp_slot) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= na) return;
-    uint64_t h = tmp_hash[t];
-    const unsigned long long* mk = tmp_mask + t * W;
-    uint64_t slot = mix64(h) & hmask;
-    tmp_slot[t] = -1;
-    while (true) {
-        int32_t prev = atomicCAS(ht + slot, kEmpty, kTempFlag | (int32_t)t);
-        if (prev == kEmpty) {
-            tmp_slot[t] = (int64_t)slot;
-            return;
+                                         uint64_t hmask, int64_t* __restrict__ tmp_slot,
+                                         const unsigned long long* __restrict__ stat) {
+    if (stat[S_OVERFLOW]) return;
+    const int64_t na = (int64_t)stat[S_NADM];
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = tmp_hash[t];
+        const unsigned long long* mk = tmp_mask + t * W;
+        uint64_t slot = mix64(h) & hmask;
+        tmp_slot[t] = -1;
+        while (true) {
+            const int32_t prev = atomicCAS(ht + slot, kEmpty, kTempFlag | (int32_t)t);
+            if (prev == kEmpty) {
+                tmp_slot[t] = (int64_t)slot;
+                break;
+            }
+            bool same;
+            if (prev & kTempFlag) {
+                const int64_t o = prev & ~kTempFlag;
+                same = tmp_hash[o] == h;
+                for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
+            } else {
+                same = R.hash[prev] == h;
+                for (int w = 0; same && w < W; ++w) same = R.mask[(int64_t)prev * W + w] == mk[w];
+            }
+            if (same) break;  // duplicate of a join admitted by another thread
+            slot = (slot + 1) & hmask;
         }
-        bool same;
-        if (prev & kTempFlag) {
-            int64_t o = prev & ~kTempFlag;
-            same = tmp_hash[o] == h;
-            for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
-        } else {
-            same = R.hash[prev] == h;
-            for (int w = 0; same && w < W; ++w) same = R.mask[(int64_t)prev * W + w] == mk[w];
-        }
-        if (same) return;  // duplicate of a join admitted by another thread
-        slot = (slot + 1) & hmask;
     }
 }
 
-__global__ void commit_candidates_kernel(int64_t na, int W, const unsigned long long* __restrict__ tmp_mask,
+__global__ void commit_candidates_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
                                          const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
                                          const int64_t* __restrict__ tmp_slot, Records R, int32_t* ht,
-                                         Counters* ctr, int32_t* const* __restrict__ b_rec_tab,
-                                         uint16_t* const* __restrict__ b_items_tab,
-                                         unsigned long long* __restrict__ b_n) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= na) return;
-    int64_t slot = tmp_slot[t];
-    if (slot < 0) return;
-    int64_t r = (int64_t)atomicAdd(&ctr->nrec, 1ull);
-    atomicAdd(&ctr->ninserted, 1ull);
-    int sz = tmp_size[t];
-    for (int w = 0; w < W; ++w) R.mask[r * W + w] = tmp_mask[t * W + w];
-    R.hash[r] = tmp_hash[t];
-    R.size[r] = sz;
-    R.support[r] = 0;
-    R.intervals[r] = 0;
-    R.shape[r] = DASHED_CIRCLE;
-    ht[slot] = (int32_t)r;
-    unsigned long long pos = atomicAdd(b_n + sz, 1ull);
-    b_rec_tab[sz][pos] = (int32_t)r;
-    uint16_t* it = b_items_tab[sz] + (int64_t)pos * sz;
-    int j = 0;
-    for (int w = 0; w < W; ++w) {
-        unsigned long long x = tmp_mask[t * W + w];
-        while (x) {
-            int b = __ffsll((long long)x) - 1;
-            x &= x - 1;
-            it[j++] = (uint16_t)(w * 64 + b);
+                                         unsigned long long* stat, int KS, int32_t* const* __restrict__ b_rec_tab,
+                                         uint16_t* const* __restrict__ b_items_tab) {
+    if (stat[S_OVERFLOW]) return;
+    const int64_t na = (int64_t)stat[S_NADM];
+    unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = tmp_slot[t];
+        if (slot < 0) continue;
+        const int64_t r = (int64_t)atomicAdd(&stat[S_NREC], 1ull);
+        atomicAdd(&stat[S_NINS], 1ull);
+        const int sz = tmp_size[t];
+        for (int w = 0; w < W; ++w) R.mask[r * W + w] = tmp_mask[t * W + w];
+        R.hash[r] = tmp_hash[t];
+        R.size[r] = sz;
+        R.support[r] = 0;
+        R.intervals[r] = 0;
+        R.shape[r] = DASHED_CIRCLE;
+        ht[slot] = (int32_t)r;
+        const unsigned long long pos = atomicAdd(bn + sz, 1ull);
+        b_rec_tab[sz][pos] = (int32_t)r;
+        uint16_t* it = b_items_tab[sz] + (int64_t)pos * sz;
+        int j = 0;
+        for (int w = 0; w < W; ++w) {
+            unsigned long long x = tmp_mask[t * W + w];
+            while (x) {
+                it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
+                x &= x - 1;
+            }
         }
     }
-}
-
-// Order-preserving compaction of one bucket (compact_dashed).
-__global__ void compact_bucket_kernel(int64_t nb, int k, const int32_t* __restrict__ keep,
-                                      const int32_t* __restrict__ pos, const int32_t* __restrict__ rec_in,
-                                      const uint16_t* __restrict__ items_in, int32_t* __restrict__ rec_out,
-                                      uint16_t* __restrict__ items_out) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nb || !keep[c]) return;
-    int64_t d = pos[c];
-    rec_out[d] = rec_in[c];
-    for (int j = 0; j < k; ++j) items_out[d * k + j] = items_in[c * k + j];
 }
 
 __global__ void collect_frequent_kernel(Records R, int64_t nrec, int32_t* out, unsigned long long* nout) {
@@ -372,13 +433,15 @@ using namespace dic;
 struct Bucket {
     int32_t* rec = nullptr;
     uint16_t* items = nullptr;
-    int64_t n = 0, cap = 0;
+    int64_t n = 0;  // filled slots (live + dead) as of the last sync
+    int64_t cap = 0;
+    int64_t dead = 0;  // slots known dead, compaction pending
 };
 
 struct dic_engine {
     const uint32_t* tids;
     int64_t n_local;
-    int m, W;
+    int m, W, KS;
     int64_t need, interval, stop_max;
     int bound;
     cudaStream_t s;
@@ -389,11 +452,12 @@ struct dic_engine {
     int64_t hcap = 0;
 
     std::vector<Bucket> buckets;  // index = itemset size
-    int32_t** d_brec = nullptr;   // device copies of bucket pointer tables
+    int kuse = 4;                 // bucket indices < kuse may be non-empty
+    int32_t** d_brec = nullptr;   // device copies of the bucket tables
     uint16_t** d_bitems = nullptr;
-    unsigned long long* d_bn = nullptr;       // [m+2] bucket sizes (device mirror)
-    unsigned long long* d_removed = nullptr;  // [m+2]
-    unsigned long long* d_adm = nullptr;      // [m+2] admitted joins by size
+    int64_t* d_bcap = nullptr;
+    unsigned long long* d_stat = nullptr;  // status words (see S_*)
+    unsigned long long* h_stat = nullptr;  // pinned mirror
 
     int32_t* level1 = nullptr;
     int64_t nL1 = 0;
@@ -404,6 +468,9 @@ struct dic_engine {
     int64_t keep_cap = 0;
     void* scan_tmp = nullptr;
     size_t scan_tmp_bytes = 0;
+    int32_t* scr_rec = nullptr;
+    uint16_t* scr_items = nullptr;
+    int64_t scr_rec_cap = 0, scr_items_cap = 0;
 
     unsigned long long* delta = nullptr;
     int64_t delta_cap = 0, delta_len = 0;
@@ -415,8 +482,7 @@ struct dic_engine {
     int64_t* tmp_slot = nullptr;
     int64_t tmp_cap = 0;
 
-    Counters* ctr = nullptr;   // device
-    Counters* hctr = nullptr;  // pinned host
+    int64_t live = 0;  // |dashed|
     bool seeded = false;
     bool counted = false;
 };
@@ -454,8 +520,7 @@ int dgrow(T** p, int64_t old_count, int64_t new_count, cudaStream_t s) {
 
 int grow_records(dic_engine* e, int64_t need_cap) {
     if (need_cap <= e->R.cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>(need_cap, e->R.cap * 2);
-    nc = std::max<int64_t>(nc, 1024);
+    int64_t nc = std::max<int64_t>({need_cap, e->R.cap * 2, (int64_t)4096});
     Records& R = e->R;
     int rc;
     if ((rc = dgrow(&R.mask, e->nrec * e->W, nc * e->W, e->s))) return rc;
@@ -471,30 +536,35 @@ int grow_records(dic_engine* e, int64_t need_cap) {
 // keep the hash load factor <= 1/2; rebuild from the records on growth
 int ensure_hash(dic_engine* e, int64_t nrec_after) {
     if (nrec_after * 2 <= e->hcap) return DIC_OK;
-    int64_t nc = 1024;
+    int64_t nc = 4096;
     while (nc < nrec_after * 2) nc <<= 1;
     nc = std::max<int64_t>(nc, e->hcap * 2);
     dfree(e->ht, e->s);
     int rc = dalloc(&e->ht, nc, e->s);
     if (rc) return rc;
     e->hcap = nc;
-    ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc); ::dic::note_launch();
+    ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc);
+    ::dic::note_launch();
     if (e->nrec > 0) {
-        ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, 0, e->nrec); ::dic::note_launch();
+        ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, 0, e->nrec);
+        ::dic::note_launch();
     }
     DIC_CHECK_LAUNCH("rehash");
     return DIC_OK;
 }
 
 int sync_bucket_tables(dic_engine* e) {
-    std::vector<int32_t*> r(e->m + 2, nullptr);
-    std::vector<uint16_t*> it(e->m + 2, nullptr);
-    for (size_t k = 0; k < e->buckets.size() && k < (size_t)e->m + 2; ++k) {
+    std::vector<int32_t*> r(e->KS, nullptr);
+    std::vector<uint16_t*> it(e->KS, nullptr);
+    std::vector<int64_t> cap(e->KS, 0);
+    for (int k = 0; k < e->KS; ++k) {
         r[k] = e->buckets[k].rec;
         it[k] = e->buckets[k].items;
+        cap[k] = e->buckets[k].cap;
     }
     DIC_CUDA(cudaMemcpyAsync(e->d_brec, r.data(), r.size() * sizeof(int32_t*), cudaMemcpyHostToDevice, e->s));
     DIC_CUDA(cudaMemcpyAsync(e->d_bitems, it.data(), it.size() * sizeof(uint16_t*), cudaMemcpyHostToDevice, e->s));
+    DIC_CUDA(cudaMemcpyAsync(e->d_bcap, cap.data(), cap.size() * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
     // the host vectors die at return: make the copies complete first
     DIC_CUDA(cudaStreamSynchronize(e->s));
     return DIC_OK;
@@ -503,52 +573,126 @@ int sync_bucket_tables(dic_engine* e) {
 int grow_bucket(dic_engine* e, int k, int64_t need_cap, bool* changed) {
     Bucket& b = e->buckets[k];
     if (need_cap <= b.cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>(need_cap, b.cap * 2);
-    nc = std::max<int64_t>(nc, 256);
+    int64_t nc = std::max<int64_t>({need_cap, b.cap * 2, (int64_t)1024});
     int rc;
     if ((rc = dgrow(&b.rec, b.n, nc, e->s))) return rc;
     if ((rc = dgrow(&b.items, b.n * k, nc * k, e->s))) return rc;
     b.cap = nc;
     *changed = true;
+    e->kuse = std::max(e->kuse, std::min(k + 2, e->KS));
     return DIC_OK;
 }
 
-int ensure_scratch(dic_engine* e, int64_t nb) {
-    if (nb <= e->keep_cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>(nb, e->keep_cap * 2);
-    dfree(e->keep, e->s);
-    dfree(e->pos, e->s);
-    int rc;
-    if ((rc = dalloc(&e->keep, nc, e->s))) return rc;
-    if ((rc = dalloc(&e->pos, nc, e->s))) return rc;
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)nc, e->s);
-    if (bytes > e->scan_tmp_bytes) {
-        if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, e->s);
-        DIC_CUDA(cudaMallocAsync(&e->scan_tmp, bytes, e->s));
-        e->scan_tmp_bytes = bytes;
-    }
-    e->keep_cap = nc;
-    return DIC_OK;
-}
-
-int read_counters(dic_engine* e) {
-    DIC_CUDA(cudaMemcpyAsync(e->hctr, e->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, e->s));
-    DIC_CUDA(cudaStreamSynchronize(e->s));
-    return DIC_OK;
-}
-
-int64_t total_dashed(const dic_engine* e) {
+int64_t total_slots(const dic_engine* e) {
     int64_t t = 0;
     for (const Bucket& b : e->buckets) t += b.n;
     return t;
 }
 
+// per-stop scratch sized for `slots` bucket entries
+int ensure_stop_scratch(dic_engine* e, int64_t slots) {
+    int rc;
+    if (slots > e->keep_cap) {
+        int64_t nc = std::max<int64_t>(slots, e->keep_cap * 2);
+        dfree(e->keep, e->s);
+        dfree(e->pos, e->s);
+        if ((rc = dalloc(&e->keep, nc, e->s)) || (rc = dalloc(&e->pos, nc, e->s))) return rc;
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)nc, e->s);
+        if (bytes > e->scan_tmp_bytes) {
+            if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, e->s);
+            DIC_CUDA(cudaMallocAsync(&e->scan_tmp, bytes, e->s));
+            e->scan_tmp_bytes = bytes;
+        }
+        e->keep_cap = nc;
+    }
+    if (slots > e->front_cap) {
+        int64_t nc = std::max<int64_t>(slots, e->front_cap * 2);
+        dfree(e->frontier, e->s);
+        if ((rc = dalloc(&e->frontier, nc, e->s))) return rc;
+        e->front_cap = nc;
+    }
+    if (slots > e->delta_cap) {
+        int64_t nc = std::max<int64_t>(slots, e->delta_cap * 2);
+        dfree(e->delta, e->s);
+        if ((rc = dalloc(&e->delta, nc, e->s))) return rc;
+        e->delta_cap = nc;
+    }
+    return DIC_OK;
+}
+
+int ensure_tmp(dic_engine* e, int64_t want) {
+    if (want <= e->tmp_cap) return DIC_OK;
+    int64_t nc = std::max<int64_t>(want, e->tmp_cap * 2);
+    dfree(e->tmp_mask, e->s);
+    dfree(e->tmp_hash, e->s);
+    dfree(e->tmp_size, e->s);
+    dfree(e->tmp_slot, e->s);
+    int rc;
+    if ((rc = dalloc(&e->tmp_mask, nc * e->W, e->s)) || (rc = dalloc(&e->tmp_hash, nc, e->s)) ||
+        (rc = dalloc(&e->tmp_size, nc, e->s)) || (rc = dalloc(&e->tmp_slot, nc, e->s)))
+        return rc;
+    e->tmp_cap = nc;
+    return DIC_OK;
+}
+
+// Headroom so most stops never overflow: >= 64k join slots, record / hash
+// room for 64k more records, every bucket in use with room to grow by half
+// (>= 4096), and the next size up allocated.  Synchronises only on growth.
+int ensure_headroom(dic_engine* e) {
+    int rc;
+    const int64_t room = std::max<int64_t>(1 << 16, e->nrec / 2);
+    if ((rc = ensure_tmp(e, 1 << 16))) return rc;
+    if ((rc = grow_records(e, e->nrec + room))) return rc;
+    if ((rc = ensure_hash(e, e->nrec + room))) return rc;
+    bool changed = false;
+    int top = 2;
+    for (int k = 2; k < e->KS; ++k)
+        if (e->buckets[k].n > 0) top = k;
+    for (int k = 3; k <= std::min(top + 1, e->KS - 1); ++k) {  // pairs are only ever seeded
+        const Bucket& b = e->buckets[k];
+        const int64_t want = b.n + std::max<int64_t>(4096, b.n / 2);
+        if (want > b.cap && (rc = grow_bucket(e, k, want, &changed))) return rc;
+    }
+    if (changed && (rc = sync_bucket_tables(e))) return rc;
+    return DIC_OK;
+}
+
+int candidate_step(dic_engine* e) {
+    const int G = sm_count() * 4;
+    unsigned long long* st = e->d_stat;
+    eval_candidates_kernel<<<G, 256, 0, e->s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
+                                                 (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
+                                                 e->tmp_cap, st, e->KS);
+    ::dic::note_launch();
+    check_capacity_kernel<<<1, 256, 0, e->s>>>(st, e->KS, e->tmp_cap, e->R.cap, e->hcap, e->d_bcap);
+    ::dic::note_launch();
+    insert_candidates_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->R, e->ht, (uint64_t)e->hcap - 1,
+                                                   e->tmp_slot, st);
+    ::dic::note_launch();
+    commit_candidates_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->R,
+                                                   e->ht, st, e->KS, e->d_brec, e->d_bitems);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("candidate_step");
+    return DIC_OK;
+}
+
+// status -> host (head words, removed / adm / bn for sizes < kuse); sync
+int read_status(dic_engine* e) {
+    const int KS = e->KS, ku = e->kuse;
+    const size_t u = sizeof(unsigned long long);
+    DIC_CUDA(cudaMemcpyAsync(e->h_stat, e->d_stat, S_HEAD * u, cudaMemcpyDeviceToHost, e->s));
+    for (int sec = 0; sec < 3; ++sec)
+        DIC_CUDA(cudaMemcpyAsync(e->h_stat + S_HEAD + sec * KS, e->d_stat + S_HEAD + sec * KS, ku * u,
+                                 cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));
+    return DIC_OK;
+}
+
 }  // namespace
 
-extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t m, int64_t need,
-                                 int64_t interval, int64_t stop_max, int32_t prune_bound, void* stream,
-                                 dic_engine** out) {
+extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t m, int64_t need, int64_t interval,
+                                 int64_t stop_max, int32_t prune_bound, void* stream, dic_engine** out) {
     DIC_REQUIRE(out, "dic_engine_create: out is null");
     DIC_REQUIRE(m >= 1 && m <= 65535, "dic_engine_create: m=%d outside [1, 65535]", m);
     DIC_REQUIRE(n_local >= 0 && (tids || n_local == 0), "dic_engine_create: bad tids/n_local");
@@ -558,28 +702,30 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->n_local = n_local;
     e->m = m;
     e->W = (m + 63) / 64;
+    e->KS = m + 2;
+    e->kuse = std::min(4, e->KS);
     e->need = need;
     e->interval = interval;
     e->stop_max = stop_max;
     e->bound = prune_bound ? 1 : 0;
     e->s = as_stream(stream);
-    e->buckets.resize(m + 2);
+    e->buckets.resize(e->KS);
+    const int KS = e->KS;
     int rc = 0;
-    if ((rc = dalloc(&e->d_brec, m + 2, e->s)) || (rc = dalloc(&e->d_bitems, m + 2, e->s)) ||
-        (rc = dalloc(&e->d_bn, m + 2, e->s)) || (rc = dalloc(&e->d_removed, m + 2, e->s)) ||
-        (rc = dalloc(&e->d_adm, m + 2, e->s)) || (rc = dalloc(&e->ctr, 1, e->s)) ||
+    if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
+        (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_stat, S_HEAD + 3 * KS, e->s)) ||
         (rc = dalloc(&e->level1, m, e->s))) {
         delete e;
         return rc;
     }
-    cudaError_t ce = cudaMallocHost((void**)&e->hctr, sizeof(Counters));
+    cudaError_t ce = cudaMallocHost((void**)&e->h_stat, (S_HEAD + 3 * KS) * sizeof(unsigned long long));
     if (ce != cudaSuccess) {
         delete e;
         return cuda_fail(ce, "cudaMallocHost");
     }
-    cudaMemsetAsync(e->d_bn, 0, (m + 2) * sizeof(unsigned long long), e->s);
-    rc = sync_bucket_tables(e);
-    if (rc) {
+    memset(e->h_stat, 0, (S_HEAD + 3 * KS) * sizeof(unsigned long long));
+    cudaMemsetAsync(e->d_stat, 0, (S_HEAD + 3 * KS) * sizeof(unsigned long long), e->s);
+    if ((rc = sync_bucket_tables(e))) {
         delete e;
         return rc;
     }
@@ -591,17 +737,17 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     if (!e) return DIC_OK;
     cudaStream_t s = e->s;
     Records& R = e->R;
-    dfree(R.mask, s); dfree(R.hash, s); dfree(R.support, s); dfree(R.intervals, s);
-    dfree(R.size, s); dfree(R.shape, s);
+    dfree(R.mask, s); dfree(R.hash, s); dfree(R.support, s); dfree(R.intervals, s); dfree(R.size, s);
+    dfree(R.shape, s);
     dfree(e->ht, s);
     for (Bucket& b : e->buckets) { dfree(b.rec, s); dfree(b.items, s); }
-    dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bn, s); dfree(e->d_removed, s);
-    dfree(e->d_adm, s); dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s);
-    dfree(e->pos, s); dfree(e->delta, s); dfree(e->tmp_mask, s); dfree(e->tmp_hash, s);
-    dfree(e->tmp_size, s); dfree(e->tmp_slot, s); dfree(e->ctr, s);
+    dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_stat, s);
+    dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->pos, s);
+    dfree(e->scr_rec, s); dfree(e->scr_items, s); dfree(e->delta, s);
+    dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
     if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, s);
     cudaStreamSynchronize(s);
-    if (e->hctr) cudaFreeHost(e->hctr);
+    if (e->h_stat) cudaFreeHost(e->h_stat);
     delete e;
     return DIC_OK;
 }
@@ -630,16 +776,21 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     const int64_t L = (int64_t)l1.size();
     const int64_t npairs = L * (L - 1) / 2;
     int rc;
-    if ((rc = grow_records(e, m + npairs + 1024))) return rc;
     e->nrec = 0;
-    if ((rc = ensure_hash(e, m + npairs))) return rc;
-    seed_singletons_kernel<<<nblk(m), 256, 0, e->s>>>(e->R, e->W, m, counts, e->need, e->stop_max); ::dic::note_launch();
+    const int64_t room = std::max<int64_t>(1 << 16, (m + npairs) / 2);
+    if ((rc = grow_records(e, m + npairs + room))) return rc;
+    if ((rc = ensure_hash(e, m + npairs + room))) return rc;
+    seed_singletons_kernel<<<nblk(m), 256, 0, e->s>>>(e->R, e->W, m, counts, e->need, e->stop_max);
+    ::dic::note_launch();
     DIC_CHECK_LAUNCH("seed_singletons_kernel");
     if (L > 0) DIC_CUDA(cudaMemcpyAsync(e->level1, l1.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, e->s));
     e->nL1 = L;
+    bool changed = false;
+    if (e->KS > 3) {
+        if ((rc = grow_bucket(e, 2, std::max<int64_t>(npairs, 1024), &changed))) return rc;
+        if ((rc = grow_bucket(e, 3, 4096, &changed))) return rc;
+    }
     if (npairs > 0) {
-        bool changed = false;
-        if ((rc = grow_bucket(e, 2, npairs, &changed))) return rc;
         std::vector<int64_t> rs(L);
         int64_t acc = 0;
         for (int64_t a = 0; a < L; ++a) { rs[a] = acc; acc += L - 1 - a; }
@@ -647,20 +798,24 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         if ((rc = dalloc(&d_rs, L, e->s))) return rc;
         DIC_CUDA(cudaMemcpyAsync(d_rs, rs.data(), L * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
         seed_pairs_kernel<<<nblk(npairs), 256, 0, e->s>>>(e->R, e->W, e->level1, L, d_rs, npairs, m,
-                                                          e->buckets[2].rec, e->buckets[2].items); ::dic::note_launch();
+                                                          e->buckets[2].rec, e->buckets[2].items);
+        ::dic::note_launch();
         DIC_CHECK_LAUNCH("seed_pairs_kernel");
         dfree(d_rs, e->s);
         e->buckets[2].n = npairs;
-        if (changed && (rc = sync_bucket_tables(e))) return rc;
     }
     e->nrec = m + npairs;
-    ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec); ::dic::note_launch();
+    ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec);
+    ::dic::note_launch();
     DIC_CHECK_LAUNCH("ht_insert_records_kernel");
-    // device mirror of bucket sizes
-    std::vector<unsigned long long> bn(m + 2, 0);
-    bn[2] = (unsigned long long)npairs;
-    DIC_CUDA(cudaMemcpyAsync(e->d_bn, bn.data(), bn.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, e->s));
-    DIC_CUDA(cudaStreamSynchronize(e->s));
+    // device status: records and bucket fill
+    std::vector<unsigned long long> head(S_HEAD, 0), bn(e->KS, 0);
+    head[S_NREC] = (unsigned long long)e->nrec;
+    if (e->KS > 2) bn[2] = (unsigned long long)npairs;
+    DIC_CUDA(cudaMemcpyAsync(e->d_stat, head.data(), S_HEAD * 8, cudaMemcpyHostToDevice, e->s));
+    DIC_CUDA(cudaMemcpyAsync(e->d_stat + S_HEAD + 2 * e->KS, bn.data(), e->KS * 8, cudaMemcpyHostToDevice, e->s));
+    if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
+    e->live = npairs;
     e->seeded = true;
     if (n_level1) *n_level1 = L;
     if (n_pairs) *n_pairs = npairs;
@@ -673,14 +828,9 @@ extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
     DIC_REQUIRE(lfirst >= 0 && (llast < lfirst || llast < e->n_local),
                 "dic_engine_count: local chunk [%lld, %lld] outside %lld local rows", (long long)lfirst,
                 (long long)llast, (long long)e->n_local);
-    const int64_t tot = total_dashed(e);
-    if (tot > e->delta_cap) {
-        dfree(e->delta, e->s);
-        int64_t nc = std::max<int64_t>(tot, e->delta_cap * 2);
-        int rc = dalloc(&e->delta, nc, e->s);
-        if (rc) return rc;
-        e->delta_cap = nc;
-    }
+    const int64_t tot = total_slots(e);
+    int rc;
+    if ((rc = ensure_stop_scratch(e, std::max<int64_t>(tot, 1)))) return rc;
     e->delta_len = tot;
     e->delta_off.assign(e->buckets.size(), 0);
     if (tot > 0) DIC_CUDA(cudaMemsetAsync(e->delta, 0, tot * sizeof(unsigned long long), e->s));
@@ -693,7 +843,7 @@ extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
         off += b.n;
     }
     if (!bk.empty() && llast >= lfirst) {
-        int rc = count_buckets_launch(e->tids, e->n_local, e->m, lfirst, llast, bk.data(), (int)bk.size(), e->s);
+        rc = count_buckets_launch(e->tids, e->n_local, e->m, lfirst, llast, bk.data(), (int)bk.size(), e->s);
         if (rc) return rc;
     }
     e->counted = true;
@@ -712,124 +862,125 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
     if (!e->counted) { set_error("dic_engine_checkpoint: no count since the last checkpoint"); return DIC_ESTATE; }
     e->counted = false;
     int rc;
-    const int64_t tot = e->delta_len;
-    st->dashed_at_start = tot;
-    // 1. apply + prune + finalize, per bucket
-    if ((rc = ensure_scratch(e, std::max<int64_t>(tot, 1)))) return rc;
-    if (tot > e->front_cap) {
-        dfree(e->frontier, e->s);
-        int64_t nc = std::max<int64_t>(tot, e->front_cap * 2);
-        if ((rc = dalloc(&e->frontier, nc, e->s))) return rc;
-        e->front_cap = nc;
-    }
-    DIC_CUDA(cudaMemsetAsync(e->ctr, 0, sizeof(Counters), e->s));
-    DIC_CUDA(cudaMemsetAsync(e->d_removed, 0, (e->m + 2) * sizeof(unsigned long long), e->s));
-    for (size_t k = 0; k < e->buckets.size(); ++k) {
-        const Bucket& b = e->buckets[k];
-        if (b.n == 0) continue;
-        int64_t off = e->delta_off[k];
-        apply_prune_finalize_kernel<<<nblk(b.n), 256, 0, e->s>>>(
-            b.rec, b.n, e->delta + off, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
-            e->keep + off, e->ctr, e->d_removed + k); ::dic::note_launch();
-    }
-    DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
-    std::vector<unsigned long long> removed(e->buckets.size(), 0);
-    DIC_CUDA(cudaMemcpyAsync(removed.data(), e->d_removed, removed.size() * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, e->s));
-    if ((rc = read_counters(e))) return rc;
-    const int64_t nfront = (int64_t)e->hctr->nfront;
-    st->promoted = nfront;
-    st->pruned = (int64_t)e->hctr->npruned;
-    st->finalized = (int64_t)e->hctr->nfinal;
-    const int64_t survivors = (int64_t)e->hctr->survivors;
+    const int KS = e->KS;
+    const size_t u = sizeof(unsigned long long);
+    st->dashed_at_start = e->live;
+    // reset the per-stop counters, removed[] and adm[] (NREC and bn[] persist)
+    DIC_CUDA(cudaMemsetAsync(e->d_stat, 0, S_NREC * u, e->s));
+    DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD, 0, 2 * (size_t)KS * u, e->s));
 
-    // 2. compaction (before appending, so new candidates keep their slots)
-    bool tables_changed = false;
-    for (size_t k = 0; k < e->buckets.size(); ++k) {
+    // 1. apply + prune + finalize over every bucket slot (one launch per 16 buckets)
+    {
+        ApplyArgs a;
+        memset(&a, 0, sizeof(a));
+        int64_t base = 0;
+        auto flush = [&]() -> int {
+            if (a.nb == 0) return DIC_OK;
+            apply_prune_finalize_kernel<<<nblk(a.total), 256, 0, e->s>>>(
+                a, e->delta + base, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier, e->keep + base,
+                e->d_stat);
+            ::dic::note_launch();
+            DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
+            memset(&a, 0, sizeof(a));
+            return DIC_OK;
+        };
+        for (int k = 0; k < KS; ++k) {
+            const Bucket& b = e->buckets[k];
+            if (b.n == 0) continue;
+            if (a.nb == kMaxApply && (rc = flush())) return rc;
+            if (a.nb == 0) base = e->delta_off[k];
+            a.k[a.nb] = k;
+            a.rec[a.nb] = b.rec;
+            a.off[a.nb] = e->delta_off[k] - base;
+            a.total = e->delta_off[k] - base + b.n;
+            ++a.nb;
+        }
+        if ((rc = flush())) return rc;
+    }
+
+    // 2. compaction of buckets holding dead slots from earlier stops (this
+    //    stop's keep flags also drop the entries that just left)
+    std::vector<char> compacted(KS, 0);
+    for (int k = 0; k < KS; ++k) {
         Bucket& b = e->buckets[k];
-        if (b.n == 0 || removed[k] == 0) continue;
-        int64_t off = e->delta_off[k];
+        if (b.n == 0 || b.dead == 0) continue;
+        const int64_t off = e->delta_off[k];
+        if (b.n > e->scr_rec_cap) {
+            dfree(e->scr_rec, e->s);
+            if ((rc = dalloc(&e->scr_rec, b.n, e->s))) return rc;
+            e->scr_rec_cap = b.n;
+        }
+        if (b.n * k > e->scr_items_cap) {
+            dfree(e->scr_items, e->s);
+            if ((rc = dalloc(&e->scr_items, b.n * k, e->s))) return rc;
+            e->scr_items_cap = b.n * k;
+        }
         size_t bytes = e->scan_tmp_bytes;
-        cub::DeviceScan::ExclusiveSum(e->scan_tmp, bytes, e->keep + off, e->pos + off, (int)b.n, e->s);
-        int32_t* nrec_arr = nullptr;
-        uint16_t* nitems = nullptr;
-        if ((rc = dalloc(&nrec_arr, b.cap, e->s)) || (rc = dalloc(&nitems, b.cap * (int64_t)k, e->s))) return rc;
-        compact_bucket_kernel<<<nblk(b.n), 256, 0, e->s>>>(b.n, (int)k, e->keep + off, e->pos + off, b.rec,
-                                                            b.items, nrec_arr, nitems); ::dic::note_launch();
-        DIC_CHECK_LAUNCH("compact_bucket_kernel");
-        dfree(b.rec, e->s);
-        dfree(b.items, e->s);
-        b.rec = nrec_arr;
-        b.items = nitems;
-        b.n -= (int64_t)removed[k];
-        tables_changed = true;
+        DIC_CUDA(cub::DeviceScan::ExclusiveSum(e->scan_tmp, bytes, e->keep + off, e->pos + off, (int)b.n, e->s));
+        unsigned long long* bn_k = e->d_stat + S_HEAD + 2 * KS + k;
+        compact_scatter_kernel<<<nblk(b.n), 256, 0, e->s>>>(b.n, k, e->keep + off, e->pos + off, b.rec, b.items,
+                                                            e->scr_rec, e->scr_items, bn_k);
+        ::dic::note_launch();
+        compact_copyback_kernel<<<std::min<unsigned>(nblk(b.n), (unsigned)sm_count() * 8), 256, 0, e->s>>>(
+            k, bn_k, b.n, e->scr_rec, e->scr_items, b.rec, b.items);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("compaction");
+        compacted[k] = 1;
     }
 
-    // 3. make_candidates from the frontier
-    int64_t inserted = 0;
-    if (nfront > 0 && e->nL1 > 0) {
-        const int64_t pairs = nfront * e->nL1;
-        int64_t want_tmp = std::min<int64_t>(pairs, std::max<int64_t>(1 << 16, e->tmp_cap));
-        for (int attempt = 0; attempt < 2; ++attempt) {
-            if (want_tmp > e->tmp_cap) {
-                dfree(e->tmp_mask, e->s); dfree(e->tmp_hash, e->s); dfree(e->tmp_size, e->s); dfree(e->tmp_slot, e->s);
-                if ((rc = dalloc(&e->tmp_mask, want_tmp * e->W, e->s)) || (rc = dalloc(&e->tmp_hash, want_tmp, e->s)) ||
-                    (rc = dalloc(&e->tmp_size, want_tmp, e->s)) || (rc = dalloc(&e->tmp_slot, want_tmp, e->s)))
-                    return rc;
-                e->tmp_cap = want_tmp;
-            }
-            DIC_CUDA(cudaMemsetAsync(&e->ctr->nadm, 0, sizeof(unsigned long long), e->s));
-            DIC_CUDA(cudaMemsetAsync(e->d_adm, 0, (e->m + 2) * sizeof(unsigned long long), e->s));
-            eval_candidates_kernel<<<nblk(pairs), 256, 0, e->s>>>(
-                e->frontier, nfront, e->level1, e->nL1, e->W, e->R, e->ht, (uint64_t)e->hcap - 1, e->tmp_mask,
-                e->tmp_hash, e->tmp_size, e->tmp_cap, e->ctr, e->d_adm); ::dic::note_launch();
-            DIC_CHECK_LAUNCH("eval_candidates_kernel");
-            if ((rc = read_counters(e))) return rc;
-            if ((int64_t)e->hctr->nadm <= e->tmp_cap) break;
-            want_tmp = (int64_t)e->hctr->nadm;  // rerun once with room for every join
+    // 3. make_candidates from the frontier (device-sized; all-or-nothing)
+    if ((rc = candidate_step(e))) return rc;
+    if ((rc = read_status(e))) return rc;
+    unsigned long long* h = e->h_stat;
+    int replays = 0;
+    while (h[S_OVERFLOW]) {
+        if (++replays > 4) {
+            set_error("dic_engine_checkpoint: candidate capacity did not converge");
+            return DIC_ENOMEM;
         }
-        const int64_t na = (int64_t)e->hctr->nadm;
-        if (na > 0) {
-            std::vector<unsigned long long> adm(e->m + 2);
-            DIC_CUDA(cudaMemcpyAsync(adm.data(), e->d_adm, adm.size() * sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, e->s));
-            DIC_CUDA(cudaStreamSynchronize(e->s));
-            if ((rc = grow_records(e, e->nrec + na))) return rc;
-            if ((rc = ensure_hash(e, e->nrec + na))) return rc;
-            for (int k = 0; k < e->m + 2; ++k) {
-                if (!adm[k]) continue;
-                if ((rc = grow_bucket(e, k, e->buckets[k].n + (int64_t)adm[k], &tables_changed))) return rc;
-            }
-            if (tables_changed) {
-                if ((rc = sync_bucket_tables(e))) return rc;
-                tables_changed = false;
-            }
-            std::vector<unsigned long long> bn(e->m + 2);
-            for (int k = 0; k < e->m + 2; ++k) bn[k] = (unsigned long long)e->buckets[k].n;
-            DIC_CUDA(cudaMemcpyAsync(e->d_bn, bn.data(), bn.size() * sizeof(unsigned long long),
-                                     cudaMemcpyHostToDevice, e->s));
-            unsigned long long nrec_now = (unsigned long long)e->nrec;
-            DIC_CUDA(cudaMemcpyAsync(&e->ctr->nrec, &nrec_now, sizeof(nrec_now), cudaMemcpyHostToDevice, e->s));
-            insert_candidates_kernel<<<nblk(na), 256, 0, e->s>>>(na, e->W, e->tmp_mask, e->tmp_hash, e->R, e->ht,
-                                                                 (uint64_t)e->hcap - 1, e->tmp_slot); ::dic::note_launch();
-            DIC_CHECK_LAUNCH("insert_candidates_kernel");
-            commit_candidates_kernel<<<nblk(na), 256, 0, e->s>>>(na, e->W, e->tmp_mask, e->tmp_hash, e->tmp_size,
-                                                                 e->tmp_slot, e->R, e->ht, e->ctr, e->d_brec,
-                                                                 e->d_bitems, e->d_bn); ::dic::note_launch();
-            DIC_CHECK_LAUNCH("commit_candidates_kernel");
-            DIC_CUDA(cudaMemcpyAsync(bn.data(), e->d_bn, bn.size() * sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, e->s));
-            if ((rc = read_counters(e))) return rc;
-            inserted = (int64_t)e->hctr->ninserted;
-            e->nrec = (int64_t)e->hctr->nrec;
-            for (int k = 0; k < e->m + 2; ++k) e->buckets[k].n = (int64_t)bn[k];
+        // adm[] for every size (a join can only grow a size by one, but read all)
+        std::vector<unsigned long long> adm(KS), bn(KS);
+        DIC_CUDA(cudaMemcpyAsync(adm.data(), e->d_stat + S_HEAD + KS, KS * u, cudaMemcpyDeviceToHost, e->s));
+        DIC_CUDA(cudaMemcpyAsync(bn.data(), e->d_stat + S_HEAD + 2 * KS, KS * u, cudaMemcpyDeviceToHost, e->s));
+        DIC_CUDA(cudaStreamSynchronize(e->s));
+        const int64_t na = (int64_t)h[S_NADM];
+        e->nrec = (int64_t)h[S_NREC];
+        if ((rc = ensure_tmp(e, na))) return rc;
+        if ((rc = grow_records(e, e->nrec + na))) return rc;
+        if ((rc = ensure_hash(e, e->nrec + na))) return rc;
+        bool changed = false;
+        for (int k = 0; k < KS; ++k) {
+            if (!adm[k]) continue;
+            e->buckets[k].n = (int64_t)bn[k];  // growth copies the filled prefix
+            if ((rc = grow_bucket(e, k, (int64_t)(bn[k] + adm[k]), &changed))) return rc;
         }
+        if (changed && (rc = sync_bucket_tables(e))) return rc;
+        // replay: reset the join counters; NFRONT / frontier / apply results stay
+        DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
+        DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
+        if ((rc = candidate_step(e))) return rc;
+        if ((rc = read_status(e))) return rc;
     }
-    if (tables_changed && (rc = sync_bucket_tables(e))) return rc;
+
+    // 4. bookkeeping from the status words
+    const int64_t pruned = (int64_t)h[S_NPRUNED], finalized = (int64_t)h[S_NFINAL];
+    const int64_t inserted = (int64_t)h[S_NINS], survivors = (int64_t)h[S_SURV];
+    e->nrec = (int64_t)h[S_NREC];
+    for (int k = 0; k < e->kuse; ++k) {
+        Bucket& b = e->buckets[k];
+        b.n = (int64_t)h[S_HEAD + 2 * KS + k];
+        b.dead = compacted[k] ? 0 : (int64_t)h[S_HEAD + k];  // not-kept slots (old + new)
+    }
+    st->promoted = (int64_t)h[S_NFRONT];
+    st->pruned = pruned;
+    st->finalized = finalized;
     st->inserted = inserted;
     st->dashed_peak = survivors + inserted;
-    st->dashed_at_end = total_dashed(e);
+    e->live = e->live - pruned - finalized + inserted;
+    st->dashed_at_end = e->live;
     st->records = e->nrec;
+    // 5. headroom for the next stop (rare growth; synchronises only then)
+    if ((rc = ensure_headroom(e))) return rc;
     return DIC_OK;
 }
 
@@ -838,12 +989,16 @@ extern "C" int dic_engine_num_frequent(dic_engine* e, int64_t* F) {
     int32_t* ids = nullptr;
     int rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s);
     if (rc) return rc;
-    DIC_CUDA(cudaMemsetAsync(&e->ctr->pad, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad); ::dic::note_launch();
+    unsigned long long* cnt = e->d_stat + S_NADM;  // scratch word between stops
+    DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
+    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
+    ::dic::note_launch();
     DIC_CHECK_LAUNCH("collect_frequent_kernel");
-    if ((rc = read_counters(e))) return rc;
+    unsigned long long hF = 0;
+    DIC_CUDA(cudaMemcpyAsync(&hF, cnt, sizeof(hF), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));
     dfree(ids, e->s);
-    *F = (int64_t)e->hctr->pad;
+    *F = (int64_t)hF;
     return DIC_OK;
 }
 
@@ -855,18 +1010,24 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
     unsigned long long* dm = nullptr;
     int32_t* dsz = nullptr;
     int64_t* dsu = nullptr;
-    if ((rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s)) || (rc = dalloc(&dm, std::max<int64_t>(F, 1) * e->W, e->s)) ||
-        (rc = dalloc(&dsz, std::max<int64_t>(F, 1), e->s)) || (rc = dalloc(&dsu, std::max<int64_t>(F, 1), e->s)))
+    const int64_t F1 = std::max<int64_t>(F, 1);
+    if ((rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s)) || (rc = dalloc(&dm, F1 * e->W, e->s)) ||
+        (rc = dalloc(&dsz, F1, e->s)) || (rc = dalloc(&dsu, F1, e->s)))
         return rc;
-    DIC_CUDA(cudaMemsetAsync(&e->ctr->pad, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, &e->ctr->pad); ::dic::note_launch();
-    if ((rc = read_counters(e))) return rc;
-    if ((int64_t)e->hctr->pad != F) {
-        set_error("dic_engine_frequent: F=%lld but %llu frequent records", (long long)F, e->hctr->pad);
+    unsigned long long* cnt = e->d_stat + S_NADM;
+    DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
+    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
+    ::dic::note_launch();
+    unsigned long long hF = 0;
+    DIC_CUDA(cudaMemcpyAsync(&hF, cnt, sizeof(hF), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));
+    if ((int64_t)hF != F) {
+        set_error("dic_engine_frequent: F=%lld but %llu frequent records", (long long)F, hF);
         return DIC_EINVAL;
     }
     if (F > 0) {
-        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->W, ids, F, dm, dsz, dsu); ::dic::note_launch();
+        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->W, ids, F, dm, dsz, dsu);
+        ::dic::note_launch();
         DIC_CHECK_LAUNCH("gather_frequent_kernel");
         DIC_CUDA(cudaMemcpyAsync(masks_host, dm, F * e->W * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s));
         DIC_CUDA(cudaMemcpyAsync(sizes_host, dsz, F * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));
