@@ -115,6 +115,20 @@ int dic_count_support(const uint32_t* tids, int64_t n, int32_t m,
                       const uint16_t* items, int32_t k, int64_t C,
                       uint64_t* support_inc, void* stream);
 
+/* All pairs at once: the 2-itemset bucket as a dense triangle ----------
+ * For every pair of items a < b < m of a tids layout:
+ *   tri[a*m - a*(a+1)/2 + (b-a-1)] += #{ j in [first, last] : row j holds a and b }
+ * (a-major, the order first_pass seeds pairs in, engine.py:165-168).  A
+ * register-blocked AND/POPC kernel over 64 x 64 blocks of the triangle; tri
+ * holds m*(m-1)/2 uint64 counts and is accumulated into.                  */
+int dic_count_pairs(const uint32_t* tids, int64_t n, int32_t m,
+                    int64_t first, int64_t last, uint64_t* tri, void* stream);
+/* The tids layout restricted to items[0..L) (in that order, L <= m); out
+ * holds dic_tids_words(n, L) words.  Lets dic_count_pairs run over the
+ * frequent items only.                                                    */
+int dic_tids_select(const uint32_t* tids, int64_t n, int32_t m,
+                    const int32_t* items, int32_t L, uint32_t* out, void* stream);
+
 /* The same count on the row bitmap, the literal `(T & I) == I` form of
  * _count_block (engine.py:54-56) for C multi-word masks [C][W].  Used as an
  * independent second kernel for parity checks and for callers that only

@@ -25,7 +25,7 @@ NVCC_FLAGS = ARCH + [
 ]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function"]
 
-CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "engine.cu", "probe.cu"]
+CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "probe.cu"]
 CPP_SOURCES = ["synth.cpp"]
 
 

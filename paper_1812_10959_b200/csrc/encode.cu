@@ -9,28 +9,64 @@
 
 namespace dic {
 
-// One thread per row: OR the row's ids into its W words, count duplicates,
-// and record the first out-of-range id in row-major order (atomicMin on the
-// CSR position, which orders rows first and then positions within a row —
-// exactly the id encode_transaction would raise on first).
-__global__ void encode_csr_kernel(const int64_t* __restrict__ indptr,
-                                  const int32_t* __restrict__ indices, int64_t n,
-                                  int32_t m, int W, unsigned long long* __restrict__ rows,
-                                  unsigned long long* __restrict__ status) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    int64_t b = indptr[r], e = indptr[r + 1];
-    unsigned long long* row = rows + r * (int64_t)W;
-    int64_t bad = -1;
-    for (int64_t q = b; q < e; ++q) {
-        int32_t it = indices[q];
-        if (it < 0 || it >= m) {
-            if (bad < 0) bad = q;
-            continue;
+// One thread per row: OR the row's ids into its W words held in registers
+// (W <= 16; wider rows fall back to atomicOr on the zeroed output), count the
+// duplicates (len - popcount) and record the first out-of-range id in
+// row-major order (atomicMin on the CSR position, which orders rows first and
+// then positions within a row — exactly the id encode_transaction would raise
+// on first).
+template <int W>
+__global__ void __launch_bounds__(256) encode_csr_kernel(const int64_t* __restrict__ indptr,
+                                                         const int32_t* __restrict__ indices, int64_t n, int32_t m,
+                                                         int Wd, unsigned long long* __restrict__ rows,
+                                                         unsigned long long* __restrict__ status) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long dup = 0;
+    if (r < n) {
+        const int64_t b = indptr[r], e = indptr[r + 1];
+        int64_t bad = -1;
+        if constexpr (W > 0) {
+            unsigned long long acc[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = 0;
+            int64_t nvalid = 0;
+            for (int64_t q = b; q < e; ++q) {
+                const int32_t it = __ldg(indices + q);
+                if (it < 0 || it >= m) {
+                    if (bad < 0) bad = q;
+                    continue;
+                }
+                ++nvalid;
+                const unsigned long long bit = 1ull << (it & 63);
+                const int wi = it >> 6;
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    if (w == wi) acc[w] |= bit;  // static register index
+            }
+            int64_t bits = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                rows[r * W + w] = acc[w];
+                bits += __popcll(acc[w]);
+            }
+            dup = (unsigned long long)(nvalid - bits);
+        } else {
+            unsigned long long* row = rows + r * (int64_t)Wd;  // zeroed by the caller
+            for (int64_t q = b; q < e; ++q) {
+                const int32_t it = indices[q];
+                if (it < 0 || it >= m) {
+                    if (bad < 0) bad = q;
+                    continue;
+                }
+                atomicOr(row + (it >> 6), 1ull << (it & 63));
+            }
         }
-        atomicOr(row + (it >> 6), 1ull << (it & 63));
+        if (bad >= 0) atomicMin(status + 1, (unsigned long long)bad);
     }
-    if (bad >= 0) atomicMin(status + 1, (unsigned long long)bad);
+    if constexpr (W > 0) {
+        for (int o = 16; o > 0; o >>= 1) dup += __shfl_down_sync(0xFFFFFFFFu, dup, o);
+        if ((threadIdx.x & 31) == 0 && dup) atomicAdd(status, dup);
+    }
 }
 
 __global__ void dedup_count_kernel(const int64_t* __restrict__ indptr, int64_t n, int W,
@@ -127,15 +163,23 @@ extern "C" int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int
     auto* st = reinterpret_cast<unsigned long long*>(status);
     init_status_kernel<<<1, 1, 0, s>>>(st); ::dic::note_launch();
     if (n == 0) { DIC_CHECK_LAUNCH("init_status_kernel"); return DIC_OK; }
-    DIC_CUDA(cudaMemsetAsync(rows, 0, (size_t)n * W * sizeof(uint64_t), s));
     const int T = 256;
-    int64_t blocks = (n + T - 1) / T;
-    encode_csr_kernel<<<(unsigned)blocks, T, 0, s>>>(indptr, indices, n, m, W,
-                                                     reinterpret_cast<unsigned long long*>(rows), st); ::dic::note_launch();
+    const int64_t blocks = (n + T - 1) / T;
+    auto* out = reinterpret_cast<unsigned long long*>(rows);
+    switch (W) {
+#define DIC_ENC(WW) \
+        case WW: encode_csr_kernel<WW><<<(unsigned)blocks, T, 0, s>>>(indptr, indices, n, m, W, out, st); break;
+        DIC_ENC(1) DIC_ENC(2) DIC_ENC(3) DIC_ENC(4) DIC_ENC(5) DIC_ENC(6) DIC_ENC(7) DIC_ENC(8)
+        DIC_ENC(9) DIC_ENC(10) DIC_ENC(11) DIC_ENC(12) DIC_ENC(13) DIC_ENC(14) DIC_ENC(15) DIC_ENC(16)
+#undef DIC_ENC
+        default:
+            DIC_CUDA(cudaMemsetAsync(rows, 0, (size_t)n * W * sizeof(uint64_t), s));
+            encode_csr_kernel<0><<<(unsigned)blocks, T, 0, s>>>(indptr, indices, n, m, W, out, st);
+            ::dic::note_launch();
+            dedup_count_kernel<<<(unsigned)blocks, T, 0, s>>>(indptr, n, W, out, st);
+    }
+    ::dic::note_launch();
     DIC_CHECK_LAUNCH("encode_csr_kernel");
-    dedup_count_kernel<<<(unsigned)blocks, T, 0, s>>>(
-        indptr, n, W, reinterpret_cast<const unsigned long long*>(rows), st); ::dic::note_launch();
-    DIC_CHECK_LAUNCH("dedup_count_kernel");
     finish_status_kernel<<<1, 1, 0, s>>>(indptr, n, st); ::dic::note_launch();
     DIC_CHECK_LAUNCH("finish_status_kernel");
     return DIC_OK;

@@ -51,6 +51,12 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
                          const BucketIn* bk, int nbk, cudaStream_t s);
 int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s);
+int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                       unsigned long long* tri, cudaStream_t s);
+int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
+                       cudaStream_t s);
+int pair_gather_launch(const uint16_t* items, int64_t C, const int32_t* rank, int64_t L,
+                       const unsigned long long* tri, unsigned long long* out, cudaStream_t s);
 
 enum : uint8_t { DASHED_CIRCLE = 0, DASHED_BOX = 1, SOLID_CIRCLE = 2, SOLID_BOX = 3, NIL = 4 };
 
@@ -482,6 +488,13 @@ struct dic_engine {
     int64_t* tmp_slot = nullptr;
     int64_t tmp_cap = 0;
 
+    // the pair bucket as a dense triangle over the frequent items (pairs.cu)
+    const uint32_t* pair_tids = nullptr;  // tids restricted to level1 (or tids itself)
+    uint32_t* pair_tids_own = nullptr;
+    int32_t* rank = nullptr;              // item -> position in level1, -1 if infrequent
+    unsigned long long* tri = nullptr;    // [L(L-1)/2] per-stop pair counts
+    int64_t tri_len = 0;
+
     int64_t live = 0;  // |dashed|
     bool seeded = false;
     bool counted = false;
@@ -745,6 +758,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->pos, s);
     dfree(e->scr_rec, s); dfree(e->scr_items, s); dfree(e->delta, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
+    dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s);
     if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, s);
     cudaStreamSynchronize(s);
     if (e->h_stat) cudaFreeHost(e->h_stat);
@@ -804,6 +818,24 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         dfree(d_rs, e->s);
         e->buckets[2].n = npairs;
     }
+    // dense pair counting over the frequent items
+    if (L >= 2 && e->n_local > 0) {
+        std::vector<int32_t> rank(m, -1);
+        for (int64_t a = 0; a < L; ++a) rank[l1[a]] = (int32_t)a;
+        if ((rc = dalloc(&e->rank, m, e->s))) return rc;
+        DIC_CUDA(cudaMemcpyAsync(e->rank, rank.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, e->s));
+        if (L == m) {
+            e->pair_tids = e->tids;  // every item frequent: level1 == identity
+        } else {
+            if ((rc = dalloc(&e->pair_tids_own, dic_tids_words(e->n_local, (int32_t)L), e->s))) return rc;
+            if ((rc = tids_select_launch(e->tids, e->n_local, m, e->level1, (int)L, e->pair_tids_own, e->s)))
+                return rc;
+            e->pair_tids = e->pair_tids_own;
+        }
+        e->tri_len = npairs;
+        if ((rc = dalloc(&e->tri, npairs, e->s))) return rc;
+        DIC_CUDA(cudaStreamSynchronize(e->s));  // rank vector dies at scope exit
+    }
     e->nrec = m + npairs;
     ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec);
     ::dic::note_launch();
@@ -836,11 +868,21 @@ extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
     if (tot > 0) DIC_CUDA(cudaMemsetAsync(e->delta, 0, tot * sizeof(unsigned long long), e->s));
     int64_t off = 0;
     std::vector<BucketIn> bk;
+    // the pair bucket goes through the dense triangle while most pairs are live
+    const bool dense_pairs = e->tri != nullptr && e->KS > 2 && e->buckets[2].n > 0 &&
+                             2 * e->buckets[2].n >= e->tri_len;
     for (size_t k = 0; k < e->buckets.size(); ++k) {
         const Bucket& b = e->buckets[k];
         e->delta_off[k] = off;
-        if (b.n > 0) bk.push_back(BucketIn{b.items, e->delta + off, b.n, (int)k});
+        if (b.n > 0 && !(k == 2 && dense_pairs)) bk.push_back(BucketIn{b.items, e->delta + off, b.n, (int)k});
         off += b.n;
+    }
+    if (dense_pairs && llast >= lfirst) {
+        DIC_CUDA(cudaMemsetAsync(e->tri, 0, e->tri_len * sizeof(unsigned long long), e->s));
+        if ((rc = count_pairs_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, e->s))) return rc;
+        if ((rc = pair_gather_launch(e->buckets[2].items, e->buckets[2].n, e->rank, e->nL1, e->tri,
+                                     e->delta + e->delta_off[2], e->s)))
+            return rc;
     }
     if (!bk.empty() && llast >= lfirst) {
         rc = count_buckets_launch(e->tids, e->n_local, e->m, lfirst, llast, bk.data(), (int)bk.size(), e->s);

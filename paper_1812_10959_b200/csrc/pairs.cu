@@ -1,0 +1,217 @@
+// pairs.cu — the 2-itemset bucket counted as a dense triangle.
+//
+// first_pass seeds EVERY pair of frequent items as a candidate
+// (engine.py:165-168), all in the same stop, so they are counted over the
+// same chunks and finalised together: for the configs' large universes this
+// C(|L1|, 2) wave is nearly all of the work (cfg4: 499,500 pairs x 10M rows).
+// Counting it pair by pair re-reads both item rows for every pair.  Here a
+// CTA owns a 64 x 64 block of the pair triangle and streams the chunk past it
+// like a GEMM's K dimension — but on the integer pipes (AND + POPC), no
+// tensor cores: each thread holds a 4 x 4 register tile of pair counters and
+// per 128 rows loads 4 + 4 item words (LDS.128) for 16 AND/POPC updates, so
+// shared-memory traffic per subset-test drops 8x and the POPC pipe is the
+// bound.  Row blocks of a tile are contiguous in the tiled layout, so each
+// operand block arrives by one bulk async copy (TMA engine), double-buffered.
+#include "async.cuh"
+
+namespace dic {
+
+constexpr int kPairBlock = 64;
+constexpr int kPairThreads = 256;  // 16 x 16 threads, a 4 x 4 pair tile each
+
+__host__ __device__ inline int64_t tri_index(int64_t a, int64_t b, int64_t m) {
+    // a < b < m, a-major: the order first_pass seeds pairs in
+    return a * m - a * (a + 1) / 2 + (b - a - 1);
+}
+
+template <int TW>
+__global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
+                                                                ChunkGeom geom, int64_t t_first, int64_t t_last,
+                                                                int64_t row_splits, int nblk,
+                                                                unsigned long long* __restrict__ tri) {
+    constexpr int RW = TW + 4;
+    constexpr int RB = RW * 4;
+    constexpr uint32_t BLK = kPairBlock * RB;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* buf = smem + 128;  // [2 stages][A block, B block]
+
+    int y = blockIdx.y, I = 0;
+    while (y >= nblk - I) {
+        y -= nblk - I;
+        ++I;
+    }
+    const int J = I + y;
+    const bool diag = I == J;
+    const int a0 = I * kPairBlock, b0 = J * kPairBlock;
+    const int na = min(kPairBlock, m - a0), nb = min(kPairBlock, m - b0);
+    const uint32_t abytes = (uint32_t)na * RB, bbytes = (uint32_t)nb * RB;
+    const int64_t tile_words = (int64_t)m * RW;
+    const int64_t nt = t_last - t_first + 1;
+    const int64_t t0 = t_first + nt * blockIdx.x / row_splits;
+    const int64_t t1 = t_first + nt * (blockIdx.x + 1) / row_splits;
+    if (t0 >= t1) return;
+
+    auto issue = [&](int64_t t, int s) {
+        uint8_t* dst = buf + (size_t)s * 2 * BLK;
+        const uint32_t* src = tids + t * tile_words;
+        mbar_expect_tx(&bar[s], abytes + (diag ? 0u : bbytes));
+        bulk_g2s(dst, src + (int64_t)a0 * RW, abytes, &bar[s]);
+        if (!diag) bulk_g2s(dst + BLK, src + (int64_t)b0 * RW, bbytes, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        issue(t0, 0);
+        if (t0 + 1 < t1) issue(t0 + 1, 1);
+    }
+    __syncthreads();
+
+    const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
+    uint32_t cnt[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cnt[i][j] = 0;
+
+    for (int64_t t = t0; t < t1; ++t) {
+        const int s = (int)((t - t0) & 1);
+        mbar_wait(&bar[s], (uint32_t)(((t - t0) >> 1) & 1));
+        uint8_t* A = buf + (size_t)s * 2 * BLK;
+        uint8_t* B = diag ? A : A + BLK;
+        if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
+            // chunk edge inside this tile: zero the rows outside [first, last]
+            const int rows = diag ? na : 2 * kPairBlock;
+            for (int idx = threadIdx.x; idx < rows * RW; idx += kPairThreads) {
+                const int r = idx / RW, slot = idx - r * RW;
+                if (slot >= TW || (r < kPairBlock ? r >= na : r - kPairBlock >= nb)) continue;
+                uint32_t* w = reinterpret_cast<uint32_t*>(A + (size_t)r * RB) + slot;
+                *w &= group_mask(geom, t * TW + slot);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < TW / 4; ++q) {
+            uint4 av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cnt[i][j] += popc4(and4(av[i], bv[j]));
+        }
+        __syncthreads();  // stage s consumed
+        if (threadIdx.x == 0 && t + 2 < t1) {
+            fence_proxy_async();
+            issue(t + 2, s);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int a = a0 + ta + 16 * i, b = b0 + tb + 16 * j;
+            if (a < b && b < m && cnt[i][j]) atomicAdd(tri + tri_index(a, b, m), (unsigned long long)cnt[i][j]);
+        }
+}
+
+// Bit-sliced copy restricted to the selected items (in the given order).
+__global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, int m,
+                                   const int32_t* __restrict__ items, int L, uint32_t* __restrict__ dst) {
+    const int TWs = tile_groups(m), TWd = tile_groups(L);
+    const int RWd = row_words(TWd);
+    const int64_t src_groups = tile_count(n, m) * TWs;
+    const int64_t total = tile_count(n, L) * (int64_t)L * RWd;
+    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < total; d += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = d / ((int64_t)L * RWd);
+        const int64_t rem = d - t * L * RWd;
+        const int r = (int)(rem / RWd), slot = (int)(rem - (int64_t)r * RWd);
+        uint32_t v = 0;
+        const int64_t g = t * TWd + slot;
+        if (slot < TWd && g < src_groups) v = src[tids_index(m, TWs, (uint32_t)items[r], g)];
+        dst[d] = v;
+    }
+}
+
+// delta[c] = tri[pair of bucket slot c] (ranks of its two items among L1)
+__global__ void pair_gather_kernel(const uint16_t* __restrict__ items, int64_t C, const int32_t* __restrict__ rank,
+                                   int64_t L, const unsigned long long* __restrict__ tri,
+                                   unsigned long long* __restrict__ out) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+        const int a = rank[items[2 * c]], b = rank[items[2 * c + 1]];
+        out[c] += tri[tri_index(a, b, L)];
+    }
+}
+
+static int g_pair_attr = 0;
+
+int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                       unsigned long long* tri, cudaStream_t s) {
+    if (last < first || m < 2) return DIC_OK;
+    const int TW = tile_groups(m);
+    const ChunkGeom geom = chunk_geom(first, last);
+    const int64_t t_first = geom.g_first / TW, t_last = geom.g_last / TW;
+    const int64_t nt = t_last - t_first + 1;
+    const int nblk = (m + kPairBlock - 1) / kPairBlock;
+    const int64_t blocks = (int64_t)nblk * (nblk + 1) / 2;
+    DIC_REQUIRE(blocks <= 65535, "count_pairs: %lld block pairs exceed one launch", (long long)blocks);
+    const size_t smem = 128 + 2 * 2 * (size_t)kPairBlock * row_words(TW) * 4;
+    if (!g_pair_attr) {
+        DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        g_pair_attr = 1;
+    }
+    // about four resident CTAs per SM
+    const int64_t target = 4LL * sm_count();
+    int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (target + blocks - 1) / blocks));
+    dim3 grid((unsigned)rs, (unsigned)blocks);
+    if (TW == 32)
+        pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri);
+    else
+        pair_tri_kernel<16><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("pair_tri_kernel");
+    return DIC_OK;
+}
+
+int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
+                       cudaStream_t s) {
+    const int64_t total = tile_count(n, L) * (int64_t)L * row_words(tile_groups(L));
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+    tids_select_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(src, n, m, items, L, dst);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("tids_select_kernel");
+    return DIC_OK;
+}
+
+int pair_gather_launch(const uint16_t* items, int64_t C, const int32_t* rank, int64_t L,
+                       const unsigned long long* tri, unsigned long long* out, cudaStream_t s) {
+    if (C <= 0) return DIC_OK;
+    const int64_t blocks = std::min<int64_t>((C + 255) / 256, (int64_t)sm_count() * 8);
+    pair_gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(items, C, rank, L, tri, out);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("pair_gather_kernel");
+    return DIC_OK;
+}
+
+}  // namespace dic
+
+using namespace dic;
+
+extern "C" int dic_count_pairs(const uint32_t* tids, int64_t n, int32_t m, int64_t first, int64_t last,
+                               uint64_t* tri, void* stream) {
+    DIC_REQUIRE(m >= 2 && m <= 65535 && tids && tri, "dic_count_pairs: bad arguments (m=%d)", m);
+    DIC_REQUIRE(0 <= first && first <= last && last < n, "chunk [%lld, %lld] outside database of %lld rows",
+                (long long)first, (long long)last, (long long)n);
+    return count_pairs_launch(tids, n, m, first, last, reinterpret_cast<unsigned long long*>(tri),
+                              as_stream(stream));
+}
+
+extern "C" int dic_tids_select(const uint32_t* tids, int64_t n, int32_t m, const int32_t* items, int32_t L,
+                               uint32_t* out, void* stream) {
+    DIC_REQUIRE(n >= 1 && m >= 1 && L >= 1 && L <= m && tids && items && out, "dic_tids_select: bad arguments");
+    return tids_select_launch(tids, n, m, items, L, out, as_stream(stream));
+}

@@ -80,6 +80,22 @@ def count_support(tids: torch.Tensor, n: int, m: int, first: int, last: int, ite
     return out
 
 
+def count_pairs(tids: torch.Tensor, n: int, m: int, first: int, last: int,
+                tri: torch.Tensor | None = None) -> torch.Tensor:
+    """Counts of all pairs a < b < m over rows [first, last], a-major triangle (int64)."""
+    if tri is None:
+        tri = torch.zeros(m * (m - 1) // 2, dtype=torch.int64, device=tids.device)
+    _abi.call("dic_count_pairs", _ptr(tids), n, m, first, last, _ptr(tri), _stream())
+    return tri
+
+
+def tids_select(tids: torch.Tensor, n: int, m: int, items: torch.Tensor) -> torch.Tensor:
+    L = items.numel()
+    out = torch.empty(max(tids_words(n, L), 1), dtype=torch.int32, device=tids.device)
+    _abi.call("dic_tids_select", _ptr(tids), n, m, _ptr(items), L, _ptr(out), _stream())
+    return out
+
+
 def count_support_rows(rows: torch.Tensor, first: int, last: int, masks: torch.Tensor,
                        out: torch.Tensor | None = None) -> torch.Tensor:
     Cn, W = masks.shape

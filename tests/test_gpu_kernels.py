@@ -145,3 +145,32 @@ def test_bad_chunk_rejected():
         D.count_support(tids, 2, 2, 1, 0, to_dev(np.array([[0]], dtype=np.int16)))
     with pytest.raises(D._abi.DicError):
         D.count_support(tids, 2, 2, 0, 2, to_dev(np.array([[0]], dtype=np.int16)))
+
+
+@pytest.mark.parametrize("m,n,density,first,last", [
+    (64, 5000, 0.3, 0, 4999), (100, 3000, 0.4, 17, 2900), (700, 40000, 0.05, 123, 39000),
+    (1000, 30000, 0.03, 0, 29999), (130, 33, 0.5, 3, 31), (2, 100, 0.5, 0, 99)])
+def test_count_pairs_matches_numpy(m, n, density, first, last):
+    rng = np.random.default_rng(m + n)
+    rows = random_rows(rng, n, m, density)
+    tids = D.rows_to_tids(to_dev(rows), n, m)
+    tri = D.count_pairs(tids, n, m, first, last).cpu().numpy()
+    blk = rows[first:last + 1]
+    bitsm = np.stack([(blk[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1) for i in range(m)], axis=1).astype(np.float64)
+    gram = bitsm.T @ bitsm
+    iu = np.triu_indices(m, k=1)  # a-major order == tri_index
+    assert np.array_equal(tri, gram[iu].astype(np.int64))
+
+
+def test_tids_select_then_pairs():
+    rng = np.random.default_rng(9)
+    m, n = 900, 20000
+    rows = random_rows(rng, n, m, 0.05)
+    tids = D.rows_to_tids(to_dev(rows), n, m)
+    items = np.sort(rng.choice(m, size=300, replace=False)).astype(np.int32)
+    sub = D.tids_select(tids, n, m, to_dev(items))
+    tri = D.count_pairs(sub, n, 300, 5, n - 2).cpu().numpy()
+    blk = rows[5:n - 1]
+    bitsm = np.stack([(blk[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1) for i in items], axis=1).astype(np.float64)
+    gram = bitsm.T @ bitsm
+    assert np.array_equal(tri, gram[np.triu_indices(300, k=1)].astype(np.int64))
