@@ -200,6 +200,22 @@ int dic_engine_delta(dic_engine* e, void** ptr, int64_t* len);
 /* Per stop, step 2: support += delta, intervals += 1, prune, make
  * candidates, check_full_pass, compact.  Synchronising; fills *st.       */
 int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st);
+/* Pipelined form of the same loop (what mine_parallel uses).  Every kernel
+ * of a stop reads its sizes from device memory, so the host can enqueue stop
+ * s while stop s-D is still running:
+ *   dic_engine_issue_count(e, lfirst, llast)   count into the delta buffer
+ *   [sum-allreduce of dic_engine_delta() across ranks, same stream]
+ *   dic_engine_issue_checkpoint(e, &seq)       apply / prune / candidates
+ *   dic_engine_poll(e, seq, &st, &replayed)    wait for stop seq, in order
+ * A stop whose new candidates do not fit raises a device abort flag that
+ * turns every later kernel into a no-op; poll() then grows the arrays,
+ * replays that stop's candidate step and sets *replayed = 1: the caller
+ * must re-issue every stop after seq.  At most 15 stops in flight.
+ * dic_engine_delta's length is the (rank-independent) slot capacity.      */
+int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t llast);
+int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq);
+int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st,
+                    int32_t* replayed);
 /* Results: number of SOLID_BOX records, then copy them out to HOST arrays
  * masks[F][W] (uint64), sizes[F], supports[F] (unsorted).  Synchronising. */
 int dic_engine_num_frequent(dic_engine* e, int64_t* F);

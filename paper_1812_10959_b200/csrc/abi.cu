@@ -19,6 +19,21 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+// Keep freed stream-ordered allocations in the device pool (the default
+// release threshold of 0 hands memory back to the driver at every sync,
+// turning each engine's allocations into cudaMalloc calls).
+void retain_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
 int sm_count() {
     static int cached = -1;
     if (cached < 0) {

@@ -25,6 +25,7 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+void retain_pool();
 // Count of kernels this library launched (dic_launch_count()).
 void note_launch();
 

@@ -88,31 +88,46 @@ __host__ __device__ constexpr int regs_per_thread(int K) {
     return K == 0 ? 2 : (K <= 2 ? 16 : (K <= 4 ? 8 : (K <= 6 ? 5 : 4)));
 }
 
+// Stage tile t into buffer `stage` (thread 0; one bulk async copy).
+__device__ __forceinline__ void issue_tile(uint8_t* smem, const uint32_t* tids, uint32_t tb, int64_t t, int stage) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    mbar_expect_tx(&bar[stage], tb);
+    bulk_g2s(smem + 128 + (size_t)stage * tb, tids + t * (int64_t)(tb / 4), tb, &bar[stage]);
+}
+
+// One work unit: candidates [blk*512*R, +512*R) of a size-k bucket against
+// tiles [t0, t1).  All threads enter; the two mbarriers are initialised and
+// idle; uses[s] counts the completed phases of barrier s (the wait parity),
+// so units can follow each other without re-initialising.
 template <int K, int TW>
-__device__ __forceinline__ void stream_body(const StreamArgs& a, const BucketDesc& B, int64_t blk, int64_t t0,
-                                            int64_t t1, uint8_t* smem) {
+__device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, int m, uint32_t tb,
+                                            const ChunkGeom& geom, const uint16_t* __restrict__ items, int kdyn,
+                                            int64_t C, unsigned long long* __restrict__ out, int64_t blk,
+                                            int64_t t0, int64_t t1, uint8_t* smem, uint32_t (&uses)[2]) {
     constexpr int R = regs_per_thread(K);
     constexpr int KK = K > 0 ? K : 1;
-    constexpr int CH = TW / 4;  // 16-byte chunks per item row
+    constexpr int CH = TW / 4;        // 16-byte chunks per item row
     constexpr int RB = (TW + 4) * 4;  // row stride in bytes
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
-    const uint32_t tb = a.tile_bytes;
     const int64_t cbase = blk * (int64_t)kStreamThreads * R;
-    const int k = K > 0 ? K : B.k;
+    const int k = K > 0 ? K : kdyn;
 
+    if (threadIdx.x == 0) {
+        fence_proxy_async();  // earlier generic writes (edge masking) before the async refill
+        issue_tile(smem, tids, tb, t0, 0);
+        if (t0 + 1 < t1) issue_tile(smem, tids, tb, t0 + 1, 1);
+    }
     uint32_t off[R][KK];
     uint32_t cnt[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
-        int64_t cc = c < B.C ? c : B.C - 1;
+        int64_t cc = c < C ? c : C - 1;
         cnt[r] = 0;
         if constexpr (K > 0) {
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                off[r][j] = (uint32_t)__ldg(B.items + cc * K + j) * RB;
-            }
+            for (int j = 0; j < K; ++j) off[r][j] = (uint32_t)__ldg(items + cc * K + j) * RB;
         } else {
             off[r][0] = (uint32_t)cc;
         }
@@ -120,14 +135,15 @@ __device__ __forceinline__ void stream_body(const StreamArgs& a, const BucketDes
 
     for (int64_t t = t0; t < t1; ++t) {
         const int s = (int)((t - t0) & 1);
-        mbar_wait(&bar[s], (uint32_t)(((t - t0) >> 1) & 1));
+        mbar_wait(&bar[s], uses[s] & 1u);
+        ++uses[s];
         uint8_t* base = bufs + (size_t)s * tb;
         // tiles holding a chunk edge: zero the rows outside [first, last]
-        if (t * TW <= a.geom.g_first || t * TW + TW - 1 >= a.geom.g_last) {
+        if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
-            for (int idx = threadIdx.x; idx < a.m * (TW + 4); idx += kStreamThreads) {
+            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += kStreamThreads) {
                 int item = idx / (TW + 4), slot = idx - item * (TW + 4);
-                if (slot < TW) w[idx] &= group_mask(a.geom, t * TW + slot);
+                if (slot < TW) w[idx] &= group_mask(geom, t * TW + slot);
             }
             __syncthreads();
         }
@@ -143,7 +159,7 @@ __device__ __forceinline__ void stream_body(const StreamArgs& a, const BucketDes
                     cnt[r] += popc4(v);
                 }
             } else {
-                const uint16_t* it = B.items + (int64_t)off[r][0] * k;
+                const uint16_t* it = items + (int64_t)off[r][0] * k;
                 for (int q = 0; q < CH; ++q) {
                     uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
                     for (int j = 0; j < k; ++j) {
@@ -157,17 +173,45 @@ __device__ __forceinline__ void stream_body(const StreamArgs& a, const BucketDes
         __syncthreads();  // buffer s fully consumed
         if (threadIdx.x == 0 && t + 2 < t1) {
             fence_proxy_async();
-            mbar_expect_tx(&bar[s], tb);
-            bulk_g2s(base, a.tids + (t + 2) * (int64_t)(tb / 4), tb, &bar[s]);
+            issue_tile(smem, tids, tb, t + 2, s);
         }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
-        if (c < B.C && cnt[r]) atomicAdd(B.out + c, (unsigned long long)cnt[r]);
+        if (c < C && cnt[r]) atomicAdd(out + c, (unsigned long long)cnt[r]);
     }
 }
 
+template <int TW>
+__device__ __forceinline__ void dispatch_unit(int k, const uint32_t* tids, int m, uint32_t tb, const ChunkGeom& geom,
+                                              const uint16_t* items, int64_t C, unsigned long long* out,
+                                              int64_t blk, int64_t t0, int64_t t1, uint8_t* smem,
+                                              uint32_t (&uses)[2]) {
+    switch (k) {
+        case 1: stream_unit<1, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 2: stream_unit<2, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 3: stream_unit<3, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 4: stream_unit<4, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 5: stream_unit<5, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 6: stream_unit<6, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 7: stream_unit<7, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        case 8: stream_unit<8, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+        default: stream_unit<0, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
+    }
+}
+
+__device__ __forceinline__ void init_barriers(uint8_t* smem) {
+    if (threadIdx.x == 0) {
+        uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+// Host-sized launch (the dic_count_support API): grid = (row splits, blocks).
 template <int TW>
 __global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const __grid_constant__ StreamArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -182,28 +226,67 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const _
     const int64_t t0 = a.t_first + nt * blockIdx.x / a.row_splits;
     const int64_t t1 = a.t_first + nt * (blockIdx.x + 1) / a.row_splits;
     if (t0 >= t1) return;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    init_barriers(smem);
+    uint32_t uses[2] = {0u, 0u};
+    dispatch_unit<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
+}
+
+// Device-sized launch (the engine's per-stop count): bucket sizes, delta
+// offsets and the dense-pair switch are read from device memory, so the
+// host can enqueue stops without knowing the sizes.  A persistent grid walks
+// the (candidate block, row split) units of every bucket.
+constexpr int kDevMaxK = 64;
+struct DevCountArgs {
+    const uint32_t* tids;
+    int32_t m, TW;
+    uint32_t tile_bytes;
+    int64_t t_first, t_last;
+    ChunkGeom geom;
+    int32_t kuse;                     // buckets 1..kuse-1 may be non-empty
+    uint16_t* const* items_tab;       // per-size item arrays
+    const unsigned long long* bn;     // per-size bucket fill
+    const int64_t* doff;              // per-size delta offsets
+    unsigned long long* delta;
+    const unsigned long long* abort;  // non-zero: stop skipped (overflow recovery)
+    int64_t tri_len;                  // > 0: bucket 2 counted densely when 2*bn[2] >= tri_len
+};
+
+template <int TW>
+__global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __grid_constant__ DevCountArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ int64_t pref[kDevMaxK + 1];
+    if (*a.abort) return;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-        for (int s = 0; s < 2 && t0 + s < t1; ++s) {
-            mbar_expect_tx(&bar[s], a.tile_bytes);
-            bulk_g2s(smem + 128 + (size_t)s * a.tile_bytes, a.tids + (t0 + s) * (int64_t)(a.tile_bytes / 4),
-                     a.tile_bytes, &bar[s]);
+        const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
+        int64_t acc = 0;
+        pref[0] = 0;
+        for (int k = 1; k < a.kuse; ++k) {
+            int64_t C = (int64_t)a.bn[k];
+            if (k == 2 && dense) C = 0;
+            const int64_t per = (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
+            pref[k] = acc;
+            acc += (C + per - 1) / per;
         }
+        pref[a.kuse] = acc;
     }
     __syncthreads();
-    switch (B.k) {
-        case 1: stream_body<1, TW>(a, B, blk, t0, t1, smem); break;
-        case 2: stream_body<2, TW>(a, B, blk, t0, t1, smem); break;
-        case 3: stream_body<3, TW>(a, B, blk, t0, t1, smem); break;
-        case 4: stream_body<4, TW>(a, B, blk, t0, t1, smem); break;
-        case 5: stream_body<5, TW>(a, B, blk, t0, t1, smem); break;
-        case 6: stream_body<6, TW>(a, B, blk, t0, t1, smem); break;
-        case 7: stream_body<7, TW>(a, B, blk, t0, t1, smem); break;
-        case 8: stream_body<8, TW>(a, B, blk, t0, t1, smem); break;
-        default: stream_body<0, TW>(a, B, blk, t0, t1, smem); break;
+    const int64_t B = pref[a.kuse];
+    if (B == 0) return;
+    const int64_t nt = a.t_last - a.t_first + 1;
+    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)gridDim.x / B));
+    const int64_t U = B * rs;
+    if ((int64_t)blockIdx.x >= U) return;
+    init_barriers(smem);
+    uint32_t uses[2] = {0u, 0u};
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+        const int64_t gb = u / rs, r = u - gb * rs;
+        int k = 1;
+        while (pref[k + 1] <= gb) ++k;
+        const int64_t t0 = a.t_first + nt * r / rs, t1 = a.t_first + nt * (r + 1) / rs;
+        if (t0 < t1)
+            dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, a.geom, a.items_tab[k], (int64_t)a.bn[k],
+                              a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+        __syncthreads();
     }
 }
 
@@ -234,6 +317,39 @@ __global__ void __launch_bounds__(256) count_global_kernel(const uint32_t* __res
             cnt += popc4(v);
         }
         if (cnt) atomicAdd(out + c, (unsigned long long)cnt);
+    }
+}
+
+// Device-sized fallback for universes too wide to stage (and for > 64
+// itemset sizes): grid-stride over (bucket, candidate, tile) with plain loads.
+__global__ void __launch_bounds__(256) count_dev_global_kernel(const __grid_constant__ DevCountArgs a) {
+    if (*a.abort) return;
+    const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
+    const int TW = a.TW, RW = row_words(TW);
+    const int64_t nt = a.t_last - a.t_first + 1;
+    const int64_t tw_words = (int64_t)a.m * RW;
+    for (int k = 1; k < a.kuse; ++k) {
+        const int64_t C = (k == 2 && dense) ? 0 : (int64_t)a.bn[k];
+        const uint16_t* items = a.items_tab[k];
+        unsigned long long* out = a.delta + a.doff[k];
+        for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < C * nt;
+             w += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t c = w / nt, t = a.t_first + (w - c * nt);
+            uint32_t cnt = 0;
+            for (int q = 0; q < TW / 4; ++q) {
+                const int64_t g = t * TW + q * 4;
+                if (g > a.geom.g_last || g + 3 < a.geom.g_first) continue;
+                uint4 v = make_uint4(group_mask(a.geom, g), group_mask(a.geom, g + 1), group_mask(a.geom, g + 2),
+                                     group_mask(a.geom, g + 3));
+                for (int j = 0; j < k; ++j) {
+                    const uint32_t item = __ldg(items + c * k + j);
+                    const uint4* row = reinterpret_cast<const uint4*>(a.tids + t * tw_words + (int64_t)item * RW);
+                    v = and4(v, __ldg(row + q));
+                }
+                cnt += popc4(v);
+            }
+            if (cnt) atomicAdd(out + c, (unsigned long long)cnt);
+        }
     }
 }
 
@@ -327,6 +443,55 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
         ::dic::note_launch();
         DIC_CHECK_LAUNCH("count_stream_kernel");
     }
+    return DIC_OK;
+}
+
+// The engine's per-stop count: device-sized, no host knowledge of bucket sizes.
+int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
+                     uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
+                     unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
+                     cudaStream_t s) {
+    if (last < first) return DIC_OK;
+    DevCountArgs a;
+    memset(&a, 0, sizeof(a));
+    a.tids = tids;
+    a.m = m;
+    a.TW = tile_groups(m);
+    a.tile_bytes = (uint32_t)((size_t)m * row_words(a.TW) * 4);
+    a.geom = chunk_geom(first, last);
+    a.t_first = a.geom.g_first / a.TW;
+    a.t_last = a.geom.g_last / a.TW;
+    a.kuse = kuse;
+    a.items_tab = items_tab;
+    a.bn = bn;
+    a.doff = doff;
+    a.delta = delta;
+    a.abort = abort_flag;
+    a.tri_len = tri_len;
+    const size_t smem = 128 + 2 * (size_t)a.tile_bytes;
+    if (smem > (size_t)max_dyn_smem() || kuse > kDevMaxK) {
+        count_dev_global_kernel<<<sm_count() * 8, 256, 0, s>>>(a);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("count_dev_global_kernel");
+        return DIC_OK;
+    }
+    static bool attr32 = false, attr16 = false;
+    if (a.TW == 32 && !attr32) {
+        DIC_CUDA(cudaFuncSetAttribute(count_dev_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_dyn_smem()));
+        attr32 = true;
+    }
+    if (a.TW == 16 && !attr16) {
+        DIC_CUDA(cudaFuncSetAttribute(count_dev_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_dyn_smem()));
+        attr16 = true;
+    }
+    if (a.TW == 32)
+        count_dev_kernel<32><<<sm_count(), kStreamThreads, smem, s>>>(a);
+    else
+        count_dev_kernel<16><<<sm_count(), kStreamThreads, smem, s>>>(a);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("count_dev_kernel");
     return DIC_OK;
 }
 

@@ -18,12 +18,16 @@
 //             (itemsets.py:130-132).
 //   frontier  record ids promoted to DASHED_BOX at this stop (prune's return).
 //
-// One host synchronisation per stop: every kernel of a checkpoint reads its
-// sizes from device memory (grid-stride loops), capacities are checked on
-// the device (an overflow skips the state change and the host grows and
-// replays the candidate step), and entries that leave the dashed vector stay
-// in their bucket as dead slots — skipped by the apply kernel — until the
-// next checkpoint compacts that bucket.
+// Pipelined stops.  Every kernel of a stop reads its sizes from device
+// memory (bucket fill, delta offsets, frontier size), so the host enqueues
+// stop s without knowing the outcome of stop s-1: it processes the status of
+// stop s-D (copied into a pinned ring) while the GPU runs stops s-D+1..s.
+// Capacities are checked on the device; a stop whose candidate step would
+// overflow sets an abort flag that turns every later kernel into a no-op,
+// and the host (at the poll of that stop) grows the arrays, replays the
+// candidate step and re-issues the aborted stops.  Slots that leave the
+// dashed vector stay in their bucket as dead entries (skipped by the apply
+// kernel) until the host schedules that bucket's compaction.
 //
 // Phase fusion (exactness argued in DESIGN.md §4): check_full_pass runs in
 // the same kernel as prune because finalisation never changes box-ness
@@ -35,28 +39,24 @@
 // engine omits it; the API-level prune on host catalogs keeps it.
 #include "common.cuh"
 
-#include <cub/device/device_scan.cuh>
-
 #include <vector>
 
 namespace dic {
 
-struct BucketIn {
-    const uint16_t* items;
-    unsigned long long* out;
-    int64_t C;
-    int k;
-};
-int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
-                         const BucketIn* bk, int nbk, cudaStream_t s);
+int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
+                     uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
+                     unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
+                     cudaStream_t s);
 int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s);
-int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
-                       unsigned long long* tri, cudaStream_t s);
+int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                           unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
+                           const unsigned long long* abort_flag, cudaStream_t s);
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
                        cudaStream_t s);
-int pair_gather_launch(const uint16_t* items, int64_t C, const int32_t* rank, int64_t L,
-                       const unsigned long long* tri, unsigned long long* out, cudaStream_t s);
+int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
+                           const int32_t* rank, int64_t L, const unsigned long long* tri,
+                           unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s);
 
 enum : uint8_t { DASHED_CIRCLE = 0, DASHED_BOX = 1, SOLID_CIRCLE = 2, SOLID_BOX = 3, NIL = 4 };
 
@@ -70,8 +70,7 @@ __host__ __device__ inline uint64_t zob(uint32_t item) {
 constexpr int32_t kEmpty = -1;
 constexpr int32_t kTempFlag = 0x40000000;
 
-// Status words (device, one contiguous u64 array; the host reads a prefix
-// of each section once per stop).
+// Status words (device, one contiguous u64 array).
 enum : int {
     S_NFRONT = 0,    // promoted DASHED_CIRCLE -> DASHED_BOX
     S_NPRUNED = 1,   // DASHED_CIRCLE -> NIL by the bound
@@ -79,9 +78,11 @@ enum : int {
     S_SURV = 3,      // live dashed entries after prune (before finalisation)
     S_NADM = 4,      // admissible joins (before dedup)
     S_NINS = 5,      // distinct new candidates committed
-    S_OVERFLOW = 6,  // a capacity check failed: candidate step not applied
-    S_NREC = 7,      // records (persistent across stops)
-    S_HEAD = 8
+    S_OVERFLOW = 6,  // this stop's candidate step did not fit (not applied)
+    S_NREC = 7,      // records (persistent)
+    S_ABORT = 8,     // persistent: set with OVERFLOW, cleared by the host's replay
+    S_SCRATCH = 9,   // scratch word (result collection)
+    S_HEAD = 10
 };
 // followed by: removed[KS] (slots not kept this stop), adm[KS] (admitted
 // joins by size), bn[KS] (bucket fill, persistent), KS = m + 2.
@@ -133,12 +134,14 @@ __global__ void ht_clear_kernel(int32_t* ht, int64_t cap) {
         ht[i] = kEmpty;
 }
 
-// Insert records [r0, r1) (known to be distinct) into the hash index.
-__global__ void ht_insert_records_kernel(int32_t* ht, uint64_t hmask, Records R, int64_t r0, int64_t r1) {
-    int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= r1) return;
-    uint64_t slot = mix64(R.hash[r]) & hmask;
-    while (atomicCAS(ht + slot, kEmpty, (int32_t)r) != kEmpty) slot = (slot + 1) & hmask;
+// Insert records [0, *nrec) — the device count, so a rebuild enqueued behind
+// in-flight stops sees their records too.
+__global__ void ht_insert_records_kernel(int32_t* ht, uint64_t hmask, Records R, const unsigned long long* nrec) {
+    const int64_t n = (int64_t)*nrec;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t slot = mix64(R.hash[r]) & hmask;
+        while (atomicCAS(ht + slot, kEmpty, (int32_t)r) != kEmpty) slot = (slot + 1) & hmask;
+    }
 }
 
 // Singletons: record i = item i (first_pass, engine.py:125-163).
@@ -186,94 +189,133 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// per stop
+// per stop (every kernel: no-op while the abort flag is up)
 // ---------------------------------------------------------------------------
-constexpr int kMaxApply = 16;
-struct ApplyArgs {
-    int nb;
-    int32_t k[kMaxApply];
-    const int32_t* rec[kMaxApply];
-    int64_t off[kMaxApply];  // slot offset of bucket i within this launch
-    int64_t total;
-};
+// Reset the per-stop counters and compute the delta offsets of the buckets.
+__global__ void stop_prep_kernel(unsigned long long* stat, int KS, int kuse, int64_t* doff) {
+    if (stat[S_ABORT]) return;
+    for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
+    for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
+        stat[S_HEAD + k] = 0;       // removed
+        stat[S_HEAD + KS + k] = 0;  // adm
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long* bn = stat + S_HEAD + 2 * KS;
+        int64_t acc = 0;
+        for (int k = 0; k < kuse; ++k) {
+            doff[k] = acc;
+            acc += (int64_t)bn[k];
+        }
+        doff[kuse] = acc;
+    }
+}
 
 // support += delta, intervals += 1 (count_support_interval), then prune
-// (engine.py:292-310) and check_full_pass (:380-388).  Slots already dead
-// (left the dashed vector at an earlier stop, compaction pending) are only
-// marked not-kept.  keep[c] = still dashed.
-__global__ void apply_prune_finalize_kernel(const __grid_constant__ ApplyArgs a,
-                                            const unsigned long long* __restrict__ delta, Records R, int64_t need,
-                                            int64_t interval, int64_t stop_max, int bound,
+// (engine.py:292-310) and check_full_pass (:380-388), grid-stride over every
+// bucket slot.  Slots already dead (left the dashed vector at an earlier
+// stop, compaction pending) are only marked not-kept.  keep[g] = still dashed.
+__global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab, const int64_t* __restrict__ doff,
+                                            int kuse, const unsigned long long* __restrict__ delta, Records R,
+                                            int64_t need, int64_t interval, int64_t stop_max, int bound,
                                             int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
                                             unsigned long long* __restrict__ stat) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool pruned = false, fin = false, surv = false, gone = false;
-    int bk = 0;
-    if (g < a.total) {
-        while (bk + 1 < a.nb && g >= a.off[bk + 1]) ++bk;
-        const int64_t c = g - a.off[bk];
-        const int32_t r = a.rec[bk][c];
-        uint8_t sh = R.shape[r];
-        bool kept = false;
-        if (is_dashed(sh)) {
-            const int64_t s = R.support[r] + (int64_t)delta[g];
-            const int64_t iv = R.intervals[r] + 1;
-            R.support[r] = s;
-            R.intervals[r] = iv;
-            if (sh == DASHED_CIRCLE) {
-                if (s >= need) {
-                    sh = DASHED_BOX;
-                    // order among promoted records is irrelevant to results and stats
-                    frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r;
-                } else if (bound && iv < stop_max && s + interval * (stop_max - iv) < need) {
-                    sh = NIL;
-                    pruned = true;
-                }
-            }
+    if (stat[S_ABORT]) return;
+    const int64_t total = doff[kuse];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t span = ((total + stride - 1) / stride) * stride;  // uniform trip count for the warp votes
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < span; g += stride) {
+        bool pruned = false, fin = false, surv = false, gone = false;
+        int bk = 0;
+        if (g < total) {
+            while (bk + 1 < kuse && g >= doff[bk + 1]) ++bk;
+            const int32_t r = rec_tab[bk][g - doff[bk]];
+            uint8_t sh = R.shape[r];
+            bool kept = false;
             if (is_dashed(sh)) {
-                surv = true;
-                if (iv == stop_max) {
-                    sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
-                    fin = true;
+                const int64_t s = R.support[r] + (int64_t)delta[g];
+                const int64_t iv = R.intervals[r] + 1;
+                R.support[r] = s;
+                R.intervals[r] = iv;
+                if (sh == DASHED_CIRCLE) {
+                    if (s >= need) {
+                        sh = DASHED_BOX;
+                        // order among promoted records is irrelevant to results and stats
+                        frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r;
+                    } else if (bound && iv < stop_max && s + interval * (stop_max - iv) < need) {
+                        sh = NIL;
+                        pruned = true;
+                    }
                 }
+                if (is_dashed(sh)) {
+                    surv = true;
+                    if (iv == stop_max) {
+                        sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
+                        fin = true;
+                    }
+                }
+                R.shape[r] = sh;
+                kept = is_dashed(sh);
             }
-            R.shape[r] = sh;
-            kept = is_dashed(sh);
+            keep[g] = kept ? 1 : 0;
+            gone = !kept;
         }
-        keep[g] = kept ? 1 : 0;
-        gone = !kept;
+        const unsigned full = 0xFFFFFFFFu;
+        const unsigned pr = __ballot_sync(full, pruned), fi = __ballot_sync(full, fin);
+        const unsigned su = __ballot_sync(full, surv);
+        if ((threadIdx.x & 31) == 0) {
+            if (pr) atomicAdd(&stat[S_NPRUNED], (unsigned long long)__popc(pr));
+            if (fi) atomicAdd(&stat[S_NFINAL], (unsigned long long)__popc(fi));
+            if (su) atomicAdd(&stat[S_SURV], (unsigned long long)__popc(su));
+        }
+        // removed[k], aggregated over the lanes of the same bucket
+        const unsigned gm = __ballot_sync(full, gone);
+        if (gone) {
+            const unsigned same = __match_any_sync(gm, bk);
+            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&stat[S_HEAD + bk], (unsigned long long)__popc(same));
+        }
     }
-    const unsigned full = 0xFFFFFFFFu;
-    unsigned pr = __ballot_sync(full, pruned), fi = __ballot_sync(full, fin), su = __ballot_sync(full, surv);
-    if ((threadIdx.x & 31) == 0) {
-        if (pr) atomicAdd(&stat[S_NPRUNED], (unsigned long long)__popc(pr));
-        if (fi) atomicAdd(&stat[S_NFINAL], (unsigned long long)__popc(fi));
-        if (su) atomicAdd(&stat[S_SURV], (unsigned long long)__popc(su));
-    }
-    if (gone) atomicAdd(&stat[S_HEAD + a.k[bk]], 1ull);  // removed[k]
 }
 
-// Order-preserving compaction of bucket k: scatter the kept slots into
-// scratch (pos = exclusive scan of keep), then copy back; bn[k] = kept.
-__global__ void compact_scatter_kernel(int64_t nb, int k, const int32_t* __restrict__ keep,
-                                       const int32_t* __restrict__ pos, const int32_t* __restrict__ rec_in,
-                                       const uint16_t* __restrict__ items_in, int32_t* __restrict__ rec_out,
-                                       uint16_t* __restrict__ items_out, unsigned long long* bn_k) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nb) return;
-    if (c == nb - 1) *bn_k = (unsigned long long)(pos[c] + keep[c]);
-    if (!keep[c]) return;
-    int64_t d = pos[c];
-    rec_out[d] = rec_in[c];
-    for (int j = 0; j < k; ++j) items_out[d * k + j] = items_in[c * k + j];
-}
-
-__global__ void compact_copyback_kernel(int k, const unsigned long long* __restrict__ bn_k, int64_t nb,
-                                        const int32_t* __restrict__ rec_s, const uint16_t* __restrict__ items_s,
-                                        int32_t* __restrict__ rec, uint16_t* __restrict__ items) {
-    const int64_t n = (int64_t)*bn_k;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n && c < nb;
-         c += (int64_t)gridDim.x * blockDim.x) {
+// Order-preserving compaction of bucket k by one CTA (rare: scheduled by the
+// host when a bucket holds many dead slots): scan of the keep flags, scatter
+// to scratch, copy back, bn[k] = kept.
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) compact_bucket_kernel(
+    int k, int32_t* const* __restrict__ rec_tab, uint16_t* const* __restrict__ items_tab,
+    const int64_t* __restrict__ doff, const int32_t* __restrict__ keep_all, int32_t* __restrict__ rec_s,
+    uint16_t* __restrict__ items_s, unsigned long long* stat, int KS) {
+    if (stat[S_ABORT]) return;
+    __shared__ int64_t part[kCompactThreads];
+    const int64_t n = (int64_t)stat[S_HEAD + 2 * KS + k];
+    const int32_t* keep = keep_all + doff[k];
+    int32_t* rec = rec_tab[k];
+    uint16_t* items = items_tab[k];
+    const int64_t per = (n + kCompactThreads - 1) / kCompactThreads;
+    const int64_t lo = min(n, per * threadIdx.x), hi = min(n, lo + per);
+    int64_t cnt = 0;
+    for (int64_t c = lo; c < hi; ++c) cnt += keep[c];
+    part[threadIdx.x] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int i = 0; i < kCompactThreads; ++i) {
+            const int64_t v = part[i];
+            part[i] = acc;
+            acc += v;
+        }
+        stat[S_HEAD + 2 * KS + k] = (unsigned long long)acc;
+    }
+    __syncthreads();
+    int64_t d = part[threadIdx.x];
+    for (int64_t c = lo; c < hi; ++c) {
+        if (!keep[c]) continue;
+        rec_s[d] = rec[c];
+        for (int j = 0; j < k; ++j) items_s[d * k + j] = items[c * k + j];
+        ++d;
+    }
+    __syncthreads();
+    const int64_t kept = (int64_t)stat[S_HEAD + 2 * KS + k];
+    for (int64_t c = threadIdx.x; c < kept; c += kCompactThreads) {
         rec[c] = rec_s[c];
         for (int j = 0; j < k; ++j) items[c * k + j] = items_s[c * k + j];
     }
@@ -289,6 +331,7 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                                        unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
                                        int32_t* __restrict__ tmp_size, int64_t tmp_cap,
                                        unsigned long long* __restrict__ stat, int KS) {
+    if (stat[S_ABORT]) return;
     const int64_t total = (int64_t)stat[S_NFRONT] * L;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -327,9 +370,11 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
     }
 }
 
-// All-or-nothing capacity check for the candidate step.
+// All-or-nothing capacity check for the candidate step; an overflow also
+// raises the abort flag so every later stop is skipped until the replay.
 __global__ void check_capacity_kernel(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap,
                                       int64_t hcap, const int64_t* __restrict__ bcap) {
+    if (stat[S_ABORT]) return;
     __shared__ int over;
     if (threadIdx.x == 0) {
         const unsigned long long na = stat[S_NADM];
@@ -342,7 +387,10 @@ __global__ void check_capacity_kernel(unsigned long long* stat, int KS, int64_t 
     for (int k = threadIdx.x; k < KS; k += blockDim.x)
         if (adm[k] && (int64_t)(bn[k] + adm[k]) > bcap[k]) over = 1;
     __syncthreads();
-    if (threadIdx.x == 0) stat[S_OVERFLOW] = over ? 1ull : 0ull;
+    if (threadIdx.x == 0) {
+        stat[S_OVERFLOW] = over ? 1ull : 0ull;
+        if (over) stat[S_ABORT] = 1ull;
+    }
 }
 
 // Dedup the admissible joins: claim a hash slot per distinct mask.  Slots
@@ -351,7 +399,7 @@ __global__ void insert_candidates_kernel(int W, const unsigned long long* __rest
                                          const uint64_t* __restrict__ tmp_hash, Records R, int32_t* ht,
                                          uint64_t hmask, int64_t* __restrict__ tmp_slot,
                                          const unsigned long long* __restrict__ stat) {
-    if (stat[S_OVERFLOW]) return;
+    if (stat[S_ABORT]) return;
     const int64_t na = (int64_t)stat[S_NADM];
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t h = tmp_hash[t];
@@ -384,7 +432,7 @@ __global__ void commit_candidates_kernel(int W, const unsigned long long* __rest
                                          const int64_t* __restrict__ tmp_slot, Records R, int32_t* ht,
                                          unsigned long long* stat, int KS, int32_t* const* __restrict__ b_rec_tab,
                                          uint16_t* const* __restrict__ b_items_tab) {
-    if (stat[S_OVERFLOW]) return;
+    if (stat[S_ABORT]) return;
     const int64_t na = (int64_t)stat[S_NADM];
     unsigned long long* bn = stat + S_HEAD + 2 * KS;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
@@ -439,10 +487,12 @@ using namespace dic;
 struct Bucket {
     int32_t* rec = nullptr;
     uint16_t* items = nullptr;
-    int64_t n = 0;  // filled slots (live + dead) as of the last sync
+    int64_t n = 0;     // filled slots (live + dead) at the last polled stop
     int64_t cap = 0;
-    int64_t dead = 0;  // slots known dead, compaction pending
+    int64_t dead = 0;  // slots known dead at the last polled stop
 };
+
+constexpr int kRing = 16;  // status slots (> max stops in flight)
 
 struct dic_engine {
     const uint32_t* tids;
@@ -453,7 +503,7 @@ struct dic_engine {
     cudaStream_t s;
 
     Records R;
-    int64_t nrec = 0;
+    int64_t nrec = 0;  // at the last polled stop
     int32_t* ht = nullptr;
     int64_t hcap = 0;
 
@@ -462,25 +512,19 @@ struct dic_engine {
     int32_t** d_brec = nullptr;   // device copies of the bucket tables
     uint16_t** d_bitems = nullptr;
     int64_t* d_bcap = nullptr;
+    int64_t* d_doff = nullptr;     // [KS + 1] per-stop delta offsets
     unsigned long long* d_stat = nullptr;  // status words (see S_*)
-    unsigned long long* h_stat = nullptr;  // pinned mirror
+    int64_t slot_cap = 0;          // >= sum of bucket capacities: delta / keep / frontier size
 
     int32_t* level1 = nullptr;
     int64_t nL1 = 0;
     int32_t* frontier = nullptr;
-    int64_t front_cap = 0;
     int32_t* keep = nullptr;
-    int32_t* pos = nullptr;
-    int64_t keep_cap = 0;
-    void* scan_tmp = nullptr;
-    size_t scan_tmp_bytes = 0;
+    unsigned long long* delta = nullptr;
     int32_t* scr_rec = nullptr;
     uint16_t* scr_items = nullptr;
     int64_t scr_rec_cap = 0, scr_items_cap = 0;
-
-    unsigned long long* delta = nullptr;
-    int64_t delta_cap = 0, delta_len = 0;
-    std::vector<int64_t> delta_off;
+    std::vector<char> compact_next;  // host decision: compact bucket k in the next issued stop
 
     unsigned long long* tmp_mask = nullptr;
     uint64_t* tmp_hash = nullptr;
@@ -495,9 +539,18 @@ struct dic_engine {
     unsigned long long* tri = nullptr;    // [L(L-1)/2] per-stop pair counts
     int64_t tri_len = 0;
 
-    int64_t live = 0;  // |dashed|
+    // pipelining
+    unsigned long long* ring = nullptr;  // pinned [kRing][S_HEAD + 3*KS]
+    cudaEvent_t ev[kRing];
+    int64_t ring_words = 0;
+    int kuse_at[kRing];                  // kuse when the slot was written
+    int64_t issued = 0;                  // stops issued (sequence numbers 0..issued-1)
+    int64_t polled = 0;                  // stops polled
+    int64_t live = 0;                    // |dashed| after the last polled stop
+    int64_t cur_first = 0, cur_last = -1;
+    int kuse_issue = 4;                  // kuse of the stop between issue_count and issue_checkpoint
     bool seeded = false;
-    bool counted = false;
+    bool counted = false;                // issue_count done, issue_checkpoint pending
 };
 
 namespace {
@@ -517,13 +570,15 @@ void dfree(T*& p, cudaStream_t s) {
     p = nullptr;
 }
 
+// stream-ordered growth: the copy runs after every kernel already enqueued,
+// so the FULL old capacity is copied (host sizes may lag the device)
 template <class T>
-int dgrow(T** p, int64_t old_count, int64_t new_count, cudaStream_t s) {
+int dgrow(T** p, int64_t old_cap, int64_t new_cap, cudaStream_t s) {
     T* q = nullptr;
-    int rc = dalloc(&q, new_count, s);
+    int rc = dalloc(&q, new_cap, s);
     if (rc) return rc;
-    if (*p && old_count > 0) {
-        cudaError_t e = cudaMemcpyAsync(q, *p, (size_t)old_count * sizeof(T), cudaMemcpyDeviceToDevice, s);
+    if (*p && old_cap > 0) {
+        cudaError_t e = cudaMemcpyAsync(q, *p, (size_t)old_cap * sizeof(T), cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(grow)");
     }
     dfree(*p, s);
@@ -533,15 +588,16 @@ int dgrow(T** p, int64_t old_count, int64_t new_count, cudaStream_t s) {
 
 int grow_records(dic_engine* e, int64_t need_cap) {
     if (need_cap <= e->R.cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>({need_cap, e->R.cap * 2, (int64_t)4096});
+    const int64_t nc = std::max<int64_t>({need_cap, e->R.cap * 2, (int64_t)4096});
     Records& R = e->R;
+    const int64_t oc = R.cap;
     int rc;
-    if ((rc = dgrow(&R.mask, e->nrec * e->W, nc * e->W, e->s))) return rc;
-    if ((rc = dgrow(&R.hash, e->nrec, nc, e->s))) return rc;
-    if ((rc = dgrow(&R.support, e->nrec, nc, e->s))) return rc;
-    if ((rc = dgrow(&R.intervals, e->nrec, nc, e->s))) return rc;
-    if ((rc = dgrow(&R.size, e->nrec, nc, e->s))) return rc;
-    if ((rc = dgrow(&R.shape, e->nrec, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.mask, oc * e->W, nc * e->W, e->s))) return rc;
+    if ((rc = dgrow(&R.hash, oc, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.support, oc, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.intervals, oc, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.size, oc, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.shape, oc, nc, e->s))) return rc;
     R.cap = nc;
     return DIC_OK;
 }
@@ -558,10 +614,8 @@ int ensure_hash(dic_engine* e, int64_t nrec_after) {
     e->hcap = nc;
     ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc);
     ::dic::note_launch();
-    if (e->nrec > 0) {
-        ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, 0, e->nrec);
-        ::dic::note_launch();
-    }
+    ht_insert_records_kernel<<<sm_count() * 8, 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, e->d_stat + S_NREC);
+    ::dic::note_launch();
     DIC_CHECK_LAUNCH("rehash");
     return DIC_OK;
 }
@@ -578,65 +632,45 @@ int sync_bucket_tables(dic_engine* e) {
     DIC_CUDA(cudaMemcpyAsync(e->d_brec, r.data(), r.size() * sizeof(int32_t*), cudaMemcpyHostToDevice, e->s));
     DIC_CUDA(cudaMemcpyAsync(e->d_bitems, it.data(), it.size() * sizeof(uint16_t*), cudaMemcpyHostToDevice, e->s));
     DIC_CUDA(cudaMemcpyAsync(e->d_bcap, cap.data(), cap.size() * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
-    // the host vectors die at return: make the copies complete first
+    // the host vectors die at return: make the copies complete first (rare: growth only)
     DIC_CUDA(cudaStreamSynchronize(e->s));
+    return DIC_OK;
+}
+
+// per-stop slot arrays (delta, keep, frontier) cover every bucket capacity
+int ensure_slot_arrays(dic_engine* e) {
+    int64_t need = 0;
+    for (const Bucket& b : e->buckets) need += b.cap;
+    need = std::max<int64_t>(need, 1);
+    if (need <= e->slot_cap) return DIC_OK;
+    const int64_t nc = std::max<int64_t>(need, e->slot_cap + e->slot_cap / 2);
+    dfree(e->delta, e->s);
+    dfree(e->keep, e->s);
+    dfree(e->frontier, e->s);
+    int rc;
+    if ((rc = dalloc(&e->delta, nc, e->s)) || (rc = dalloc(&e->keep, nc, e->s)) ||
+        (rc = dalloc(&e->frontier, nc, e->s)))
+        return rc;
+    e->slot_cap = nc;
     return DIC_OK;
 }
 
 int grow_bucket(dic_engine* e, int k, int64_t need_cap, bool* changed) {
     Bucket& b = e->buckets[k];
     if (need_cap <= b.cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>({need_cap, b.cap * 2, (int64_t)1024});
+    const int64_t nc = std::max<int64_t>({need_cap, b.cap * 2, (int64_t)1024});
     int rc;
-    if ((rc = dgrow(&b.rec, b.n, nc, e->s))) return rc;
-    if ((rc = dgrow(&b.items, b.n * k, nc * k, e->s))) return rc;
+    if ((rc = dgrow(&b.rec, b.cap, nc, e->s))) return rc;
+    if ((rc = dgrow(&b.items, b.cap * k, nc * k, e->s))) return rc;
     b.cap = nc;
     *changed = true;
     e->kuse = std::max(e->kuse, std::min(k + 2, e->KS));
     return DIC_OK;
 }
 
-int64_t total_slots(const dic_engine* e) {
-    int64_t t = 0;
-    for (const Bucket& b : e->buckets) t += b.n;
-    return t;
-}
-
-// per-stop scratch sized for `slots` bucket entries
-int ensure_stop_scratch(dic_engine* e, int64_t slots) {
-    int rc;
-    if (slots > e->keep_cap) {
-        int64_t nc = std::max<int64_t>(slots, e->keep_cap * 2);
-        dfree(e->keep, e->s);
-        dfree(e->pos, e->s);
-        if ((rc = dalloc(&e->keep, nc, e->s)) || (rc = dalloc(&e->pos, nc, e->s))) return rc;
-        size_t bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)nc, e->s);
-        if (bytes > e->scan_tmp_bytes) {
-            if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, e->s);
-            DIC_CUDA(cudaMallocAsync(&e->scan_tmp, bytes, e->s));
-            e->scan_tmp_bytes = bytes;
-        }
-        e->keep_cap = nc;
-    }
-    if (slots > e->front_cap) {
-        int64_t nc = std::max<int64_t>(slots, e->front_cap * 2);
-        dfree(e->frontier, e->s);
-        if ((rc = dalloc(&e->frontier, nc, e->s))) return rc;
-        e->front_cap = nc;
-    }
-    if (slots > e->delta_cap) {
-        int64_t nc = std::max<int64_t>(slots, e->delta_cap * 2);
-        dfree(e->delta, e->s);
-        if ((rc = dalloc(&e->delta, nc, e->s))) return rc;
-        e->delta_cap = nc;
-    }
-    return DIC_OK;
-}
-
 int ensure_tmp(dic_engine* e, int64_t want) {
     if (want <= e->tmp_cap) return DIC_OK;
-    int64_t nc = std::max<int64_t>(want, e->tmp_cap * 2);
+    const int64_t nc = std::max<int64_t>(want, e->tmp_cap * 2);
     dfree(e->tmp_mask, e->s);
     dfree(e->tmp_hash, e->s);
     dfree(e->tmp_size, e->s);
@@ -649,9 +683,9 @@ int ensure_tmp(dic_engine* e, int64_t want) {
     return DIC_OK;
 }
 
-// Headroom so most stops never overflow: >= 64k join slots, record / hash
-// room for 64k more records, every bucket in use with room to grow by half
-// (>= 4096), and the next size up allocated.  Synchronises only on growth.
+// Headroom for the stops in flight: >= 64k join slots and record / hash room,
+// every bucket of size >= 3 in use with room to grow by half (>= 4096), the
+// next size up allocated, slot arrays covering the capacities.
 int ensure_headroom(dic_engine* e) {
     int rc;
     const int64_t room = std::max<int64_t>(1 << 16, e->nrec / 2);
@@ -667,6 +701,7 @@ int ensure_headroom(dic_engine* e) {
         const int64_t want = b.n + std::max<int64_t>(4096, b.n / 2);
         if (want > b.cap && (rc = grow_bucket(e, k, want, &changed))) return rc;
     }
+    if ((rc = ensure_slot_arrays(e))) return rc;
     if (changed && (rc = sync_bucket_tables(e))) return rc;
     return DIC_OK;
 }
@@ -690,15 +725,18 @@ int candidate_step(dic_engine* e) {
     return DIC_OK;
 }
 
-// status -> host (head words, removed / adm / bn for sizes < kuse); sync
-int read_status(dic_engine* e) {
+// status of the stop in ring slot `slot`: head words and removed / adm / bn
+// for sizes < kuse, then an event
+int copy_status(dic_engine* e, int slot) {
     const int KS = e->KS, ku = e->kuse;
     const size_t u = sizeof(unsigned long long);
-    DIC_CUDA(cudaMemcpyAsync(e->h_stat, e->d_stat, S_HEAD * u, cudaMemcpyDeviceToHost, e->s));
+    unsigned long long* dst = e->ring + (int64_t)slot * e->ring_words;
+    DIC_CUDA(cudaMemcpyAsync(dst, e->d_stat, S_HEAD * u, cudaMemcpyDeviceToHost, e->s));
     for (int sec = 0; sec < 3; ++sec)
-        DIC_CUDA(cudaMemcpyAsync(e->h_stat + S_HEAD + sec * KS, e->d_stat + S_HEAD + sec * KS, ku * u,
+        DIC_CUDA(cudaMemcpyAsync(dst + S_HEAD + sec * KS, e->d_stat + S_HEAD + sec * KS, ku * u,
                                  cudaMemcpyDeviceToHost, e->s));
-    DIC_CUDA(cudaStreamSynchronize(e->s));
+    e->kuse_at[slot] = ku;
+    DIC_CUDA(cudaEventRecord(e->ev[slot], e->s));
     return DIC_OK;
 }
 
@@ -710,6 +748,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     DIC_REQUIRE(m >= 1 && m <= 65535, "dic_engine_create: m=%d outside [1, 65535]", m);
     DIC_REQUIRE(n_local >= 0 && (tids || n_local == 0), "dic_engine_create: bad tids/n_local");
     DIC_REQUIRE(interval >= 1 && stop_max >= 1, "dic_engine_create: bad interval/stop_max");
+    retain_pool();
     dic_engine* e = new dic_engine();
     e->tids = tids;
     e->n_local = n_local;
@@ -723,21 +762,26 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->bound = prune_bound ? 1 : 0;
     e->s = as_stream(stream);
     e->buckets.resize(e->KS);
+    e->compact_next.assign(e->KS, 0);
     const int KS = e->KS;
+    e->ring_words = S_HEAD + 3 * (int64_t)KS;
     int rc = 0;
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
-        (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_stat, S_HEAD + 3 * KS, e->s)) ||
-        (rc = dalloc(&e->level1, m, e->s))) {
+        (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
+        (rc = dalloc(&e->d_stat, e->ring_words, e->s)) || (rc = dalloc(&e->level1, m, e->s))) {
         delete e;
         return rc;
     }
-    cudaError_t ce = cudaMallocHost((void**)&e->h_stat, (S_HEAD + 3 * KS) * sizeof(unsigned long long));
+    cudaError_t ce = cudaMallocHost((void**)&e->ring, (size_t)kRing * e->ring_words * sizeof(unsigned long long));
     if (ce != cudaSuccess) {
         delete e;
         return cuda_fail(ce, "cudaMallocHost");
     }
-    memset(e->h_stat, 0, (S_HEAD + 3 * KS) * sizeof(unsigned long long));
-    cudaMemsetAsync(e->d_stat, 0, (S_HEAD + 3 * KS) * sizeof(unsigned long long), e->s);
+    for (int i = 0; i < kRing; ++i) {
+        cudaEventCreateWithFlags(&e->ev[i], cudaEventDisableTiming);
+        e->kuse_at[i] = 0;
+    }
+    cudaMemsetAsync(e->d_stat, 0, e->ring_words * sizeof(unsigned long long), e->s);
     if ((rc = sync_bucket_tables(e))) {
         delete e;
         return rc;
@@ -749,19 +793,21 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
 extern "C" int dic_engine_destroy(dic_engine* e) {
     if (!e) return DIC_OK;
     cudaStream_t s = e->s;
+    cudaStreamSynchronize(s);
     Records& R = e->R;
     dfree(R.mask, s); dfree(R.hash, s); dfree(R.support, s); dfree(R.intervals, s); dfree(R.size, s);
     dfree(R.shape, s);
     dfree(e->ht, s);
     for (Bucket& b : e->buckets) { dfree(b.rec, s); dfree(b.items, s); }
-    dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_stat, s);
-    dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->pos, s);
-    dfree(e->scr_rec, s); dfree(e->scr_items, s); dfree(e->delta, s);
+    dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_doff, s); dfree(e->d_stat, s);
+    dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->delta, s);
+    dfree(e->scr_rec, s); dfree(e->scr_items, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s);
-    if (e->scan_tmp) cudaFreeAsync(e->scan_tmp, s);
     cudaStreamSynchronize(s);
-    if (e->h_stat) cudaFreeHost(e->h_stat);
+    for (int i = 0; i < kRing; ++i)
+        if (e->ev[i]) cudaEventDestroy(e->ev[i]);
+    if (e->ring) cudaFreeHost(e->ring);
     delete e;
     return DIC_OK;
 }
@@ -790,10 +836,15 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     const int64_t L = (int64_t)l1.size();
     const int64_t npairs = L * (L - 1) / 2;
     int rc;
-    e->nrec = 0;
+    e->nrec = m + npairs;
+    // device record count first: the hash build reads it
+    std::vector<unsigned long long> head(S_HEAD, 0), bn(e->KS, 0);
+    head[S_NREC] = (unsigned long long)e->nrec;
+    if (e->KS > 2) bn[2] = (unsigned long long)npairs;
+    DIC_CUDA(cudaMemcpyAsync(e->d_stat, head.data(), S_HEAD * 8, cudaMemcpyHostToDevice, e->s));
+    DIC_CUDA(cudaMemcpyAsync(e->d_stat + S_HEAD + 2 * e->KS, bn.data(), e->KS * 8, cudaMemcpyHostToDevice, e->s));
     const int64_t room = std::max<int64_t>(1 << 16, (m + npairs) / 2);
     if ((rc = grow_records(e, m + npairs + room))) return rc;
-    if ((rc = ensure_hash(e, m + npairs + room))) return rc;
     seed_singletons_kernel<<<nblk(m), 256, 0, e->s>>>(e->R, e->W, m, counts, e->need, e->stop_max);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("seed_singletons_kernel");
@@ -818,9 +869,10 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         dfree(d_rs, e->s);
         e->buckets[2].n = npairs;
     }
+    if ((rc = ensure_hash(e, m + npairs + room))) return rc;  // builds from the device record count
     // dense pair counting over the frequent items
+    std::vector<int32_t> rank(m, -1);
     if (L >= 2 && e->n_local > 0) {
-        std::vector<int32_t> rank(m, -1);
         for (int64_t a = 0; a < L; ++a) rank[l1[a]] = (int32_t)a;
         if ((rc = dalloc(&e->rank, m, e->s))) return rc;
         DIC_CUDA(cudaMemcpyAsync(e->rank, rank.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, e->s));
@@ -834,18 +886,8 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         }
         e->tri_len = npairs;
         if ((rc = dalloc(&e->tri, npairs, e->s))) return rc;
-        DIC_CUDA(cudaStreamSynchronize(e->s));  // rank vector dies at scope exit
     }
-    e->nrec = m + npairs;
-    ht_insert_records_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R, 0, e->nrec);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("ht_insert_records_kernel");
-    // device status: records and bucket fill
-    std::vector<unsigned long long> head(S_HEAD, 0), bn(e->KS, 0);
-    head[S_NREC] = (unsigned long long)e->nrec;
-    if (e->KS > 2) bn[2] = (unsigned long long)npairs;
-    DIC_CUDA(cudaMemcpyAsync(e->d_stat, head.data(), S_HEAD * 8, cudaMemcpyHostToDevice, e->s));
-    DIC_CUDA(cudaMemcpyAsync(e->d_stat + S_HEAD + 2 * e->KS, bn.data(), e->KS * 8, cudaMemcpyHostToDevice, e->s));
+    if ((rc = ensure_headroom(e))) return rc;
     if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
     e->live = npairs;
     e->seeded = true;
@@ -854,39 +896,40 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     return DIC_OK;
 }
 
-extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
-    DIC_REQUIRE(e, "dic_engine_count: null engine");
-    if (!e->seeded) { set_error("dic_engine_count: engine not seeded"); return DIC_ESTATE; }
+// ---------------------------------------------------------------------------
+// pipelined stop API
+// ---------------------------------------------------------------------------
+extern "C" int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t llast) {
+    DIC_REQUIRE(e, "dic_engine_issue_count: null engine");
+    if (!e->seeded || e->counted) {
+        set_error("dic_engine_issue_count: engine not seeded or checkpoint pending");
+        return DIC_ESTATE;
+    }
     DIC_REQUIRE(lfirst >= 0 && (llast < lfirst || llast < e->n_local),
                 "dic_engine_count: local chunk [%lld, %lld] outside %lld local rows", (long long)lfirst,
                 (long long)llast, (long long)e->n_local);
-    const int64_t tot = total_slots(e);
     int rc;
-    if ((rc = ensure_stop_scratch(e, std::max<int64_t>(tot, 1)))) return rc;
-    e->delta_len = tot;
-    e->delta_off.assign(e->buckets.size(), 0);
-    if (tot > 0) DIC_CUDA(cudaMemsetAsync(e->delta, 0, tot * sizeof(unsigned long long), e->s));
-    int64_t off = 0;
-    std::vector<BucketIn> bk;
-    // the pair bucket goes through the dense triangle while most pairs are live
-    const bool dense_pairs = e->tri != nullptr && e->KS > 2 && e->buckets[2].n > 0 &&
-                             2 * e->buckets[2].n >= e->tri_len;
-    for (size_t k = 0; k < e->buckets.size(); ++k) {
-        const Bucket& b = e->buckets[k];
-        e->delta_off[k] = off;
-        if (b.n > 0 && !(k == 2 && dense_pairs)) bk.push_back(BucketIn{b.items, e->delta + off, b.n, (int)k});
-        off += b.n;
-    }
-    if (dense_pairs && llast >= lfirst) {
-        DIC_CUDA(cudaMemsetAsync(e->tri, 0, e->tri_len * sizeof(unsigned long long), e->s));
-        if ((rc = count_pairs_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, e->s))) return rc;
-        if ((rc = pair_gather_launch(e->buckets[2].items, e->buckets[2].n, e->rank, e->nL1, e->tri,
-                                     e->delta + e->delta_off[2], e->s)))
+    e->cur_first = lfirst;
+    e->cur_last = llast;
+    e->kuse_issue = e->kuse;
+    DIC_CUDA(cudaMemsetAsync(e->delta, 0, e->slot_cap * sizeof(unsigned long long), e->s));
+    stop_prep_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->d_doff);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("stop_prep_kernel");
+    if (llast >= lfirst) {
+        const unsigned long long* abort_flag = e->d_stat + S_ABORT;
+        const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
+        if (e->tri) {
+            if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
+                                             e->tri_len, abort_flag, e->s)))
+                return rc;
+            if ((rc = pair_gather_dev_launch(e->d_bitems, bn, e->d_doff, e->rank, e->nL1, e->tri, e->delta,
+                                             abort_flag, e->s)))
+                return rc;
+        }
+        if ((rc = count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse, e->d_bitems, bn, e->d_doff,
+                                   e->delta, abort_flag, e->tri ? e->tri_len : 0, e->s)))
             return rc;
-    }
-    if (!bk.empty() && llast >= lfirst) {
-        rc = count_buckets_launch(e->tids, e->n_local, e->m, lfirst, llast, bk.data(), (int)bk.size(), e->s);
-        if (rc) return rc;
     }
     e->counted = true;
     return DIC_OK;
@@ -895,92 +938,77 @@ extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
 extern "C" int dic_engine_delta(dic_engine* e, void** ptr, int64_t* len) {
     DIC_REQUIRE(e && ptr && len, "dic_engine_delta: null argument");
     *ptr = e->delta;
-    *len = e->delta_len;
+    *len = e->slot_cap;  // zero beyond the live slots: a fixed-size sum-allreduce is exact
     return DIC_OK;
 }
 
-extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
-    DIC_REQUIRE(e && st, "dic_engine_checkpoint: null argument");
-    if (!e->counted) { set_error("dic_engine_checkpoint: no count since the last checkpoint"); return DIC_ESTATE; }
+extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
+    DIC_REQUIRE(e && seq, "dic_engine_issue_checkpoint: null argument");
+    if (!e->counted) { set_error("dic_engine_issue_checkpoint: no count issued"); return DIC_ESTATE; }
+    if (e->issued - e->polled >= kRing - 1) {
+        set_error("dic_engine_issue_checkpoint: more than %d stops in flight", kRing - 1);
+        return DIC_ESTATE;
+    }
     e->counted = false;
     int rc;
     const int KS = e->KS;
-    const size_t u = sizeof(unsigned long long);
-    st->dashed_at_start = e->live;
-    // reset the per-stop counters, removed[] and adm[] (NREC and bn[] persist)
-    DIC_CUDA(cudaMemsetAsync(e->d_stat, 0, S_NREC * u, e->s));
-    DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD, 0, 2 * (size_t)KS * u, e->s));
-
-    // 1. apply + prune + finalize over every bucket slot (one launch per 16 buckets)
-    {
-        ApplyArgs a;
-        memset(&a, 0, sizeof(a));
-        int64_t base = 0;
-        auto flush = [&]() -> int {
-            if (a.nb == 0) return DIC_OK;
-            apply_prune_finalize_kernel<<<nblk(a.total), 256, 0, e->s>>>(
-                a, e->delta + base, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier, e->keep + base,
-                e->d_stat);
-            ::dic::note_launch();
-            DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
-            memset(&a, 0, sizeof(a));
-            return DIC_OK;
-        };
-        for (int k = 0; k < KS; ++k) {
-            const Bucket& b = e->buckets[k];
-            if (b.n == 0) continue;
-            if (a.nb == kMaxApply && (rc = flush())) return rc;
-            if (a.nb == 0) base = e->delta_off[k];
-            a.k[a.nb] = k;
-            a.rec[a.nb] = b.rec;
-            a.off[a.nb] = e->delta_off[k] - base;
-            a.total = e->delta_off[k] - base + b.n;
-            ++a.nb;
-        }
-        if ((rc = flush())) return rc;
-    }
-
-    // 2. compaction of buckets holding dead slots from earlier stops (this
-    //    stop's keep flags also drop the entries that just left)
-    std::vector<char> compacted(KS, 0);
-    for (int k = 0; k < KS; ++k) {
-        Bucket& b = e->buckets[k];
-        if (b.n == 0 || b.dead == 0) continue;
-        const int64_t off = e->delta_off[k];
-        if (b.n > e->scr_rec_cap) {
+    // 1. apply + prune + finalize over every slot
+    apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, e->s>>>(
+        e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
+        e->keep, e->d_stat);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
+    // 2. compaction the host scheduled from an earlier status
+    for (int k = 0; k < KS && k < e->kuse_issue; ++k) {
+        if (!e->compact_next[k]) continue;
+        e->compact_next[k] = 0;
+        const Bucket& b = e->buckets[k];
+        if (b.cap > e->scr_rec_cap) {
             dfree(e->scr_rec, e->s);
-            if ((rc = dalloc(&e->scr_rec, b.n, e->s))) return rc;
-            e->scr_rec_cap = b.n;
+            if ((rc = dalloc(&e->scr_rec, b.cap, e->s))) return rc;
+            e->scr_rec_cap = b.cap;
         }
-        if (b.n * k > e->scr_items_cap) {
+        if (b.cap * k > e->scr_items_cap) {
             dfree(e->scr_items, e->s);
-            if ((rc = dalloc(&e->scr_items, b.n * k, e->s))) return rc;
-            e->scr_items_cap = b.n * k;
+            if ((rc = dalloc(&e->scr_items, b.cap * k, e->s))) return rc;
+            e->scr_items_cap = b.cap * k;
         }
-        size_t bytes = e->scan_tmp_bytes;
-        DIC_CUDA(cub::DeviceScan::ExclusiveSum(e->scan_tmp, bytes, e->keep + off, e->pos + off, (int)b.n, e->s));
-        unsigned long long* bn_k = e->d_stat + S_HEAD + 2 * KS + k;
-        compact_scatter_kernel<<<nblk(b.n), 256, 0, e->s>>>(b.n, k, e->keep + off, e->pos + off, b.rec, b.items,
-                                                            e->scr_rec, e->scr_items, bn_k);
+        compact_bucket_kernel<<<1, kCompactThreads, 0, e->s>>>(k, e->d_brec, e->d_bitems, e->d_doff, e->keep,
+                                                               e->scr_rec, e->scr_items, e->d_stat, KS);
         ::dic::note_launch();
-        compact_copyback_kernel<<<std::min<unsigned>(nblk(b.n), (unsigned)sm_count() * 8), 256, 0, e->s>>>(
-            k, bn_k, b.n, e->scr_rec, e->scr_items, b.rec, b.items);
-        ::dic::note_launch();
-        DIC_CHECK_LAUNCH("compaction");
-        compacted[k] = 1;
+        DIC_CHECK_LAUNCH("compact_bucket_kernel");
     }
-
     // 3. make_candidates from the frontier (device-sized; all-or-nothing)
     if ((rc = candidate_step(e))) return rc;
-    if ((rc = read_status(e))) return rc;
-    unsigned long long* h = e->h_stat;
-    int replays = 0;
+    const int slot = (int)(e->issued % kRing);
+    if ((rc = copy_status(e, slot))) return rc;
+    *seq = e->issued++;
+    return DIC_OK;
+}
+
+extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, int32_t* replayed) {
+    DIC_REQUIRE(e && st && replayed, "dic_engine_poll: null argument");
+    if (seq != e->polled || seq >= e->issued) {
+        set_error("dic_engine_poll: stop %lld polled out of order (next %lld, issued %lld)", (long long)seq,
+                  (long long)e->polled, (long long)e->issued);
+        return DIC_ESTATE;
+    }
+    const int KS = e->KS;
+    const size_t u = sizeof(unsigned long long);
+    const int slot = (int)(seq % kRing);
+    DIC_CUDA(cudaEventSynchronize(e->ev[slot]));
+    unsigned long long* h = e->ring + (int64_t)slot * e->ring_words;
+    int ku = e->kuse_at[slot];
+    *replayed = 0;
+    int rc, replays = 0;
     while (h[S_OVERFLOW]) {
+        // every later stop was skipped (abort flag): grow, replay this stop's
+        // candidate step, and tell the caller to re-issue the skipped stops
         if (++replays > 4) {
-            set_error("dic_engine_checkpoint: candidate capacity did not converge");
+            set_error("dic_engine_poll: candidate capacity did not converge");
             return DIC_ENOMEM;
         }
-        // adm[] for every size (a join can only grow a size by one, but read all)
+        DIC_CUDA(cudaStreamSynchronize(e->s));
         std::vector<unsigned long long> adm(KS), bn(KS);
         DIC_CUDA(cudaMemcpyAsync(adm.data(), e->d_stat + S_HEAD + KS, KS * u, cudaMemcpyDeviceToHost, e->s));
         DIC_CUDA(cudaMemcpyAsync(bn.data(), e->d_stat + S_HEAD + 2 * KS, KS * u, cudaMemcpyDeviceToHost, e->s));
@@ -993,26 +1021,29 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
         bool changed = false;
         for (int k = 0; k < KS; ++k) {
             if (!adm[k]) continue;
-            e->buckets[k].n = (int64_t)bn[k];  // growth copies the filled prefix
+            e->buckets[k].n = (int64_t)bn[k];
             if ((rc = grow_bucket(e, k, (int64_t)(bn[k] + adm[k]), &changed))) return rc;
         }
+        if ((rc = ensure_slot_arrays(e))) return rc;
         if (changed && (rc = sync_bucket_tables(e))) return rc;
-        // replay: reset the join counters; NFRONT / frontier / apply results stay
+        // reset the join counters and the abort flag; NFRONT / frontier / apply results stay
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
+        DIC_CUDA(cudaMemsetAsync(e->d_stat + S_ABORT, 0, u, e->s));
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
         if ((rc = candidate_step(e))) return rc;
-        if ((rc = read_status(e))) return rc;
+        if ((rc = copy_status(e, slot))) return rc;
+        DIC_CUDA(cudaEventSynchronize(e->ev[slot]));
+        ku = e->kuse_at[slot];
+        // the skipped stops are re-issued by the caller
+        e->issued = seq + 1;
+        e->counted = false;
+        *replayed = 1;
     }
-
-    // 4. bookkeeping from the status words
+    e->polled = seq + 1;
+    // bookkeeping from the status words
     const int64_t pruned = (int64_t)h[S_NPRUNED], finalized = (int64_t)h[S_NFINAL];
     const int64_t inserted = (int64_t)h[S_NINS], survivors = (int64_t)h[S_SURV];
-    e->nrec = (int64_t)h[S_NREC];
-    for (int k = 0; k < e->kuse; ++k) {
-        Bucket& b = e->buckets[k];
-        b.n = (int64_t)h[S_HEAD + 2 * KS + k];
-        b.dead = compacted[k] ? 0 : (int64_t)h[S_HEAD + k];  // not-kept slots (old + new)
-    }
+    st->dashed_at_start = e->live;
     st->promoted = (int64_t)h[S_NFRONT];
     st->pruned = pruned;
     st->finalized = finalized;
@@ -1020,18 +1051,44 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
     st->dashed_peak = survivors + inserted;
     e->live = e->live - pruned - finalized + inserted;
     st->dashed_at_end = e->live;
+    e->nrec = (int64_t)h[S_NREC];
     st->records = e->nrec;
-    // 5. headroom for the next stop (rare growth; synchronises only then)
+    for (int k = 0; k < ku; ++k) {
+        Bucket& b = e->buckets[k];
+        b.n = (int64_t)h[S_HEAD + 2 * KS + k];
+        b.dead = (int64_t)h[S_HEAD + k];
+        // schedule a compaction when dead slots are a quarter of the bucket
+        if (b.n > 0 && b.dead > 0 && (b.dead * 4 >= b.n || b.dead == b.n)) e->compact_next[k] = 1;
+    }
+    // headroom for the stops issued next (growth is stream-ordered)
     if ((rc = ensure_headroom(e))) return rc;
     return DIC_OK;
 }
 
+// Synchronous forms (one stop at a time): count, then checkpoint = issue + poll.
+extern "C" int dic_engine_count(dic_engine* e, int64_t lfirst, int64_t llast) {
+    return dic_engine_issue_count(e, lfirst, llast);
+}
+
+extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
+    DIC_REQUIRE(e && st, "dic_engine_checkpoint: null argument");
+    int64_t seq = 0;
+    int rc = dic_engine_issue_checkpoint(e, &seq);
+    if (rc) return rc;
+    int32_t replayed = 0;
+    return dic_engine_poll(e, seq, st, &replayed);
+}
+
 extern "C" int dic_engine_num_frequent(dic_engine* e, int64_t* F) {
     DIC_REQUIRE(e && F, "dic_engine_num_frequent: null argument");
+    DIC_CUDA(cudaStreamSynchronize(e->s));
+    unsigned long long nrec_d = 0;
+    DIC_CUDA(cudaMemcpy(&nrec_d, e->d_stat + S_NREC, sizeof(nrec_d), cudaMemcpyDeviceToHost));
+    e->nrec = (int64_t)nrec_d;
     int32_t* ids = nullptr;
     int rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s);
     if (rc) return rc;
-    unsigned long long* cnt = e->d_stat + S_NADM;  // scratch word between stops
+    unsigned long long* cnt = e->d_stat + S_SCRATCH;
     DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
     collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
     ::dic::note_launch();
@@ -1056,7 +1113,7 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
     if ((rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s)) || (rc = dalloc(&dm, F1 * e->W, e->s)) ||
         (rc = dalloc(&dsz, F1, e->s)) || (rc = dalloc(&dsu, F1, e->s)))
         return rc;
-    unsigned long long* cnt = e->d_stat + S_NADM;
+    unsigned long long* cnt = e->d_stat + S_SCRATCH;
     DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
     collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
     ::dic::note_launch();

@@ -28,7 +28,11 @@ template <int TW>
 __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
                                                                 ChunkGeom geom, int64_t t_first, int64_t t_last,
                                                                 int64_t row_splits, int nblk,
-                                                                unsigned long long* __restrict__ tri) {
+                                                                unsigned long long* __restrict__ tri,
+                                                                const unsigned long long* bn2, int64_t tri_len,
+                                                                const unsigned long long* abort_flag) {
+    // engine use: skip while aborted, or once the pair bucket is mostly gone
+    if (abort_flag && (*abort_flag || 2 * (int64_t)*bn2 < tri_len)) return;
     constexpr int RW = TW + 4;
     constexpr int RB = RW * 4;
     constexpr uint32_t BLK = kPairBlock * RB;
@@ -136,10 +140,17 @@ __global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, 
     }
 }
 
-// delta[c] = tri[pair of bucket slot c] (ranks of its two items among L1)
-__global__ void pair_gather_kernel(const uint16_t* __restrict__ items, int64_t C, const int32_t* __restrict__ rank,
-                                   int64_t L, const unsigned long long* __restrict__ tri,
-                                   unsigned long long* __restrict__ out) {
+// delta[c] += tri[pair of bucket-2 slot c] (ranks of its two items among L1);
+// sizes and the dense switch come from device memory
+__global__ void pair_gather_kernel(uint16_t* const* __restrict__ items_tab, const unsigned long long* __restrict__ bn,
+                                   const int64_t* __restrict__ doff, const int32_t* __restrict__ rank, int64_t L,
+                                   const unsigned long long* __restrict__ tri, unsigned long long* __restrict__ delta,
+                                   const unsigned long long* __restrict__ abort_flag) {
+    const int64_t tri_len = L * (L - 1) / 2;
+    const int64_t C = (int64_t)bn[2];
+    if (*abort_flag || 2 * C < tri_len) return;
+    const uint16_t* items = items_tab[2];
+    unsigned long long* out = delta + doff[2];
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
         const int a = rank[items[2 * c]], b = rank[items[2 * c + 1]];
         out[c] += tri[tri_index(a, b, L)];
@@ -149,7 +160,8 @@ __global__ void pair_gather_kernel(const uint16_t* __restrict__ items, int64_t C
 static int g_pair_attr = 0;
 
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
-                       unsigned long long* tri, cudaStream_t s) {
+                       unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
+                       int64_t tri_len = 0, const unsigned long long* abort_flag = nullptr) {
     if (last < first || m < 2) return DIC_OK;
     const int TW = tile_groups(m);
     const ChunkGeom geom = chunk_geom(first, last);
@@ -169,9 +181,11 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
     int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (target + blocks - 1) / blocks));
     dim3 grid((unsigned)rs, (unsigned)blocks);
     if (TW == 32)
-        pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri);
+        pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
+                                                             tri_len, abort_flag);
     else
-        pair_tri_kernel<16><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri);
+        pair_tri_kernel<16><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
+                                                             tri_len, abort_flag);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("pair_tri_kernel");
     return DIC_OK;
@@ -187,11 +201,18 @@ int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* ite
     return DIC_OK;
 }
 
-int pair_gather_launch(const uint16_t* items, int64_t C, const int32_t* rank, int64_t L,
-                       const unsigned long long* tri, unsigned long long* out, cudaStream_t s) {
-    if (C <= 0) return DIC_OK;
-    const int64_t blocks = std::min<int64_t>((C + 255) / 256, (int64_t)sm_count() * 8);
-    pair_gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(items, C, rank, L, tri, out);
+// engine: pairs of the current stop into the delta slots of bucket 2
+int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
+                           unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
+                           const unsigned long long* abort_flag, cudaStream_t s) {
+    DIC_CUDA(cudaMemsetAsync(tri, 0, (size_t)tri_len * sizeof(unsigned long long), s));
+    return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag);
+}
+
+int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
+                           const int32_t* rank, int64_t L, const unsigned long long* tri,
+                           unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s) {
+    pair_gather_kernel<<<sm_count() * 8, 256, 0, s>>>(items_tab, bn, doff, rank, L, tri, delta, abort_flag);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("pair_gather_kernel");
     return DIC_OK;

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+from collections import deque
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -76,16 +77,14 @@ class DeviceEngine:
         _abi.call("dic_engine_seed", self.h, counts.data_ptr(), C.byref(L), C.byref(P))
         return L.value, P.value
 
-    def count(self, lfirst: int, llast: int) -> None:
-        _abi.call("dic_engine_count", self.h, lfirst, llast)
+    def issue_count(self, lfirst: int, llast: int) -> None:
+        _abi.call("dic_engine_issue_count", self.h, lfirst, llast)
 
     def delta(self):
         """The per-stop count deltas as a (non-owning) int64 CUDA tensor."""
         ptr, ln = C.c_void_p(), C.c_int64()
         _abi.call("dic_engine_delta", self.h, C.byref(ptr), C.byref(ln))
         n = ln.value
-        if n == 0:
-            return self._torch.empty(0, dtype=self._torch.int64, device="cuda")
 
         class _View:
             __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr.value, False), "version": 3,
@@ -93,10 +92,15 @@ class DeviceEngine:
 
         return self._torch.as_tensor(_View(), device="cuda")
 
-    def checkpoint(self) -> _abi.StopStatus:
-        st = _abi.StopStatus()
-        _abi.call("dic_engine_checkpoint", self.h, C.byref(st))
-        return st
+    def issue_checkpoint(self) -> int:
+        seq = C.c_int64()
+        _abi.call("dic_engine_issue_checkpoint", self.h, C.byref(seq))
+        return seq.value
+
+    def poll(self, seq: int) -> tuple[_abi.StopStatus, bool]:
+        st, rep = _abi.StopStatus(), C.c_int32()
+        _abi.call("dic_engine_poll", self.h, seq, C.byref(st), C.byref(rep))
+        return st, bool(rep.value)
 
     def frequent(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         F = C.c_int64()
@@ -120,13 +124,14 @@ def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray) -> t
 def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound: bool = True,
                plan: ShardPlan | None = None, group=None, trace: StopTrace | None = None,
                t0: float | None = None, count_events: list | None = None,
-               engine_factory=None) -> MiningResult:
+               engine_factory=None, depth: int = 4) -> MiningResult:
     """The checkpoint loop of _run over one rank's local rows.
 
     ``plan``/``group``: chunk-sliced sharding (sharding.py) with a
     torch.distributed process group; counts are sum-allreduced per stop.
-    ``count_events``: if a list, (start, end, word_tests) CUDA events are
-    appended around every count launch (the bench's roofline figures).
+    ``count_events``: if a list, [start, end, word_popcounts, rows] entries
+    are appended around every count launch (the bench's roofline figures).
+    ``depth``: stops in flight (1 = the reference's strictly sequential loop).
     ``engine_factory``: test seam (a CPU stand-in engine for the gloo
     multi-rank tests); the product always uses DeviceEngine."""
     import torch
@@ -145,32 +150,57 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
         stats.candidates_generated = npairs
         stats.peak_dashed = npairs
         scanned = params.n
-        dashed = npairs
+        # Pipelined checkpoint loop: stops are enqueued up to `depth` ahead
+        # and their statuses consumed in order (the reference's loop test
+        # `while catalog.dashed` is evaluated on the polled status; stops
+        # enqueued after the last live one are no-ops and are not counted).
+        inflight: deque = deque()
         stop = 0
-        while dashed:
-            stop = stop + 1 if stop < params.intervals_per_pass else 1
-            first, last = params.chunk_bounds(stop)
-            lfirst, llast = local_chunks[stop - 1] if local_chunks is not None else (first, last)
-            stats.interval_counts += dashed
+        live = npairs
+        done = live == 0
+        while True:
+            while not done and len(inflight) < depth:
+                stop = stop + 1 if stop < params.intervals_per_pass else 1
+                first, last = params.chunk_bounds(stop)
+                lfirst, llast = local_chunks[stop - 1] if local_chunks is not None else (first, last)
+                if count_events is not None:
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev1 = torch.cuda.Event(enable_timing=True)
+                    ev0.record()
+                    eng.issue_count(lfirst, llast)
+                    ev1.record()
+                    count_events.append([ev0, ev1, 0, llast - lfirst + 1])
+                else:
+                    eng.issue_count(lfirst, llast)
+                if sharded:
+                    dist.all_reduce(eng.delta(), group=group)
+                inflight.append((eng.issue_checkpoint(), stop, first, last))
+            if not inflight:
+                break
+            seq, s_stop, first, last = inflight.popleft()
+            st, replayed = eng.poll(seq)
+            if done:
+                continue  # a no-op stop issued after the last live one
             if count_events is not None:
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                eng.count(lfirst, llast)
-                ev1.record()
-                count_events.append((ev0, ev1, dashed * (-(-max(llast - lfirst + 1, 0) // 32))))
-            else:
-                eng.count(lfirst, llast)
-            if sharded:
-                dist.all_reduce(eng.delta(), group=group)
-            st = eng.checkpoint()
+                # word-popcount work of this stop's count launch
+                ev = count_events[len(count_events) - len(inflight) - 1]
+                ev[2] = st.dashed_at_start * (-(-max(ev[3], 0) // 32))
+            stats.interval_counts += st.dashed_at_start
             scanned += last - first + 1
             stats.candidates_pruned += st.pruned
             stats.candidates_generated += st.inserted
             stats.peak_dashed = max(stats.peak_dashed, st.dashed_peak)
-            dashed = st.dashed_at_end
+            live = st.dashed_at_end
             if trace is not None:
-                trace.stops.append({f: getattr(st, f) for f, _ in _abi.StopStatus._fields_} | {"stop": stop})
+                trace.stops.append({f: getattr(st, f) for f, _ in _abi.StopStatus._fields_} | {"stop": s_stop})
+            if replayed:
+                # stops after seq were skipped on the device: re-issue them
+                if count_events is not None:
+                    del count_events[len(count_events) - len(inflight):]
+                inflight.clear()
+                stop = s_stop
+            if live == 0:
+                done = True
         frequent = sorted_frequent(*eng.frequent())
     finally:
         eng.close()

@@ -104,6 +104,18 @@ class CpuStandInEngine:
         st.dashed_at_end = len(self.cat.dashed)
         return st
 
+    # pipelined protocol of DeviceEngine (statuses are ready immediately here)
+    def issue_count(self, lfirst, llast):
+        self.count(lfirst, llast)
+
+    def issue_checkpoint(self):
+        self._done = getattr(self, "_done", [])
+        self._done.append(self.checkpoint())
+        return len(self._done) - 1
+
+    def poll(self, seq):
+        return self._done[seq], False
+
     def frequent(self):
         recs = [r for r in self.cat.solid if r.shape is Shape.SOLID_BOX]
         W = bits.words_for(self.m)

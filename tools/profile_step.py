@@ -1,0 +1,62 @@
+"""Per-kernel breakdown of one DIC run (torch.profiler / CUPTI; no nsys
+needed): kernel name, launches, total and mean device time, and the share of
+the run's wall time the GPU was busy.  Prints a table and writes JSON."""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from collections import defaultdict
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import paper_1812_10959_b200 as dic  # noqa: E402
+from paper_1812_10959_b200 import device as D  # noqa: E402
+from paper_1812_10959_b200.miner import run_engine  # noqa: E402
+from paper_1812_10959_b200.workloads import CONFIGS, generate_csr  # noqa: E402
+
+
+def main() -> None:
+    idx = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    depth = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    out_json = sys.argv[3] if len(sys.argv) > 3 else None
+    cfg = CONFIGS[idx]
+    D.require_cuda()
+    ip, ix = generate_csr(cfg)
+    db = dic.BitDatabase.from_csr(ip, ix, cfg.m)
+    tids = db.device_tids()
+    params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    run_engine(tids, cfg.n, cfg.m, params, depth=depth)  # warm-up
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        t = time.perf_counter()
+        res = run_engine(tids, cfg.n, cfg.m, params, depth=depth)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t
+    agg = defaultdict(lambda: [0, 0.0])
+    busy = 0.0
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA":
+            continue
+        a = agg[ev.name[:90]]
+        a[0] += 1
+        a[1] += ev.device_time_total / 1000.0  # us -> ms
+        busy += ev.device_time_total / 1000.0
+    rows = sorted(agg.items(), key=lambda kv: -kv[1][1])
+    print(f"{cfg.name}: wall {wall * 1000:.1f} ms, GPU busy {busy:.1f} ms, frequent {len(res.frequent)}")
+    for name, (n, ms) in rows[:25]:
+        print(f"{ms:9.3f} ms {n:6d} x {ms / n * 1000:9.2f} us  {name}")
+    if out_json:
+        Path(out_json).write_text(json.dumps({"config": cfg.name, "depth": depth, "wall_ms": wall * 1000,
+                                              "gpu_busy_ms": busy,
+                                              "kernels": [{"name": k, "launches": n, "total_ms": ms}
+                                                          for k, (n, ms) in rows]}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
