@@ -469,7 +469,15 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
     a.abort = abort_flag;
     a.tri_len = tri_len;
     const size_t smem = 128 + 2 * (size_t)a.tile_bytes;
-    if (smem > (size_t)max_dyn_smem() || kuse > kDevMaxK) {
+    // the kernel's static shared memory (the unit prefix table) shares the budget
+    static size_t static_smem = 0;
+    if (!static_smem) {
+        cudaFuncAttributes fa32, fa16;
+        DIC_CUDA(cudaFuncGetAttributes(&fa32, count_dev_kernel<32>));
+        DIC_CUDA(cudaFuncGetAttributes(&fa16, count_dev_kernel<16>));
+        static_smem = std::max(fa32.sharedSizeBytes, fa16.sharedSizeBytes) + 16;
+    }
+    if (smem + static_smem > (size_t)max_dyn_smem() || kuse > kDevMaxK) {
         count_dev_global_kernel<<<sm_count() * 8, 256, 0, s>>>(a);
         ::dic::note_launch();
         DIC_CHECK_LAUNCH("count_dev_global_kernel");
@@ -478,12 +486,12 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
     static bool attr32 = false, attr16 = false;
     if (a.TW == 32 && !attr32) {
         DIC_CUDA(cudaFuncSetAttribute(count_dev_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      max_dyn_smem()));
+                                      max_dyn_smem() - (int)static_smem));
         attr32 = true;
     }
     if (a.TW == 16 && !attr16) {
         DIC_CUDA(cudaFuncSetAttribute(count_dev_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      max_dyn_smem()));
+                                      max_dyn_smem() - (int)static_smem));
         attr16 = true;
     }
     if (a.TW == 32)
