@@ -49,6 +49,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--config", type=int, default=CFG_INDEX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-bench", action="store_true")
     ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
     return ap.parse_args()
 
@@ -129,6 +130,53 @@ def measured_hbm() -> tuple[float, str]:
         return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
+    """cfg5: dic_count_support over a 50M x 512 i.i.d. Bernoulli(0.05) bitmap
+    for 100k random candidates (k ~ U{2..6}), one launch per size bucket, all
+    rows.  Buckets are sorted lexicographically (any order gives the same
+    counts).  Roofline: >= 1 POPC per (candidate, 32-row word)."""
+    import torch
+
+    from paper_1812_10959_b200 import device as D
+    from paper_1812_10959_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[5]
+    n, m, C = cfg.n, cfg.m, cfg.params["candidates"]
+    rows = D.bernoulli_rows(n, m, cfg.params["p"], cfg.seed)
+    tids = D.rows_to_tids(rows, n, m)
+    del rows
+    ks, items = D.synth_candidates(C, m, cfg.params["kmin"], cfg.params["kmax"], cfg.seed)
+    buckets = []
+    for k in range(cfg.params["kmin"], cfg.params["kmax"] + 1):
+        sel = items[ks == k][:, :k]
+        sel = sel[np.lexsort(sel.T[::-1])]
+        buckets.append(torch.from_numpy(np.ascontiguousarray(sel).view(np.int16)).cuda())
+    outs = [torch.zeros(b.shape[0], dtype=torch.int64, device="cuda") for b in buckets]
+    for b, o in zip(buckets, outs):
+        D.count_support(tids, n, m, 0, n - 1, b, o)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        for o in outs:
+            o.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for b, o in zip(buckets, outs):
+            D.count_support(tids, n, m, 0, n - 1, b, o)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    words = float(C) * ((n + 31) // 32)
+    achieved = words / (best * 1e-3)
+    checksum = int(sum(int(o.sum().item()) for o in outs))
+    del tids
+    torch.cuda.empty_cache()
+    return {"workload": cfg.name, "n": n, "m": m, "candidates": C, "ms": best,
+            "subset_tests_per_s": C * n / (best * 1e-3), "roofline_bound": "int-pipe (POPC)",
+            "achieved_T_word_popcounts_per_s": achieved / 1e12, "peak_T": peaks["popc"] / 1e12,
+            "frac": achieved / peaks["popc"], "support_checksum": checksum}
 
 
 def subset_tests(n: int, m: int, params, trace) -> int:
@@ -262,8 +310,8 @@ def main() -> None:
 
     # roofline of the dominant kernel (the streaming support count) over the
     # last timed run: per launch >= 1 POPC per (candidate, 32-row word)
-    count_ms = [a.elapsed_time(b) for a, b, _ in count_events]
-    words = [w for _, _, w in count_events]
+    count_ms = [ev[0].elapsed_time(ev[1]) for ev in count_events]
+    words = [ev[2] for ev in count_events]
     peaks = int_peaks()
     hbm_gbs, hbm_src = measured_hbm()
     tot_ms = sum(count_ms)
@@ -311,6 +359,11 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, db, params)
+    kernel = None
+    if rank == 0 and world == 1 and not args.no_kernel_bench:
+        del db, tids
+        torch.cuda.empty_cache()
+        kernel = kernel_microbench(peaks)
 
     if rank == 0:
         s = ref.stats
@@ -327,7 +380,7 @@ def main() -> None:
                        "db_passes": s.db_passes, "candidates_generated": s.candidates_generated,
                        "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu, "kernel_microbench": kernel,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -55,7 +55,7 @@ int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
                        cudaStream_t s);
 int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
-                           const int32_t* rank, int64_t L, const unsigned long long* tri,
+                           const int32_t* rank, int64_t L, unsigned long long* tri,
                            unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s);
 
 enum : uint8_t { DASHED_CIRCLE = 0, DASHED_BOX = 1, SOLID_CIRCLE = 2, SOLID_BOX = 3, NIL = 4 };
@@ -215,7 +215,7 @@ __global__ void stop_prep_kernel(unsigned long long* stat, int KS, int kuse, int
 // bucket slot.  Slots already dead (left the dashed vector at an earlier
 // stop, compaction pending) are only marked not-kept.  keep[g] = still dashed.
 __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab, const int64_t* __restrict__ doff,
-                                            int kuse, const unsigned long long* __restrict__ delta, Records R,
+                                            int kuse, unsigned long long* __restrict__ delta, Records R,
                                             int64_t need, int64_t interval, int64_t stop_max, int bound,
                                             int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
                                             unsigned long long* __restrict__ stat) {
@@ -231,8 +231,10 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
             const int32_t r = rec_tab[bk][g - doff[bk]];
             uint8_t sh = R.shape[r];
             bool kept = false;
+            const int64_t dg = (int64_t)delta[g];
+            delta[g] = 0;  // the buffer is zero again for the next stop's count
             if (is_dashed(sh)) {
-                const int64_t s = R.support[r] + (int64_t)delta[g];
+                const int64_t s = R.support[r] + dg;
                 const int64_t iv = R.intervals[r] + 1;
                 R.support[r] = s;
                 R.intervals[r] = iv;
@@ -462,6 +464,18 @@ __global__ void commit_candidates_kernel(int W, const unsigned long long* __rest
     }
 }
 
+// The stop's status into its (host-mapped, pinned) ring slot: head words,
+// then removed[k], adm[k], bn[k] for k < kuse.
+__global__ void status_kernel(const unsigned long long* __restrict__ stat, int KS, int kuse,
+                              unsigned long long* __restrict__ slot) {
+    for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
+    for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
+        slot[S_HEAD + 3 * k] = stat[S_HEAD + k];
+        slot[S_HEAD + 3 * k + 1] = stat[S_HEAD + KS + k];
+        slot[S_HEAD + 3 * k + 2] = stat[S_HEAD + 2 * KS + k];
+    }
+}
+
 __global__ void collect_frequent_kernel(Records R, int64_t nrec, int32_t* out, unsigned long long* nout) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nrec || R.shape[r] != SOLID_BOX) return;
@@ -540,7 +554,8 @@ struct dic_engine {
     int64_t tri_len = 0;
 
     // pipelining
-    unsigned long long* ring = nullptr;  // pinned [kRing][S_HEAD + 3*KS]
+    unsigned long long* ring = nullptr;  // pinned, device-mapped [kRing][S_HEAD + 3*KS]
+    unsigned long long* ring_dev = nullptr;
     cudaEvent_t ev[kRing];
     int64_t ring_words = 0;
     int kuse_at[kRing];                  // kuse when the slot was written
@@ -646,11 +661,11 @@ int ensure_slot_arrays(dic_engine* e) {
     const int64_t nc = std::max<int64_t>(need, e->slot_cap + e->slot_cap / 2);
     dfree(e->delta, e->s);
     dfree(e->keep, e->s);
-    dfree(e->frontier, e->s);
     int rc;
-    if ((rc = dalloc(&e->delta, nc, e->s)) || (rc = dalloc(&e->keep, nc, e->s)) ||
-        (rc = dalloc(&e->frontier, nc, e->s)))
-        return rc;
+    if ((rc = dalloc(&e->delta, nc, e->s)) || (rc = dalloc(&e->keep, nc, e->s))) return rc;
+    DIC_CUDA(cudaMemsetAsync(e->delta, 0, nc * sizeof(unsigned long long), e->s));  // apply re-zeroes
+    // the frontier of a stop awaiting a candidate replay must survive growth
+    if ((rc = dgrow(&e->frontier, e->slot_cap, nc, e->s))) return rc;
     e->slot_cap = nc;
     return DIC_OK;
 }
@@ -725,17 +740,13 @@ int candidate_step(dic_engine* e) {
     return DIC_OK;
 }
 
-// status of the stop in ring slot `slot`: head words and removed / adm / bn
-// for sizes < kuse, then an event
+// status of the stop into ring slot `slot` (one kernel writing host-mapped
+// pinned memory), then an event
 int copy_status(dic_engine* e, int slot) {
-    const int KS = e->KS, ku = e->kuse;
-    const size_t u = sizeof(unsigned long long);
-    unsigned long long* dst = e->ring + (int64_t)slot * e->ring_words;
-    DIC_CUDA(cudaMemcpyAsync(dst, e->d_stat, S_HEAD * u, cudaMemcpyDeviceToHost, e->s));
-    for (int sec = 0; sec < 3; ++sec)
-        DIC_CUDA(cudaMemcpyAsync(dst + S_HEAD + sec * KS, e->d_stat + S_HEAD + sec * KS, ku * u,
-                                 cudaMemcpyDeviceToHost, e->s));
-    e->kuse_at[slot] = ku;
+    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("status_kernel");
+    e->kuse_at[slot] = e->kuse;
     DIC_CUDA(cudaEventRecord(e->ev[slot], e->s));
     return DIC_OK;
 }
@@ -772,11 +783,14 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
         delete e;
         return rc;
     }
-    cudaError_t ce = cudaMallocHost((void**)&e->ring, (size_t)kRing * e->ring_words * sizeof(unsigned long long));
+    cudaError_t ce = cudaHostAlloc((void**)&e->ring, (size_t)kRing * e->ring_words * sizeof(unsigned long long),
+                                   cudaHostAllocMapped);
+    if (ce == cudaSuccess) ce = cudaHostGetDevicePointer((void**)&e->ring_dev, e->ring, 0);
     if (ce != cudaSuccess) {
         delete e;
-        return cuda_fail(ce, "cudaMallocHost");
+        return cuda_fail(ce, "cudaHostAlloc(mapped status ring)");
     }
+    memset(e->ring, 0, (size_t)kRing * e->ring_words * sizeof(unsigned long long));
     for (int i = 0; i < kRing; ++i) {
         cudaEventCreateWithFlags(&e->ev[i], cudaEventDisableTiming);
         e->kuse_at[i] = 0;
@@ -886,6 +900,7 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         }
         e->tri_len = npairs;
         if ((rc = dalloc(&e->tri, npairs, e->s))) return rc;
+        DIC_CUDA(cudaMemsetAsync(e->tri, 0, npairs * sizeof(unsigned long long), e->s));  // gather re-zeroes
     }
     if ((rc = ensure_headroom(e))) return rc;
     if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
@@ -912,7 +927,6 @@ extern "C" int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t lla
     e->cur_first = lfirst;
     e->cur_last = llast;
     e->kuse_issue = e->kuse;
-    DIC_CUDA(cudaMemsetAsync(e->delta, 0, e->slot_cap * sizeof(unsigned long long), e->s));
     stop_prep_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("stop_prep_kernel");
@@ -1055,8 +1069,8 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
     st->records = e->nrec;
     for (int k = 0; k < ku; ++k) {
         Bucket& b = e->buckets[k];
-        b.n = (int64_t)h[S_HEAD + 2 * KS + k];
-        b.dead = (int64_t)h[S_HEAD + k];
+        b.n = (int64_t)h[S_HEAD + 3 * k + 2];
+        b.dead = (int64_t)h[S_HEAD + 3 * k];
         // schedule a compaction when dead slots are a quarter of the bucket
         if (b.n > 0 && b.dead > 0 && (b.dead * 4 >= b.n || b.dead == b.n)) e->compact_next[k] = 1;
     }

@@ -144,7 +144,7 @@ __global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, 
 // sizes and the dense switch come from device memory
 __global__ void pair_gather_kernel(uint16_t* const* __restrict__ items_tab, const unsigned long long* __restrict__ bn,
                                    const int64_t* __restrict__ doff, const int32_t* __restrict__ rank, int64_t L,
-                                   const unsigned long long* __restrict__ tri, unsigned long long* __restrict__ delta,
+                                   unsigned long long* __restrict__ tri, unsigned long long* __restrict__ delta,
                                    const unsigned long long* __restrict__ abort_flag) {
     const int64_t tri_len = L * (L - 1) / 2;
     const int64_t C = (int64_t)bn[2];
@@ -153,7 +153,9 @@ __global__ void pair_gather_kernel(uint16_t* const* __restrict__ items_tab, cons
     unsigned long long* out = delta + doff[2];
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
         const int a = rank[items[2 * c]], b = rank[items[2 * c + 1]];
-        out[c] += tri[tri_index(a, b, L)];
+        const int64_t p = tri_index(a, b, L);
+        out[c] += tri[p];
+        tri[p] = 0;  // zero again for the next stop (each pair has one slot)
     }
 }
 
@@ -205,12 +207,12 @@ int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* ite
 int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                            unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
                            const unsigned long long* abort_flag, cudaStream_t s) {
-    DIC_CUDA(cudaMemsetAsync(tri, 0, (size_t)tri_len * sizeof(unsigned long long), s));
+    // tri is all-zero between stops: the gather re-zeroes every entry it reads
     return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag);
 }
 
 int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
-                           const int32_t* rank, int64_t L, const unsigned long long* tri,
+                           const int32_t* rank, int64_t L, unsigned long long* tri,
                            unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s) {
     pair_gather_kernel<<<sm_count() * 8, 256, 0, s>>>(items_tab, bn, doff, rank, L, tri, delta, abort_flag);
     ::dic::note_launch();
