@@ -75,6 +75,7 @@ struct BucketDesc {
 struct StreamArgs {
     const uint32_t* tids;
     int32_t m, TW;
+    int32_t rowlanes;  // TW == 32: use the conflict-free row-lane units
     uint32_t tile_bytes;
     int64_t t_first, t_last;  // inclusive tile range of the chunk
     int64_t row_splits;
@@ -183,6 +184,113 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     }
 }
 
+// Row-lane variant (TW = 32): 8 lanes share a candidate, lane `sub` reading
+// 16-byte chunk `sub` of each item row, so a quarter-warp always reads one
+// contiguous 128-byte row — conflict-free whatever the items are (random
+// candidates, e.g. cfg5).  Item ids stay packed two per register (the row
+// offset is one IMAD away) so a CTA still holds 64 x R candidates; each
+// lane's partial count is reduced over its 8 lanes once per unit.
+__host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 24 : (K <= 6 ? 16 : 12)); }
+constexpr int kRLSlots = kStreamThreads / 8;  // candidate slots per CTA row
+
+template <int K>
+__device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids, int m, uint32_t tb,
+                                               const ChunkGeom& geom, const uint16_t* __restrict__ items, int64_t C,
+                                               unsigned long long* __restrict__ out, int64_t blk, int64_t t0,
+                                               int64_t t1, uint8_t* smem, uint32_t (&uses)[2]) {
+    constexpr int TW = 32, RB = (TW + 4) * 4, R = rl_regs(K), KP = (K + 1) / 2;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* bufs = smem + 128;
+    const int sub = threadIdx.x & 7, slot = threadIdx.x >> 3;
+    const int64_t cbase = blk * (int64_t)kRLSlots * R;
+    if (threadIdx.x == 0) {
+        fence_proxy_async();
+        issue_tile(smem, tids, tb, t0, 0);
+        if (t0 + 1 < t1) issue_tile(smem, tids, tb, t0 + 1, 1);
+    }
+    uint32_t it[R][KP];
+    uint32_t cnt[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t c = cbase + (int64_t)r * kRLSlots + slot;
+        const int64_t cc = c < C ? c : C - 1;
+        cnt[r] = 0;
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+            uint32_t lo = __ldg(items + cc * K + 2 * j);
+            uint32_t hi = (2 * j + 1 < K) ? (uint32_t)__ldg(items + cc * K + 2 * j + 1) : 0u;
+            it[r][j] = lo | (hi << 16);
+        }
+    }
+    for (int64_t t = t0; t < t1; ++t) {
+        const int s = (int)((t - t0) & 1);
+        mbar_wait(&bar[s], uses[s] & 1u);
+        ++uses[s];
+        uint8_t* base = bufs + (size_t)s * tb;
+        if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
+            uint32_t* w = reinterpret_cast<uint32_t*>(base);
+            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += kStreamThreads) {
+                int item = idx / (TW + 4), sl = idx - item * (TW + 4);
+                if (sl < TW) w[idx] &= group_mask(geom, t * TW + sl);
+            }
+            __syncthreads();
+        }
+        const uint8_t* bs = base + sub * 16;
+        // keep the row offsets derived per tile (one IMAD each) instead of
+        // letting the compiler hoist R*K of them into registers
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int j = 0; j < KP; ++j) asm volatile("" : "+r"(it[r][j]));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint4 v = *reinterpret_cast<const uint4*>(bs + (it[r][0] & 0xFFFFu) * RB);
+#pragma unroll
+            for (int j = 1; j < K; ++j) {
+                const uint32_t item = (j & 1) ? (it[r][j >> 1] >> 16) : (it[r][j >> 1] & 0xFFFFu);
+                v = and4(v, *reinterpret_cast<const uint4*>(bs + item * RB));
+            }
+            cnt[r] += popc4(v);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && t + 2 < t1) {
+            fence_proxy_async();
+            issue_tile(smem, tids, tb, t + 2, s);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        uint32_t x = cnt[r];
+        x += __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x += __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        x += __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+        const int64_t c = cbase + (int64_t)r * kRLSlots + slot;
+        if (sub == 0 && c < C && x) atomicAdd(out + c, (unsigned long long)x);
+    }
+}
+
+__device__ __forceinline__ void dispatch_unit_rl(int k, const uint32_t* tids, int m, uint32_t tb,
+                                                 const ChunkGeom& geom, const uint16_t* items, int64_t C,
+                                                 unsigned long long* out, int64_t blk, int64_t t0, int64_t t1,
+                                                 uint8_t* smem, uint32_t (&uses)[2]) {
+    switch (k) {
+        case 1: stream_unit_rl<1>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 2: stream_unit_rl<2>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 3: stream_unit_rl<3>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 4: stream_unit_rl<4>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 5: stream_unit_rl<5>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 6: stream_unit_rl<6>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 7: stream_unit_rl<7>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        default: stream_unit_rl<8>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+    }
+}
+
+// candidates per block of the unit kind used for (TW, k)
+__host__ __device__ inline int64_t cands_per_block(int TW, int k, bool rowlanes) {
+    if (rowlanes && TW == 32 && k <= 8) return (int64_t)kRLSlots * rl_regs(k);
+    return (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
+}
+
 template <int TW>
 __device__ __forceinline__ void dispatch_unit(int k, const uint32_t* tids, int m, uint32_t tb, const ChunkGeom& geom,
                                               const uint16_t* items, int64_t C, unsigned long long* out,
@@ -228,7 +336,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const _
     if (t0 >= t1) return;
     init_barriers(smem);
     uint32_t uses[2] = {0u, 0u};
-    dispatch_unit<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
+    if (TW == 32 && a.rowlanes && B.k <= 8)
+        dispatch_unit_rl(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
+    else
+        dispatch_unit<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
 }
 
 // Device-sized launch (the engine's per-stop count): bucket sizes, delta
@@ -373,7 +484,7 @@ struct BucketIn {
 
 // Count every bucket over rows [first, last] in as few launches as possible.
 int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
-                         const BucketIn* bk, int nbk, cudaStream_t s) {
+                         const BucketIn* bk, int nbk, cudaStream_t s, bool rowlanes = true) {
     if (last < first) return DIC_OK;
     const int TW = tile_groups(m);
     const ChunkGeom geom = chunk_geom(first, last);
@@ -415,15 +526,16 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
         a.t_last = t_last;
         a.geom = geom;
         int64_t blocks = 0;
+        a.rowlanes = rowlanes ? 1 : 0;
         for (; i < nbk && a.nb < kMaxBuckets; ++i) {
             if (bk[i].C <= 0) continue;
-            const int R = regs_per_thread(bk[i].k <= 8 ? bk[i].k : 0);
+            const int64_t per = cands_per_block(TW, bk[i].k, rowlanes);
             BucketDesc& d = a.b[a.nb++];
             d.items = bk[i].items;
             d.out = bk[i].out;
             d.C = bk[i].C;
             d.k = bk[i].k;
-            d.blocks = (int32_t)((bk[i].C + (int64_t)kStreamThreads * R - 1) / ((int64_t)kStreamThreads * R));
+            d.blocks = (int32_t)((bk[i].C + per - 1) / per);
             blocks += d.blocks;
         }
         if (a.nb == 0) break;
