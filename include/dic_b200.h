@@ -213,6 +213,10 @@ int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st);
  * must re-issue every stop after seq.  At most 15 stops in flight.
  * dic_engine_delta's length is the (rank-independent) slot capacity.      */
 int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t llast);
+/* The dense pair-triangle counts of the stop (device uint64/int64 [*len],
+ * *len == 0 when the engine has none): sharded callers sum-allreduce it
+ * together with dic_engine_delta() before the checkpoint.                 */
+int dic_engine_pair_counts(dic_engine* e, void** ptr, int64_t* len);
 int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq);
 int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st,
                     int32_t* replayed);

@@ -42,6 +42,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// carry-save adder: a + b + c == s + 2*c_out, bitwise (two LOP3s)
+__device__ __forceinline__ void csa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cout) {
+    s = a ^ b ^ c;
+    cout = (a & b) | (b & c) | (a & c);
+}
+
 __device__ __forceinline__ uint32_t popc4(uint4 v) {
     return __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
 }

@@ -54,9 +54,6 @@ int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first
                            const unsigned long long* abort_flag, cudaStream_t s);
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
                        cudaStream_t s);
-int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
-                           const int32_t* rank, int64_t L, unsigned long long* tri,
-                           unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s);
 
 enum : uint8_t { DASHED_CIRCLE = 0, DASHED_BOX = 1, SOLID_CIRCLE = 2, SOLID_BOX = 3, NIL = 4 };
 
@@ -82,8 +79,10 @@ enum : int {
     S_NREC = 7,      // records (persistent)
     S_ABORT = 8,     // persistent: set with OVERFLOW, cleared by the host's replay
     S_SCRATCH = 9,   // scratch word (result collection)
-    S_HEAD = 10
+    S_DONE = 10,     // eval blocks finished (last one runs the capacity check)
+    S_HEAD = 12
 };
+constexpr int kDoffMax = 256;  // delta offsets kept for sizes < 256
 // followed by: removed[KS] (slots not kept this stop), adm[KS] (admitted
 // joins by size), bn[KS] (bucket fill, persistent), KS = m + 2.
 
@@ -191,36 +190,30 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
 // ---------------------------------------------------------------------------
 // per stop (every kernel: no-op while the abort flag is up)
 // ---------------------------------------------------------------------------
-// Reset the per-stop counters and compute the delta offsets of the buckets.
-__global__ void stop_prep_kernel(unsigned long long* stat, int KS, int kuse, int64_t* doff) {
-    if (stat[S_ABORT]) return;
-    for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
-    for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
-        stat[S_HEAD + k] = 0;       // removed
-        stat[S_HEAD + KS + k] = 0;  // adm
-    }
-    if (threadIdx.x == 0) {
-        const unsigned long long* bn = stat + S_HEAD + 2 * KS;
-        int64_t acc = 0;
-        for (int k = 0; k < kuse; ++k) {
-            doff[k] = acc;
-            acc += (int64_t)bn[k];
-        }
-        doff[kuse] = acc;
-    }
-}
-
 // support += delta, intervals += 1 (count_support_interval), then prune
 // (engine.py:292-310) and check_full_pass (:380-388), grid-stride over every
 // bucket slot.  Slots already dead (left the dashed vector at an earlier
 // stop, compaction pending) are only marked not-kept.  keep[g] = still dashed.
+struct PairArgs {  // the dense pair triangle (tri == nullptr: none)
+    unsigned long long* tri;
+    const int32_t* rank;
+    uint16_t* const* items_tab;
+    int64_t L, tri_len;
+};
+
+__device__ __forceinline__ int64_t tri_pos(int64_t a, int64_t b, int64_t L) {
+    return a * L - a * (a + 1) / 2 + (b - a - 1);
+}
+
 __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab, const int64_t* __restrict__ doff,
                                             int kuse, unsigned long long* __restrict__ delta, Records R,
                                             int64_t need, int64_t interval, int64_t stop_max, int bound,
                                             int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
-                                            unsigned long long* __restrict__ stat) {
+                                            unsigned long long* __restrict__ stat, PairArgs pa, int KS) {
     if (stat[S_ABORT]) return;
     const int64_t total = doff[kuse];
+    // pair counts come from the triangle while the pair bucket is dense
+    const bool dense = pa.tri != nullptr && 2 * (int64_t)stat[S_HEAD + 2 * KS + 2] >= pa.tri_len;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t span = ((total + stride - 1) / stride) * stride;  // uniform trip count for the warp votes
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < span; g += stride) {
@@ -228,11 +221,18 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
         int bk = 0;
         if (g < total) {
             while (bk + 1 < kuse && g >= doff[bk + 1]) ++bk;
-            const int32_t r = rec_tab[bk][g - doff[bk]];
+            const int64_t c = g - doff[bk];
+            const int32_t r = rec_tab[bk][c];
             uint8_t sh = R.shape[r];
             bool kept = false;
-            const int64_t dg = (int64_t)delta[g];
+            int64_t dg = (int64_t)delta[g];
             delta[g] = 0;  // the buffer is zero again for the next stop's count
+            if (bk == 2 && dense) {
+                const uint16_t* it = pa.items_tab[2] + 2 * c;
+                const int64_t p = tri_pos(pa.rank[it[0]], pa.rank[it[1]], pa.L);
+                dg = (int64_t)pa.tri[p];
+                pa.tri[p] = 0;  // each pair has one slot: zero again for the next stop
+            }
             if (is_dashed(sh)) {
                 const int64_t s = R.support[r] + dg;
                 const int64_t iv = R.intervals[r] + 1;
@@ -328,11 +328,15 @@ __global__ void __launch_bounds__(kCompactThreads) compact_bucket_kernel(
 // Admission needs cand not in known and every immediate subset known with a
 // box shape; the subset equal to src is a box by construction (it was just
 // promoted) and is skipped.
+__device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap, int64_t hcap,
+                               const int64_t* __restrict__ bcap);
+
 __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, const int32_t* __restrict__ level1,
                                        int64_t L, int W, Records R, const int32_t* __restrict__ ht, uint64_t hmask,
                                        unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
                                        int32_t* __restrict__ tmp_size, int64_t tmp_cap,
-                                       unsigned long long* __restrict__ stat, int KS) {
+                                       unsigned long long* __restrict__ stat, int KS, int64_t rec_cap, int64_t hcap,
+                                       const int64_t* __restrict__ bcap) {
     if (stat[S_ABORT]) return;
     const int64_t total = (int64_t)stat[S_NFRONT] * L;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -370,24 +374,39 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
             tmp_size[pos] = sz;
         }
     }
+    // the last block to finish runs the all-or-nothing capacity check
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&stat[S_DONE], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        check_capacity(stat, KS, tmp_cap, rec_cap, hcap, bcap);
+        if (threadIdx.x == 0) stat[S_DONE] = 0;
+    }
 }
 
-// All-or-nothing capacity check for the candidate step; an overflow also
-// raises the abort flag so every later stop is skipped until the replay.
-__global__ void check_capacity_kernel(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap,
-                                      int64_t hcap, const int64_t* __restrict__ bcap) {
-    if (stat[S_ABORT]) return;
+// All-or-nothing capacity check for the candidate step (run by the last
+// eval block); an overflow also raises the abort flag so every later stop is
+// skipped until the host's replay.
+__device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap, int64_t hcap,
+                               const int64_t* __restrict__ bcap) {
     __shared__ int over;
     if (threadIdx.x == 0) {
-        const unsigned long long na = stat[S_NADM];
+        const unsigned long long na = *(volatile unsigned long long*)&stat[S_NADM];
         over = (int64_t)na > tmp_cap || (int64_t)(stat[S_NREC] + na) > rec_cap ||
                (int64_t)(stat[S_NREC] + na) * 2 > hcap;
     }
     __syncthreads();
-    const unsigned long long* adm = stat + S_HEAD + KS;
+    const volatile unsigned long long* adm = stat + S_HEAD + KS;
     const unsigned long long* bn = stat + S_HEAD + 2 * KS;
-    for (int k = threadIdx.x; k < KS; k += blockDim.x)
-        if (adm[k] && (int64_t)(bn[k] + adm[k]) > bcap[k]) over = 1;
+    for (int k = threadIdx.x; k < KS; k += blockDim.x) {
+        const unsigned long long ak = adm[k];
+        if (ak && (int64_t)(bn[k] + ak) > bcap[k]) over = 1;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         stat[S_OVERFLOW] = over ? 1ull : 0ull;
@@ -395,23 +414,48 @@ __global__ void check_capacity_kernel(unsigned long long* stat, int KS, int64_t 
     }
 }
 
-// Dedup the admissible joins: claim a hash slot per distinct mask.  Slots
-// hold either a record id or kTempFlag | tmp index (resolved by commit).
-__global__ void insert_candidates_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
-                                         const uint64_t* __restrict__ tmp_hash, Records R, int32_t* ht,
-                                         uint64_t hmask, int64_t* __restrict__ tmp_slot,
-                                         const unsigned long long* __restrict__ stat) {
+// Dedup + commit the admissible joins in one pass: the thread whose CAS
+// claims a hash slot for a mask creates the record, appends it to its size
+// bucket and publishes the record id in the slot; a thread meeting an
+// occupied slot compares masks (temporary entries: kTempFlag | tmp index)
+// and drops its join as a duplicate.  Records published in this kernel are
+// read through L2 (__ldcg): L1 is not coherent within a launch.
+__global__ void insert_commit_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
+                                     const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
+                                     Records R, int32_t* ht, uint64_t hmask, unsigned long long* stat, int KS,
+                                     int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
     if (stat[S_ABORT]) return;
     const int64_t na = (int64_t)stat[S_NADM];
+    unsigned long long* bn = stat + S_HEAD + 2 * KS;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t h = tmp_hash[t];
         const unsigned long long* mk = tmp_mask + t * W;
         uint64_t slot = mix64(h) & hmask;
-        tmp_slot[t] = -1;
         while (true) {
             const int32_t prev = atomicCAS(ht + slot, kEmpty, kTempFlag | (int32_t)t);
             if (prev == kEmpty) {
-                tmp_slot[t] = (int64_t)slot;
+                const int64_t r = (int64_t)atomicAdd(&stat[S_NREC], 1ull);
+                atomicAdd(&stat[S_NINS], 1ull);
+                const int sz = tmp_size[t];
+                for (int w = 0; w < W; ++w) R.mask[r * W + w] = mk[w];
+                R.hash[r] = h;
+                R.size[r] = sz;
+                R.support[r] = 0;
+                R.intervals[r] = 0;
+                R.shape[r] = DASHED_CIRCLE;
+                const unsigned long long pos = atomicAdd(bn + sz, 1ull);
+                b_rec_tab[sz][pos] = (int32_t)r;
+                uint16_t* it = b_items_tab[sz] + (int64_t)pos * sz;
+                int j = 0;
+                for (int w = 0; w < W; ++w) {
+                    unsigned long long x = mk[w];
+                    while (x) {
+                        it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
+                        x &= x - 1;
+                    }
+                }
+                __threadfence();
+                atomicExch(ht + slot, (int32_t)r);
                 break;
             }
             bool same;
@@ -420,8 +464,8 @@ __global__ void insert_candidates_kernel(int W, const unsigned long long* __rest
                 same = tmp_hash[o] == h;
                 for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
             } else {
-                same = R.hash[prev] == h;
-                for (int w = 0; same && w < W; ++w) same = R.mask[(int64_t)prev * W + w] == mk[w];
+                same = __ldcg(R.hash + prev) == h;
+                for (int w = 0; same && w < W; ++w) same = __ldcg(R.mask + (int64_t)prev * W + w) == mk[w];
             }
             if (same) break;  // duplicate of a join admitted by another thread
             slot = (slot + 1) & hmask;
@@ -429,50 +473,37 @@ __global__ void insert_candidates_kernel(int W, const unsigned long long* __rest
     }
 }
 
-__global__ void commit_candidates_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
-                                         const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
-                                         const int64_t* __restrict__ tmp_slot, Records R, int32_t* ht,
-                                         unsigned long long* stat, int KS, int32_t* const* __restrict__ b_rec_tab,
-                                         uint16_t* const* __restrict__ b_items_tab) {
-    if (stat[S_ABORT]) return;
-    const int64_t na = (int64_t)stat[S_NADM];
-    unsigned long long* bn = stat + S_HEAD + 2 * KS;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t slot = tmp_slot[t];
-        if (slot < 0) continue;
-        const int64_t r = (int64_t)atomicAdd(&stat[S_NREC], 1ull);
-        atomicAdd(&stat[S_NINS], 1ull);
-        const int sz = tmp_size[t];
-        for (int w = 0; w < W; ++w) R.mask[r * W + w] = tmp_mask[t * W + w];
-        R.hash[r] = tmp_hash[t];
-        R.size[r] = sz;
-        R.support[r] = 0;
-        R.intervals[r] = 0;
-        R.shape[r] = DASHED_CIRCLE;
-        ht[slot] = (int32_t)r;
-        const unsigned long long pos = atomicAdd(bn + sz, 1ull);
-        b_rec_tab[sz][pos] = (int32_t)r;
-        uint16_t* it = b_items_tab[sz] + (int64_t)pos * sz;
-        int j = 0;
-        for (int w = 0; w < W; ++w) {
-            unsigned long long x = tmp_mask[t * W + w];
-            while (x) {
-                it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
-                x &= x - 1;
-            }
-        }
-    }
-}
-
 // The stop's status into its (host-mapped, pinned) ring slot: head words,
 // then removed[k], adm[k], bn[k] for k < kuse.
-__global__ void status_kernel(const unsigned long long* __restrict__ stat, int KS, int kuse,
-                              unsigned long long* __restrict__ slot) {
-    for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
-    for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
-        slot[S_HEAD + 3 * k] = stat[S_HEAD + k];
-        slot[S_HEAD + 3 * k + 1] = stat[S_HEAD + KS + k];
-        slot[S_HEAD + 3 * k + 2] = stat[S_HEAD + 2 * KS + k];
+// Then (unless the stop overflowed: the replay needs its counters) reset the
+// per-stop counters and compute the next stop's delta offsets from the
+// bucket fill.  slot == nullptr: reset only (engine seeding).
+__global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int kuse,
+                              unsigned long long* __restrict__ slot, int64_t* __restrict__ doff) {
+    if (slot) {
+        for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
+        for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
+            slot[S_HEAD + 3 * k] = stat[S_HEAD + k];
+            slot[S_HEAD + 3 * k + 1] = stat[S_HEAD + KS + k];
+            slot[S_HEAD + 3 * k + 2] = stat[S_HEAD + 2 * KS + k];
+        }
+    }
+    __syncthreads();
+    if (stat[S_ABORT]) return;
+    for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
+    for (int k = threadIdx.x; k < KS && k < kDoffMax; k += blockDim.x) {
+        stat[S_HEAD + k] = 0;       // removed
+        stat[S_HEAD + KS + k] = 0;  // adm
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long* bn = stat + S_HEAD + 2 * KS;
+        int64_t acc = 0;
+        const int top = KS < kDoffMax ? KS : kDoffMax;
+        for (int k = 0; k < top; ++k) {
+            doff[k] = acc;
+            acc += (int64_t)bn[k];
+        }
+        doff[top] = acc;
     }
 }
 
@@ -680,6 +711,10 @@ int grow_bucket(dic_engine* e, int k, int64_t need_cap, bool* changed) {
     b.cap = nc;
     *changed = true;
     e->kuse = std::max(e->kuse, std::min(k + 2, e->KS));
+    if (e->kuse > kDoffMax) {
+        set_error("dic_engine: itemsets of more than %d items are not supported", kDoffMax - 2);
+        return DIC_EINVAL;
+    }
     return DIC_OK;
 }
 
@@ -726,15 +761,10 @@ int candidate_step(dic_engine* e) {
     unsigned long long* st = e->d_stat;
     eval_candidates_kernel<<<G, 256, 0, e->s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
                                                  (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
-                                                 e->tmp_cap, st, e->KS);
+                                                 e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap);
     ::dic::note_launch();
-    check_capacity_kernel<<<1, 256, 0, e->s>>>(st, e->KS, e->tmp_cap, e->R.cap, e->hcap, e->d_bcap);
-    ::dic::note_launch();
-    insert_candidates_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->R, e->ht, (uint64_t)e->hcap - 1,
-                                                   e->tmp_slot, st);
-    ::dic::note_launch();
-    commit_candidates_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->R,
-                                                   e->ht, st, e->KS, e->d_brec, e->d_bitems);
+    insert_commit_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht,
+                                               (uint64_t)e->hcap - 1, st, e->KS, e->d_brec, e->d_bitems);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("candidate_step");
     return DIC_OK;
@@ -743,7 +773,8 @@ int candidate_step(dic_engine* e) {
 // status of the stop into ring slot `slot` (one kernel writing host-mapped
 // pinned memory), then an event
 int copy_status(dic_engine* e, int slot) {
-    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words);
+    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words,
+                                       e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
     e->kuse_at[slot] = e->kuse;
@@ -903,6 +934,10 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         DIC_CUDA(cudaMemsetAsync(e->tri, 0, npairs * sizeof(unsigned long long), e->s));  // gather re-zeroes
     }
     if ((rc = ensure_headroom(e))) return rc;
+    // per-stop counters zero, first stop's delta offsets
+    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, e->d_doff);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("status_kernel");
     if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
     e->live = npairs;
     e->seeded = true;
@@ -927,18 +962,12 @@ extern "C" int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t lla
     e->cur_first = lfirst;
     e->cur_last = llast;
     e->kuse_issue = e->kuse;
-    stop_prep_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->d_doff);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("stop_prep_kernel");
     if (llast >= lfirst) {
         const unsigned long long* abort_flag = e->d_stat + S_ABORT;
         const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
         if (e->tri) {
             if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
                                              e->tri_len, abort_flag, e->s)))
-                return rc;
-            if ((rc = pair_gather_dev_launch(e->d_bitems, bn, e->d_doff, e->rank, e->nL1, e->tri, e->delta,
-                                             abort_flag, e->s)))
                 return rc;
         }
         if ((rc = count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse, e->d_bitems, bn, e->d_doff,
@@ -956,6 +985,13 @@ extern "C" int dic_engine_delta(dic_engine* e, void** ptr, int64_t* len) {
     return DIC_OK;
 }
 
+extern "C" int dic_engine_pair_counts(dic_engine* e, void** ptr, int64_t* len) {
+    DIC_REQUIRE(e && ptr && len, "dic_engine_pair_counts: null argument");
+    *ptr = e->tri;
+    *len = e->tri ? e->tri_len : 0;
+    return DIC_OK;
+}
+
 extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     DIC_REQUIRE(e && seq, "dic_engine_issue_checkpoint: null argument");
     if (!e->counted) { set_error("dic_engine_issue_checkpoint: no count issued"); return DIC_ESTATE; }
@@ -967,9 +1003,10 @@ extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     int rc;
     const int KS = e->KS;
     // 1. apply + prune + finalize over every slot
+    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0};
     apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, e->s>>>(
         e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
-        e->keep, e->d_stat);
+        e->keep, e->d_stat, pa, e->KS);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
     // 2. compaction the host scheduled from an earlier status

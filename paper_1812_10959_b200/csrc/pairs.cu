@@ -95,17 +95,35 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
             }
             __syncthreads();
         }
+        // two 16-byte chunks (8 words = 256 rows) per step; per pair the 8
+        // AND'ed words go through a carry-save tree (7 -> ones/twos/fours,
+        // plus one leftover): 4 POPC + 8 LOP3 instead of 8 POPC, which moves
+        // the bound from the POPC pipe (16 lanes/SM/clk) to LOP3 (64)
 #pragma unroll
-        for (int q = 0; q < TW / 4; ++q) {
-            uint4 av[4], bv[4];
+        for (int q = 0; q < TW / 4; q += 2) {
+            uint4 av0[4], av1[4], bv0[4], bv1[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
+            for (int i = 0; i < 4; ++i) {
+                av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
+                av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16 + 16);
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
+            for (int j = 0; j < 4; ++j) {
+                bv0[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
+                bv1[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) cnt[i][j] += popc4(and4(av[i], bv[j]));
+                for (int j = 0; j < 4; ++j) {
+                    const uint4 x = and4(av0[i], bv0[j]), y = and4(av1[i], bv1[j]);
+                    uint32_t c1, c2, c3, s1, s2, s3, t, f;
+                    csa(x.x, x.y, x.z, s1, c1);
+                    csa(x.w, y.x, y.y, s2, c2);
+                    csa(s1, s2, y.z, s3, c3);
+                    csa(c1, c2, c3, t, f);
+                    cnt[i][j] += __popc(s3) + __popc(y.w) + 2u * __popc(t) + 4u * __popc(f);
+                }
         }
         __syncthreads();  // stage s consumed
         if (threadIdx.x == 0 && t + 2 < t1) {
@@ -140,26 +158,8 @@ __global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, 
     }
 }
 
-// delta[c] += tri[pair of bucket-2 slot c] (ranks of its two items among L1);
-// sizes and the dense switch come from device memory
-__global__ void pair_gather_kernel(uint16_t* const* __restrict__ items_tab, const unsigned long long* __restrict__ bn,
-                                   const int64_t* __restrict__ doff, const int32_t* __restrict__ rank, int64_t L,
-                                   unsigned long long* __restrict__ tri, unsigned long long* __restrict__ delta,
-                                   const unsigned long long* __restrict__ abort_flag) {
-    const int64_t tri_len = L * (L - 1) / 2;
-    const int64_t C = (int64_t)bn[2];
-    if (*abort_flag || 2 * C < tri_len) return;
-    const uint16_t* items = items_tab[2];
-    unsigned long long* out = delta + doff[2];
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
-        const int a = rank[items[2 * c]], b = rank[items[2 * c + 1]];
-        const int64_t p = tri_index(a, b, L);
-        out[c] += tri[p];
-        tri[p] = 0;  // zero again for the next stop (each pair has one slot)
-    }
-}
-
 static int g_pair_attr = 0;
+static int g_pair_slots[2] = {0, 0};  // resident CTAs per SM for TW = 16 / 32
 
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                        unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
@@ -178,9 +178,17 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
         DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
         g_pair_attr = 1;
     }
-    // about four resident CTAs per SM
-    const int64_t target = 4LL * sm_count();
-    int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (target + blocks - 1) / blocks));
+    // one full wave: as many row splits as the resident CTA slots allow
+    int& per_sm = g_pair_slots[TW == 32 ? 1 : 0];
+    if (per_sm == 0) {
+        if (TW == 32)
+            DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<32>, kPairThreads, smem));
+        else
+            DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<16>, kPairThreads, smem));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t slots = (int64_t)per_sm * sm_count();
+    int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, slots / blocks));
     dim3 grid((unsigned)rs, (unsigned)blocks);
     if (TW == 32)
         pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
@@ -211,14 +219,6 @@ int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first
     return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag);
 }
 
-int pair_gather_dev_launch(uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
-                           const int32_t* rank, int64_t L, unsigned long long* tri,
-                           unsigned long long* delta, const unsigned long long* abort_flag, cudaStream_t s) {
-    pair_gather_kernel<<<sm_count() * 8, 256, 0, s>>>(items_tab, bn, doff, rank, L, tri, delta, abort_flag);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("pair_gather_kernel");
-    return DIC_OK;
-}
 
 }  // namespace dic
 

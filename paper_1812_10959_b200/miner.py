@@ -80,17 +80,26 @@ class DeviceEngine:
     def issue_count(self, lfirst: int, llast: int) -> None:
         _abi.call("dic_engine_issue_count", self.h, lfirst, llast)
 
-    def delta(self):
-        """The per-stop count deltas as a (non-owning) int64 CUDA tensor."""
+    def _device_view(self, fn: str):
         ptr, ln = C.c_void_p(), C.c_int64()
-        _abi.call("dic_engine_delta", self.h, C.byref(ptr), C.byref(ln))
+        _abi.call(fn, self.h, C.byref(ptr), C.byref(ln))
         n = ln.value
+        if n == 0:
+            return self._torch.empty(0, dtype=self._torch.int64, device="cuda")
 
         class _View:
             __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr.value, False), "version": 3,
                                         "strides": None}
 
         return self._torch.as_tensor(_View(), device="cuda")
+
+    def delta(self):
+        """The per-stop count deltas as a (non-owning) int64 CUDA tensor."""
+        return self._device_view("dic_engine_delta")
+
+    def pair_counts(self):
+        """The per-stop dense pair-triangle counts (empty if none)."""
+        return self._device_view("dic_engine_pair_counts")
 
     def issue_checkpoint(self) -> int:
         seq = C.c_int64()
@@ -174,6 +183,9 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
                     eng.issue_count(lfirst, llast)
                 if sharded:
                     dist.all_reduce(eng.delta(), group=group)
+                    tri = eng.pair_counts()
+                    if tri.numel():
+                        dist.all_reduce(tri, group=group)
                 inflight.append((eng.issue_checkpoint(), stop, first, last))
             if not inflight:
                 break

@@ -67,6 +67,9 @@ class CpuStandInEngine:
     def delta(self):
         return self._delta
 
+    def pair_counts(self):
+        return torch.empty(0, dtype=torch.int64)
+
     def checkpoint(self):
         st = _abi.StopStatus()
         st.dashed_at_start = len(self.cat.dashed)
