@@ -337,7 +337,8 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                                        int32_t* __restrict__ tmp_size, int64_t tmp_cap,
                                        unsigned long long* __restrict__ stat, int KS, int64_t rec_cap, int64_t hcap,
                                        const int64_t* __restrict__ bcap) {
-    if (stat[S_ABORT]) return;
+    // nothing promoted: no joins, OVERFLOW stays 0 (reset by the last status)
+    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t total = (int64_t)stat[S_NFRONT] * L;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -424,7 +425,7 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
                                      const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
                                      Records R, int32_t* ht, uint64_t hmask, unsigned long long* stat, int KS,
                                      int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
-    if (stat[S_ABORT]) return;
+    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t na = (int64_t)stat[S_NADM];
     unsigned long long* bn = stat + S_HEAD + 2 * KS;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
@@ -495,16 +496,21 @@ __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int
         stat[S_HEAD + k] = 0;       // removed
         stat[S_HEAD + KS + k] = 0;  // adm
     }
-    if (threadIdx.x == 0) {
-        const unsigned long long* bn = stat + S_HEAD + 2 * KS;
-        int64_t acc = 0;
-        const int top = KS < kDoffMax ? KS : kDoffMax;
-        for (int k = 0; k < top; ++k) {
-            doff[k] = acc;
-            acc += (int64_t)bn[k];
-        }
-        doff[top] = acc;
+    // exclusive prefix of the bucket fill (blockDim == kDoffMax threads)
+    __shared__ int64_t sh[kDoffMax];
+    const int top = KS < kDoffMax ? KS : kDoffMax;
+    const int k = threadIdx.x;
+    const int64_t v = k < top ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
+    sh[k] = v;
+    __syncthreads();
+    for (int off = 1; off < kDoffMax; off <<= 1) {
+        const int64_t add = k >= off ? sh[k - off] : 0;
+        __syncthreads();
+        sh[k] += add;
+        __syncthreads();
     }
+    if (k < top) doff[k] = sh[k] - v;
+    if (k == top - 1) doff[top] = sh[k];
 }
 
 __global__ void collect_frequent_kernel(Records R, int64_t nrec, int32_t* out, unsigned long long* nout) {
@@ -773,8 +779,8 @@ int candidate_step(dic_engine* e) {
 // status of the stop into ring slot `slot` (one kernel writing host-mapped
 // pinned memory), then an event
 int copy_status(dic_engine* e, int slot) {
-    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words,
-                                       e->d_doff);
+    status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words,
+                                            e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
     e->kuse_at[slot] = e->kuse;
@@ -935,7 +941,7 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     }
     if ((rc = ensure_headroom(e))) return rc;
     // per-stop counters zero, first stop's delta offsets
-    status_kernel<<<1, 256, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, e->d_doff);
+    status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
     if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
