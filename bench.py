@@ -310,7 +310,7 @@ def main() -> None:
 
     # roofline of the dominant kernel (the streaming support count) over the
     # last timed run: per launch >= 1 POPC per (candidate, 32-row word)
-    count_ms = [ev[0].elapsed_time(ev[1]) for ev in count_events]
+    count_ms = [ev[1] if ev[0] == "native" else ev[0].elapsed_time(ev[1]) for ev in count_events]
     words = [ev[2] for ev in count_events]
     peaks = int_peaks()
     hbm_gbs, hbm_src = measured_hbm()

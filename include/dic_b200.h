@@ -220,6 +220,24 @@ int dic_engine_pair_counts(dic_engine* e, void** ptr, int64_t* len);
 int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq);
 int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st,
                     int32_t* replayed);
+/* The whole pipelined loop on one unsharded GPU, natively: stop s (1-based,
+ * wrapping after stop_max) counts local rows [lfirst[s-1], llast[s-1]] and
+ * scans rows[s-1] global rows; `depth` stops in flight.  *out receives the
+ * loop's MiningStats counters; count_ms / dashed (optional, max_stops
+ * entries) the CUDA-event time of each stop's count launches and its
+ * |dashed| at start.                                                      */
+typedef struct dic_run_stats {
+    int64_t stops;
+    int64_t scanned;
+    int64_t interval_counts;
+    int64_t candidates_generated;
+    int64_t candidates_pruned;
+    int64_t peak_dashed;
+} dic_run_stats;
+int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_t* llast,
+                   const int64_t* rows, int64_t stop_max, int32_t depth,
+                   dic_run_stats* out, float* count_ms, int64_t* dashed,
+                   int64_t max_stops);
 /* Results: number of SOLID_BOX records, then copy them out to HOST arrays
  * masks[F][W] (uint64), sizes[F], supports[F] (unsorted).  Synchronising. */
 int dic_engine_num_frequent(dic_engine* e, int64_t* F);

@@ -31,6 +31,17 @@ class StopStatus(C.Structure):
     ]
 
 
+class RunStats(C.Structure):
+    _fields_ = [
+        ("stops", i64),
+        ("scanned", i64),
+        ("interval_counts", i64),
+        ("candidates_generated", i64),
+        ("candidates_pruned", i64),
+        ("peak_dashed", i64),
+    ]
+
+
 # name -> (restype, argtypes); kept in the order of include/dic_b200.h
 SIGNATURES: dict[str, tuple] = {
     "dic_abi_version": (C.c_int, []),
@@ -58,6 +69,7 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_pair_counts": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_issue_checkpoint": (C.c_int, [vp, P(i64)]),
     "dic_engine_poll": (C.c_int, [vp, i64, P(StopStatus), P(i32)]),
+    "dic_engine_run": (C.c_int, [vp, vp, vp, vp, i64, i32, P(RunStats), vp, vp, i64]),
     "dic_engine_num_frequent": (C.c_int, [vp, P(i64)]),
     "dic_engine_frequent": (C.c_int, [vp, vp, vp, vp, i64]),
     "dic_engine_words": (C.c_int, [vp]),

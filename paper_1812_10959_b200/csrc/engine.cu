@@ -39,6 +39,7 @@
 // engine omits it; the API-level prune on host catalogs keeps it.
 #include "common.cuh"
 
+#include <deque>
 #include <vector>
 
 namespace dic {
@@ -1134,6 +1135,70 @@ extern "C" int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st) {
     if (rc) return rc;
     int32_t replayed = 0;
     return dic_engine_poll(e, seq, st, &replayed);
+}
+
+// The whole pipelined checkpoint loop of one unsharded GPU, natively (the
+// host side of _run, engine.py:422-441, with up to `depth` stops in flight).
+extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_t* llast, const int64_t* rows,
+                              int64_t stop_max, int32_t depth, dic_run_stats* out, float* count_ms,
+                              int64_t* dashed, int64_t max_stops) {
+    DIC_REQUIRE(e && lfirst && llast && rows && out, "dic_engine_run: null argument");
+    DIC_REQUIRE(stop_max >= 1 && depth >= 1 && depth < kRing, "dic_engine_run: bad stop_max/depth");
+    if (!e->seeded) { set_error("dic_engine_run: engine not seeded"); return DIC_ESTATE; }
+    memset(out, 0, sizeof(*out));
+    struct Flight { int64_t seq; int64_t stop; };
+    std::deque<Flight> inflight;
+    cudaEvent_t t0[kRing], t1[kRing];
+    const bool timed = count_ms != nullptr;
+    if (timed)
+        for (int i = 0; i < kRing; ++i) {
+            DIC_CUDA(cudaEventCreate(&t0[i]));
+            DIC_CUDA(cudaEventCreate(&t1[i]));
+        }
+    int rc = DIC_OK;
+    int64_t stop = 0;
+    bool done = e->live == 0;
+    while (rc == DIC_OK) {
+        while (!done && (int64_t)inflight.size() < depth) {
+            stop = stop < stop_max ? stop + 1 : 1;
+            const int slot = (int)(e->issued % kRing);
+            if (timed) cudaEventRecord(t0[slot], e->s);
+            if ((rc = dic_engine_issue_count(e, lfirst[stop - 1], llast[stop - 1]))) break;
+            if (timed) cudaEventRecord(t1[slot], e->s);
+            int64_t seq = 0;
+            if ((rc = dic_engine_issue_checkpoint(e, &seq))) break;
+            inflight.push_back({seq, stop});
+        }
+        if (rc || inflight.empty()) break;
+        const Flight f = inflight.front();
+        inflight.pop_front();
+        dic_stop_status st;
+        int32_t replayed = 0;
+        if ((rc = dic_engine_poll(e, f.seq, &st, &replayed))) break;
+        if (done) continue;  // a no-op stop issued after the last live one
+        const int64_t i = out->stops;
+        if (i < max_stops) {
+            if (timed) cudaEventElapsedTime(&count_ms[i], t0[f.seq % kRing], t1[f.seq % kRing]);
+            if (dashed) dashed[i] = st.dashed_at_start;
+        }
+        out->stops++;
+        out->interval_counts += st.dashed_at_start;
+        out->scanned += rows[f.stop - 1];
+        out->candidates_generated += st.inserted;
+        out->candidates_pruned += st.pruned;
+        out->peak_dashed = std::max<int64_t>(out->peak_dashed, st.dashed_peak);
+        if (replayed) {  // stops after f.seq were skipped on the device: re-issue them
+            inflight.clear();
+            stop = f.stop;
+        }
+        if (st.dashed_at_end == 0) done = true;
+    }
+    if (timed)
+        for (int i = 0; i < kRing; ++i) {
+            cudaEventDestroy(t0[i]);
+            cudaEventDestroy(t1[i]);
+        }
+    return rc;
 }
 
 extern "C" int dic_engine_num_frequent(dic_engine* e, int64_t* F) {

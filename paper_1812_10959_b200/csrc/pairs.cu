@@ -115,15 +115,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint4 x = and4(av0[i], bv0[j]), y = and4(av1[i], bv1[j]);
-                    uint32_t c1, c2, c3, s1, s2, s3, t, f;
-                    csa(x.x, x.y, x.z, s1, c1);
-                    csa(x.w, y.x, y.y, s2, c2);
-                    csa(s1, s2, y.z, s3, c3);
-                    csa(c1, c2, c3, t, f);
-                    cnt[i][j] += __popc(s3) + __popc(y.w) + 2u * __popc(t) + 4u * __popc(f);
-                }
+                for (int j = 0; j < 4; ++j) cnt[i][j] += and_popc8(av0[i], av1[i], bv0[j], bv1[j]);
         }
         __syncthreads();  // stage s consumed
         if (threadIdx.x == 0 && t + 2 < t1) {

@@ -111,6 +111,17 @@ class DeviceEngine:
         _abi.call("dic_engine_poll", self.h, seq, C.byref(st), C.byref(rep))
         return st, bool(rep.value)
 
+    def run(self, lfirst: np.ndarray, llast: np.ndarray, rows: np.ndarray, stop_max: int, depth: int,
+            timed: bool, max_stops: int = 1 << 16) -> tuple[_abi.RunStats, np.ndarray | None, np.ndarray]:
+        """The whole checkpoint loop natively (dic_engine_run)."""
+        out = _abi.RunStats()
+        count_ms = np.zeros(max_stops, dtype=np.float32) if timed else None
+        dashed = np.zeros(max_stops, dtype=np.int64)
+        _abi.call("dic_engine_run", self.h, lfirst.ctypes.data, llast.ctypes.data, rows.ctypes.data, stop_max, depth,
+                  C.byref(out), count_ms.ctypes.data if timed else None, dashed.ctypes.data, max_stops)
+        k = min(out.stops, max_stops)
+        return out, (count_ms[:k] if timed else None), dashed[:k]
+
     def frequent(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         F = C.c_int64()
         _abi.call("dic_engine_num_frequent", self.h, C.byref(F))
@@ -159,6 +170,29 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
         stats.candidates_generated = npairs
         stats.peak_dashed = npairs
         scanned = params.n
+        if engine_factory is None and not sharded:
+            # the whole loop natively: no Python on the per-stop path
+            nst = params.intervals_per_pass
+            bounds = [params.chunk_bounds(s) for s in range(1, nst + 1)]
+            lf = np.array([b[0] for b in bounds], dtype=np.int64)
+            ll = np.array([b[1] for b in bounds], dtype=np.int64)
+            rows = ll - lf + 1
+            out, cms, dashed = eng.run(lf, ll, rows, nst, depth, count_events is not None)
+            stats.interval_counts += out.interval_counts
+            stats.candidates_pruned += out.candidates_pruned
+            stats.candidates_generated += out.candidates_generated
+            stats.peak_dashed = max(stats.peak_dashed, out.peak_dashed)
+            scanned += out.scanned
+            for i in range(len(dashed)):
+                stop_no = i % nst + 1
+                if trace is not None:
+                    trace.stops.append({"stop": stop_no, "dashed_at_start": int(dashed[i])})
+                if count_events is not None:
+                    count_events.append(("native", float(cms[i]), int(dashed[i]) * (-(-int(rows[stop_no - 1]) // 32)),
+                                         int(rows[stop_no - 1])))
+            frequent = sorted_frequent(*eng.frequent())
+            eng.close()
+            eng = None
         # Pipelined checkpoint loop: stops are enqueued up to `depth` ahead
         # and their statuses consumed in order (the reference's loop test
         # `while catalog.dashed` is evaluated on the polled status; stops
@@ -166,7 +200,7 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
         inflight: deque = deque()
         stop = 0
         live = npairs
-        done = live == 0
+        done = live == 0 or eng is None
         while True:
             while not done and len(inflight) < depth:
                 stop = stop + 1 if stop < params.intervals_per_pass else 1
@@ -213,9 +247,11 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
                 stop = s_stop
             if live == 0:
                 done = True
-        frequent = sorted_frequent(*eng.frequent())
+        if eng is not None:
+            frequent = sorted_frequent(*eng.frequent())
     finally:
-        eng.close()
+        if eng is not None:
+            eng.close()
     if torch.cuda.is_available():
         torch.cuda.synchronize()
     stats.db_passes = scanned / params.n
