@@ -202,7 +202,9 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
     const int sub = threadIdx.x & 7, slot = threadIdx.x >> 3;
-    const int64_t cbase = blk * (int64_t)kRLSlots * R;
+    // a thread owns R CONSECUTIVE candidates: in a sorted bucket they mostly
+    // share their first item, whose chunk is then loaded once per tile
+    const int64_t cbase = blk * (int64_t)kRLSlots * R + (int64_t)slot * R;
     if (threadIdx.x == 0) {
         fence_proxy_async();
         issue_tile(smem, tids, tb, t0, 0);
@@ -212,7 +214,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     uint32_t cnt[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int64_t c = cbase + (int64_t)r * kRLSlots + slot;
+        const int64_t c = cbase + r;
         const int64_t cc = c < C ? c : C - 1;
         cnt[r] = 0;
 #pragma unroll
@@ -242,9 +244,16 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int j = 0; j < KP; ++j) asm volatile("" : "+r"(it[r][j]));
+        uint32_t prev0 = 0xFFFFFFFFu;
+        uint4 v0 = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            uint4 v = *reinterpret_cast<const uint4*>(bs + (it[r][0] & 0xFFFFu) * RB);
+            const uint32_t i0 = it[r][0] & 0xFFFFu;
+            if (i0 != prev0) {
+                v0 = *reinterpret_cast<const uint4*>(bs + i0 * RB);
+                prev0 = i0;
+            }
+            uint4 v = v0;
 #pragma unroll
             for (int j = 1; j < K; ++j) {
                 const uint32_t item = (j & 1) ? (it[r][j >> 1] >> 16) : (it[r][j >> 1] & 0xFFFFu);
@@ -264,7 +273,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         x += __shfl_xor_sync(0xFFFFFFFFu, x, 1);
         x += __shfl_xor_sync(0xFFFFFFFFu, x, 2);
         x += __shfl_xor_sync(0xFFFFFFFFu, x, 4);
-        const int64_t c = cbase + (int64_t)r * kRLSlots + slot;
+        const int64_t c = cbase + r;
         if (sub == 0 && c < C && x) atomicAdd(out + c, (unsigned long long)x);
     }
 }
