@@ -50,6 +50,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-bench", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=500, help="nvidia-smi sampling period in the timed region")
     ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
     return ap.parse_args()
 
@@ -62,8 +63,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_ms: int = 500):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.proc = None
         self.path = None
 
@@ -73,7 +75,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", str(self.period_ms)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -292,7 +294,7 @@ def main() -> None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.dic_launch_count()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(local_rank, args.clock_ms) as clocks:
         e0.record(stream)
         for i in range(args.steps):
             res = one_run(count_events=count_events if i == args.steps - 1 else None)
