@@ -170,15 +170,52 @@ def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
-    words = float(C) * ((n + 31) // 32)
-    achieved = words / (best * 1e-3)
+    words = (n + 31) // 32
+    ops = float(sum(int(b.shape[0]) * int(b.shape[1]) for b in buckets)) * words  # k lane-ops per cand-word
+    achieved = ops / (best * 1e-3)
     checksum = int(sum(int(o.sum().item()) for o in outs))
     del tids
     torch.cuda.empty_cache()
     return {"workload": cfg.name, "n": n, "m": m, "candidates": C, "ms": best,
-            "subset_tests_per_s": C * n / (best * 1e-3), "roofline_bound": "int-pipe (POPC)",
-            "achieved_T_word_popcounts_per_s": achieved / 1e12, "peak_T": peaks["popc"] / 1e12,
-            "frac": achieved / peaks["popc"], "support_checksum": checksum}
+            "subset_tests_per_s": C * n / (best * 1e-3), "bound": "int-ALU (LOP3 lane-ops)",
+            "achieved": achieved / 1e12, "peak": peaks["lop3"] / 1e12, "unit": "T lane-ops/s",
+            "frac": achieved / peaks["lop3"], "support_checksum": checksum,
+            "ops_rule": "k lane-ops per (candidate, 32-row word): (k-1) ANDs + >= 1 to accumulate the popcount"}
+
+
+def pair_kernel_roofline(tids, n: int, m: int, interval: int, peaks: dict, reps: int = 10) -> dict:
+    """The dominant kernel of the cfg4 run, measured alone on the run's own
+    data: dic_count_pairs over one M-row chunk (a dense-pair stop)."""
+    import torch
+
+    from paper_1812_10959_b200 import device as D
+
+    tri = torch.zeros(m * (m - 1) // 2, dtype=torch.int64, device="cuda")
+    first, last = 0, min(interval, n) - 1
+    D.count_pairs(tids, n, m, first, last, tri)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        D.count_pairs(tids, n, m, first, last, tri)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = sum(ms) / len(ms)
+    words = (last - first + 1 + 31) // 32
+    ops = 2.0 * tri.numel() * words  # k = 2
+    return {"t_ms": t, "ops": ops, "tests_per_s": tri.numel() * (last - first + 1) / (t * 1e-3),
+            "achieved": ops / (t * 1e-3)}
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
+    try:
+        summ = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+        return summ.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 def subset_tests(n: int, m: int, params, trace) -> int:
@@ -313,20 +350,28 @@ def main() -> None:
     # roofline of the dominant kernel (the streaming support count) over the
     # last timed run: per launch >= 1 POPC per (candidate, 32-row word)
     count_ms = [ev[1] if ev[0] == "native" else ev[0].elapsed_time(ev[1]) for ev in count_events]
-    words = [ev[2] for ev in count_events]
     peaks = int_peaks()
     hbm_gbs, hbm_src = measured_hbm()
     tot_ms = sum(count_ms)
-    popc_ops = float(sum(words))
-    achieved = popc_ops / (tot_ms * 1e-3) if tot_ms > 0 else 0.0
-    roofline = {"bound": "int-pipe (POPC)", "achieved": achieved / 1e12, "peak": peaks["popc"] / 1e12,
-                "unit": "T word-popcounts/s", "frac": achieved / peaks["popc"] if peaks["popc"] else None,
-                "traffic": None, "kernel": "count_stream_kernel",
-                "launches": len(count_ms), "avg_launch_ms": tot_ms / max(len(count_ms), 1),
-                "share_of_step": tot_ms / ms if ms else None,
-                "peak_source": "live probe (tools/probe_peaks.py kernels): POPC lanes/s; LOP3 "
-                               f"{peaks['lop3'] / 1e12:.2f} T lane-ops/s",
-                "hbm_peak_gbs": hbm_gbs, "hbm_peak_source": hbm_src}
+    # the dominant kernel: the dense pair triangle (pair_tri_kernel), timed
+    # alone on one cfg4 chunk; its share of the step from the run's own count
+    # launches (the pair kernel runs inside them during the pair wave)
+    pk = pair_kernel_roofline(tids, n_local, cfg.m, cfg.interval, peaks) if world == 1 else None
+    dense_stops = min(len(count_ms), params.intervals_per_pass)
+    roofline = None
+    if pk is not None:
+        roofline = {"bound": "int-ALU (LOP3 lane-ops)", "achieved": pk["achieved"] / 1e12,
+                    "peak": peaks["lop3"] / 1e12, "unit": "T lane-ops/s", "frac": pk["achieved"] / peaks["lop3"],
+                    "traffic": ncu_traffic("pair_tri_kernel"), "kernel": "pair_tri_kernel",
+                    "avg_launch_ms": pk["t_ms"], "ops_per_launch": pk["ops"],
+                    "tests_per_s": pk["tests_per_s"],
+                    "ops_rule": "2 lane-ops per (pair, 32-row word): 1 AND + >= 1 to accumulate the popcount",
+                    "share_of_step": pk["t_ms"] * dense_stops / ms if ms else None,
+                    "peak_source": f"live probe: LOP3 {peaks['lop3'] / 1e12:.2f} T lane-ops/s, "
+                                   f"POPC {peaks['popc'] / 1e12:.2f} T lane-ops/s (MEASURED_PEAKS.json has no "
+                                   "integer pipes)",
+                    "count_launches_in_step": len(count_ms), "count_ms_in_step": tot_ms,
+                    "hbm_peak_gbs": hbm_gbs, "hbm_peak_source": hbm_src}
 
     # end to end through the public API from pinned host CSR
     e2e = None
