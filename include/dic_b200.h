@@ -239,7 +239,9 @@ int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_t* llast,
                    dic_run_stats* out, float* count_ms, int64_t* dashed,
                    int64_t max_stops);
 /* Results: number of SOLID_BOX records, then copy them out to HOST arrays
- * masks[F][W] (uint64), sizes[F], supports[F] (unsorted).  Synchronising. */
+ * masks[F][W] (uint64), sizes[F], supports[F] in the reference's canonical
+ * order (engine.py:446-455): by size, then mask as an integer (MSW first).
+ * Synchronising.                                                          */
 int dic_engine_num_frequent(dic_engine* e, int64_t* F);
 int dic_engine_frequent(dic_engine* e, uint64_t* masks_host,
                         int32_t* sizes_host, int64_t* supports_host,

@@ -93,20 +93,16 @@ def masks_to_array(masks: Iterable[int], W: int) -> np.ndarray:
 
 
 def array_to_masks(arr: np.ndarray) -> list[int]:
-    """uint64 [len][W] -> Python ints."""
+    """uint64 [len][W] (LSW first) -> Python ints."""
     a = np.asarray(arr, dtype=np.uint64)
     if a.ndim == 1:
-        return [int(v) for v in a]
+        return a.tolist()
     if a.shape[1] == 1:
-        return [int(v) for v in a[:, 0]]
-    cols = [a[:, w].tolist() for w in range(a.shape[1])]
-    out = []
-    for j in range(a.shape[0]):
-        x = 0
-        for w in range(a.shape[1] - 1, -1, -1):
-            x = (x << WORD) | cols[w][j]
-        out.append(x)
-    return out
+        return a[:, 0].tolist()
+    raw = np.ascontiguousarray(a, dtype="<u8").tobytes()
+    step = a.shape[1] * 8
+    fb = int.from_bytes
+    return [fb(raw[i:i + step], "little") for i in range(0, len(raw), step)]
 
 
 def masks_to_items(masks: list[int], k: int) -> np.ndarray:

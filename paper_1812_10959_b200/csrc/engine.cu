@@ -39,7 +39,9 @@
 // engine omits it; the API-level prune on host catalogs keeps it.
 #include "common.cuh"
 
+#include <algorithm>
 #include <deque>
+#include <numeric>
 #include <vector>
 
 namespace dic {
@@ -1256,5 +1258,29 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
     }
     dfree(ids, e->s); dfree(dm, e->s); dfree(dsz, e->s); dfree(dsu, e->s);
     DIC_CUDA(cudaStreamSynchronize(e->s));
+    // canonical order of the reference's result (engine.py:446-455): by size,
+    // then by the mask as an integer, i.e. most significant word first
+    const int W = e->W;
+    std::vector<int64_t> idx(F);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+        if (sizes_host[a] != sizes_host[b]) return sizes_host[a] < sizes_host[b];
+        for (int w = W - 1; w >= 0; --w) {
+            const uint64_t x = masks_host[a * W + w], y = masks_host[b * W + w];
+            if (x != y) return x < y;
+        }
+        return false;
+    });
+    std::vector<uint64_t> m2((size_t)F * W);
+    std::vector<int32_t> s2(F);
+    std::vector<int64_t> p2(F);
+    for (int64_t i = 0; i < F; ++i) {
+        std::copy(masks_host + idx[i] * W, masks_host + idx[i] * W + W, m2.begin() + i * W);
+        s2[i] = sizes_host[idx[i]];
+        p2[i] = supports_host[idx[i]];
+    }
+    std::copy(m2.begin(), m2.end(), masks_host);
+    std::copy(s2.begin(), s2.end(), sizes_host);
+    std::copy(p2.begin(), p2.end(), supports_host);
     return DIC_OK;
 }

@@ -44,6 +44,8 @@ class StopTrace:
 class DeviceEngine:
     """RAII handle over dic_engine (one per rank)."""
 
+    presorted = True  # dic_engine_frequent returns the canonical (size, mask) order
+
     def __init__(self, tids, n_local: int, m: int, params: MiningParams, prune_bound: bool):
         import torch
 
@@ -133,12 +135,19 @@ class DeviceEngine:
         return masks[: F.value], sizes[: F.value], sups[: F.value]
 
 
-def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray) -> tuple[FrequentItemset, ...]:
-    """Canonical (size, mask) order with masks compared as Python ints (MSW first)."""
+def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray,
+                    presorted: bool = False) -> tuple[FrequentItemset, ...]:
+    """Canonical (size, mask) order (engine.py:446-455) with masks compared as
+    Python ints, i.e. most significant word first (dic_engine_frequent
+    already returns that order: presorted)."""
+    if len(sizes) == 0:
+        return ()
+    if not presorted:
+        W = masks.shape[1]
+        order = np.lexsort(tuple(masks[:, w] for w in range(W)) + (sizes,))
+        masks, sizes, sups = masks[order], sizes[order], sups[order]
     ints = bits.array_to_masks(masks)
-    items = [FrequentItemset(mk, int(sz), int(sp)) for mk, sz, sp in zip(ints, sizes.tolist(), sups.tolist())]
-    items.sort(key=lambda f: (f.size, f.mask))
-    return tuple(items)
+    return tuple(map(FrequentItemset, ints, sizes.tolist(), sups.tolist()))
 
 
 def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound: bool = True,
@@ -190,7 +199,7 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
                 if count_events is not None:
                     count_events.append(("native", float(cms[i]), int(dashed[i]) * (-(-int(rows[stop_no - 1]) // 32)),
                                          int(rows[stop_no - 1])))
-            frequent = sorted_frequent(*eng.frequent())
+            frequent = sorted_frequent(*eng.frequent(), presorted=getattr(eng, "presorted", False))
             eng.close()
             eng = None
         # Pipelined checkpoint loop: stops are enqueued up to `depth` ahead
@@ -248,7 +257,7 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
             if live == 0:
                 done = True
         if eng is not None:
-            frequent = sorted_frequent(*eng.frequent())
+            frequent = sorted_frequent(*eng.frequent(), presorted=getattr(eng, "presorted", False))
     finally:
         if eng is not None:
             eng.close()
