@@ -332,11 +332,15 @@ def main() -> None:
     torch.cuda.synchronize()
     launches0 = lib.dic_launch_count()
     with ClockSampler(local_rank, args.clock_ms) as clocks:
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         e0.record(stream)
+        step_ev[0].record(stream)
         for i in range(args.steps):
             res = one_run(count_events=count_events if i == args.steps - 1 else None)
+            step_ev[i + 1].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     if world > 1:
         dist.barrier()
     launches = (lib.dic_launch_count() - launches0) // args.steps
@@ -426,6 +430,7 @@ def main() -> None:
                        "frequent_itemsets": len(ref.frequent), "stops": len(trace.stops),
                        "db_passes": s.db_passes, "candidates_generated": s.candidates_generated,
                        "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
+            "step_ms": [round(x, 3) for x in step_ms], "host_loop": trace.native,
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
             "cpu_baseline": cpu, "kernel_microbench": kernel,
         }

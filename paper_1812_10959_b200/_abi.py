@@ -39,6 +39,9 @@ class RunStats(C.Structure):
         ("candidates_generated", i64),
         ("candidates_pruned", i64),
         ("peak_dashed", i64),
+        ("replays", i64),
+        ("issue_us", dbl),
+        ("poll_us", dbl),
     ]
 
 

@@ -40,6 +40,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <deque>
 #include <numeric>
 #include <vector>
@@ -1160,7 +1161,12 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     int rc = DIC_OK;
     int64_t stop = 0;
     bool done = e->live == 0;
+    using clk = std::chrono::steady_clock;
+    auto us_since = [](clk::time_point t) {
+        return std::chrono::duration<double, std::micro>(clk::now() - t).count();
+    };
     while (rc == DIC_OK) {
+        const clk::time_point ti = clk::now();
         while (!done && (int64_t)inflight.size() < depth) {
             stop = stop < stop_max ? stop + 1 : 1;
             const int slot = (int)(e->issued % kRing);
@@ -1171,12 +1177,16 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
             if ((rc = dic_engine_issue_checkpoint(e, &seq))) break;
             inflight.push_back({seq, stop});
         }
+        out->issue_us += us_since(ti);
         if (rc || inflight.empty()) break;
         const Flight f = inflight.front();
         inflight.pop_front();
         dic_stop_status st;
         int32_t replayed = 0;
+        const clk::time_point tp = clk::now();
         if ((rc = dic_engine_poll(e, f.seq, &st, &replayed))) break;
+        out->poll_us += us_since(tp);
+        out->replays += replayed;
         if (done) continue;  // a no-op stop issued after the last live one
         const int64_t i = out->stops;
         if (i < max_stops) {

@@ -39,6 +39,7 @@ class StopTrace:
     """Per-stop engine status (for tests and the bench's accounting)."""
 
     stops: list[dict] = field(default_factory=list)
+    native: dict | None = None  # host-side diagnostics of the native loop
 
 
 class DeviceEngine:
@@ -187,6 +188,9 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
             ll = np.array([b[1] for b in bounds], dtype=np.int64)
             rows = ll - lf + 1
             out, cms, dashed = eng.run(lf, ll, rows, nst, depth, count_events is not None)
+            if trace is not None:
+                trace.native = {"stops": out.stops, "replays": out.replays, "issue_ms": out.issue_us / 1e3,
+                                "poll_ms": out.poll_us / 1e3}
             stats.interval_counts += out.interval_counts
             stats.candidates_pruned += out.candidates_pruned
             stats.candidates_generated += out.candidates_generated
