@@ -154,7 +154,7 @@ def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray,
 def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound: bool = True,
                plan: ShardPlan | None = None, group=None, trace: StopTrace | None = None,
                t0: float | None = None, count_events: list | None = None,
-               engine_factory=None, depth: int = 4) -> MiningResult:
+               engine_factory=None, depth: int = 4, collective: bool | None = None) -> MiningResult:
     """The checkpoint loop of _run over one rank's local rows.
 
     ``plan``/``group``: chunk-sliced sharding (sharding.py) with a
@@ -168,7 +168,9 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
     import torch.distributed as dist
 
     t0 = time.perf_counter() if t0 is None else t0
-    sharded = plan is not None and plan.world > 1
+    # per-stop collectives: whenever sharded (collective=True forces the
+    # collective loop even for one rank, e.g. to test the NCCL path on one GPU)
+    sharded = (plan is not None and plan.world > 1) if collective is None else collective
     local_chunks = plan.local_chunks() if plan is not None else None
     eng = (engine_factory or DeviceEngine)(tids, n_local, m, params, prune_bound)
     try:
