@@ -9,7 +9,6 @@ from __future__ import annotations
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -53,4 +52,3 @@ def test_collective_loop_matches_oracle(nccl_group, idx, n, interval):
     # and the native single-GPU loop agrees with it
     res2 = run_engine(db.device_tids(), cfg.n, cfg.m, params)
     assert [(f.mask, f.support) for f in res2.frequent] == [(f.mask, f.support) for f in res.frequent]
-    del np
