@@ -213,6 +213,17 @@ int dic_engine_checkpoint(dic_engine* e, dic_stop_status* st);
  * must re-issue every stop after seq.  At most 15 stops in flight.
  * dic_engine_delta's length is the (rank-independent) slot capacity.      */
 int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t llast);
+/* Declare the chunk cycle of the coming stops: the next issued stop counts
+ * local rows [lfirst[0], llast[0]], the one after [lfirst[1], llast[1]], ...
+ * wrapping after nstops.  A dic_engine_issue_count() whose chunk matches the
+ * schedule launches the stop's count as one captured CUDA graph (the chunk is
+ * read on the device); any other chunk takes the direct launch path.  The
+ * checkpoint half is always a graph.  graphs_captured / graph_launches are
+ * diagnostics (dic_engine_graph_stats).                                   */
+int dic_engine_set_schedule(dic_engine* e, const int64_t* lfirst,
+                            const int64_t* llast, int64_t nstops);
+int dic_engine_graph_stats(dic_engine* e, int64_t* graphs_captured,
+                           int64_t* graph_launches);
 /* The dense pair-triangle counts of the stop (device uint64/int64 [*len],
  * *len == 0 when the engine has none): sharded callers sum-allreduce it
  * together with dic_engine_delta() before the checkpoint.                 */

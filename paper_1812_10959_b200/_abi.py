@@ -69,6 +69,8 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_delta": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_checkpoint": (C.c_int, [vp, P(StopStatus)]),
     "dic_engine_issue_count": (C.c_int, [vp, i64, i64]),
+    "dic_engine_set_schedule": (C.c_int, [vp, vp, vp, i64]),
+    "dic_engine_graph_stats": (C.c_int, [vp, P(i64), P(i64)]),
     "dic_engine_pair_counts": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_issue_checkpoint": (C.c_int, [vp, P(i64)]),
     "dic_engine_poll": (C.c_int, [vp, i64, P(StopStatus), P(i32)]),

@@ -11,6 +11,7 @@ static thread_local char g_err[512] = "";
 static unsigned long long g_launches = 0;
 
 void note_launch() { __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED); }
+void note_launches(long long n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
 void set_error(const char* fmt, ...) {
     va_list ap;

@@ -28,6 +28,8 @@ int sm_count();
 void retain_pool();
 // Count of kernels this library launched (dic_launch_count()).
 void note_launch();
+// Adjust that count by n (graphs: kernels captured are noted per graph launch).
+void note_launches(long long n);
 
 #define DIC_CHECK_LAUNCH(what)                                   \
     do {                                                         \

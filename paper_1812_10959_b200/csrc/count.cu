@@ -369,13 +369,38 @@ struct DevCountArgs {
     unsigned long long* delta;
     const unsigned long long* abort;  // non-zero: stop skipped (overflow recovery)
     int64_t tri_len;                  // > 0: bucket 2 counted densely when 2*bn[2] >= tri_len
+    // engine graphs: the stop's local chunk [first, last] is read from
+    // chunk_ring[2 * (*seq % ring)] at run time (geom/t_first/t_last unused)
+    const int64_t* chunk_ring;
+    const unsigned long long* seq;
+    int32_t ring;
 };
+
+// The chunk geometry of this launch (host-given, or read from the ring).
+__device__ __forceinline__ bool dev_chunk(const DevCountArgs& a, ChunkGeom& geom, int64_t& t_first,
+                                          int64_t& t_last) {
+    geom = a.geom;
+    t_first = a.t_first;
+    t_last = a.t_last;
+    if (a.chunk_ring) {
+        const int64_t sl = (int64_t)(*a.seq % (unsigned long long)a.ring);
+        const int64_t f = a.chunk_ring[2 * sl], l = a.chunk_ring[2 * sl + 1];
+        if (l < f) return false;
+        geom = chunk_geom(f, l);
+        t_first = geom.g_first / a.TW;
+        t_last = geom.g_last / a.TW;
+    }
+    return true;
+}
 
 template <int TW>
 __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __grid_constant__ DevCountArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int64_t pref[kDevMaxK + 1];
     if (*a.abort) return;
+    ChunkGeom geom;
+    int64_t t_first, t_last;
+    if (!dev_chunk(a, geom, t_first, t_last)) return;
     if (threadIdx.x == 0) {
         const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
         int64_t acc = 0;
@@ -392,7 +417,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __gr
     __syncthreads();
     const int64_t B = pref[a.kuse];
     if (B == 0) return;
-    const int64_t nt = a.t_last - a.t_first + 1;
+    const int64_t nt = t_last - t_first + 1;
     const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)gridDim.x / B));
     const int64_t U = B * rs;
     if ((int64_t)blockIdx.x >= U) return;
@@ -402,9 +427,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __gr
         const int64_t gb = u / rs, r = u - gb * rs;
         int k = 1;
         while (pref[k + 1] <= gb) ++k;
-        const int64_t t0 = a.t_first + nt * r / rs, t1 = a.t_first + nt * (r + 1) / rs;
+        const int64_t t0 = t_first + nt * r / rs, t1 = t_first + nt * (r + 1) / rs;
         if (t0 < t1)
-            dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, a.geom, a.items_tab[k], (int64_t)a.bn[k],
+            dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
                               a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
         __syncthreads();
     }
@@ -444,9 +469,12 @@ __global__ void __launch_bounds__(256) count_global_kernel(const uint32_t* __res
 // itemset sizes): grid-stride over (bucket, candidate, tile) with plain loads.
 __global__ void __launch_bounds__(256) count_dev_global_kernel(const __grid_constant__ DevCountArgs a) {
     if (*a.abort) return;
+    ChunkGeom geom;
+    int64_t t_first, t_last;
+    if (!dev_chunk(a, geom, t_first, t_last)) return;
     const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
     const int TW = a.TW, RW = row_words(TW);
-    const int64_t nt = a.t_last - a.t_first + 1;
+    const int64_t nt = t_last - t_first + 1;
     const int64_t tw_words = (int64_t)a.m * RW;
     for (int k = 1; k < a.kuse; ++k) {
         const int64_t C = (k == 2 && dense) ? 0 : (int64_t)a.bn[k];
@@ -454,13 +482,13 @@ __global__ void __launch_bounds__(256) count_dev_global_kernel(const __grid_cons
         unsigned long long* out = a.delta + a.doff[k];
         for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < C * nt;
              w += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t c = w / nt, t = a.t_first + (w - c * nt);
+            const int64_t c = w / nt, t = t_first + (w - c * nt);
             uint32_t cnt = 0;
             for (int q = 0; q < TW / 4; ++q) {
                 const int64_t g = t * TW + q * 4;
-                if (g > a.geom.g_last || g + 3 < a.geom.g_first) continue;
-                uint4 v = make_uint4(group_mask(a.geom, g), group_mask(a.geom, g + 1), group_mask(a.geom, g + 2),
-                                     group_mask(a.geom, g + 3));
+                if (g > geom.g_last || g + 3 < geom.g_first) continue;
+                uint4 v = make_uint4(group_mask(geom, g), group_mask(geom, g + 1), group_mask(geom, g + 2),
+                                     group_mask(geom, g + 3));
                 for (int j = 0; j < k; ++j) {
                     const uint32_t item = __ldg(items + c * k + j);
                     const uint4* row = reinterpret_cast<const uint4*>(a.tids + t * tw_words + (int64_t)item * RW);
@@ -571,8 +599,9 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
 int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
                      uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
                      unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
-                     cudaStream_t s) {
-    if (last < first) return DIC_OK;
+                     cudaStream_t s, const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
+                     int ring = 0) {
+    if (!chunk_ring && last < first) return DIC_OK;
     DevCountArgs a;
     memset(&a, 0, sizeof(a));
     a.tids = tids;
@@ -589,6 +618,9 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
     a.delta = delta;
     a.abort = abort_flag;
     a.tri_len = tri_len;
+    a.chunk_ring = chunk_ring;
+    a.seq = seq;
+    a.ring = ring;
     const size_t smem = 128 + 2 * (size_t)a.tile_bytes;
     // the kernel's static shared memory (the unit prefix table) shares the budget
     static size_t static_smem = 0;

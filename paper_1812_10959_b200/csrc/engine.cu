@@ -50,12 +50,13 @@ namespace dic {
 int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
                      uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
                      unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
-                     cudaStream_t s);
+                     cudaStream_t s, const int64_t* chunk_ring, const unsigned long long* seq, int ring);
 int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s);
 int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                            unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
-                           const unsigned long long* abort_flag, cudaStream_t s);
+                           const unsigned long long* abort_flag, cudaStream_t s, const int64_t* chunk_ring,
+                           const unsigned long long* seq, int ring);
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
                        cudaStream_t s);
 
@@ -84,11 +85,15 @@ enum : int {
     S_ABORT = 8,     // persistent: set with OVERFLOW, cleared by the host's replay
     S_SCRATCH = 9,   // scratch word (result collection)
     S_DONE = 10,     // eval blocks finished (last one runs the capacity check)
+    S_SEQ = 11,      // persistent: stops completed (the status kernel advances it)
     S_HEAD = 12
 };
 constexpr int kDoffMax = 256;  // delta offsets kept for sizes < 256
-// followed by: removed[KS] (slots not kept this stop), adm[KS] (admitted
-// joins by size), bn[KS] (bucket fill, persistent), KS = m + 2.
+constexpr int kRing = 16;      // status ring slots (> max stops in flight)
+// followed by: removed[KS] (dead slots this stop), adm[KS] (admitted joins by
+// size), bn[KS] (bucket fill, persistent), cflag[KS] (compact bucket k at the
+// next stop), KS = m + 2.  The first S_HEAD + 3*KS words are the status
+// snapshot copied to the host ring.
 
 struct Records {
     unsigned long long* mask = nullptr;  // [cap][W]
@@ -282,48 +287,70 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
     }
 }
 
-// Order-preserving compaction of bucket k by one CTA (rare: scheduled by the
-// host when a bucket holds many dead slots): scan of the keep flags, scatter
-// to scratch, copy back, bn[k] = kept.
+// Order-preserving in-place compaction (compact_dashed, itemsets.py:130-132)
+// of every bucket the previous status flagged, one CTA per bucket: chunks of
+// E slots are scanned (keep flags of this stop's apply), staged in shared
+// memory and written back to their compacted positions, which never pass the
+// chunk being read.  bn[k] = kept, removed[k] = cflag[k] = 0.
 constexpr int kCompactThreads = 1024;
-__global__ void __launch_bounds__(kCompactThreads) compact_bucket_kernel(
-    int k, int32_t* const* __restrict__ rec_tab, uint16_t* const* __restrict__ items_tab,
-    const int64_t* __restrict__ doff, const int32_t* __restrict__ keep_all, int32_t* __restrict__ rec_s,
-    uint16_t* __restrict__ items_s, unsigned long long* stat, int KS) {
-    if (stat[S_ABORT]) return;
-    __shared__ int64_t part[kCompactThreads];
-    const int64_t n = (int64_t)stat[S_HEAD + 2 * KS + k];
+constexpr int kCompactItems = 16384;  // staged item ids per chunk (32 KB)
+__global__ void __launch_bounds__(kCompactThreads) compact_flagged_kernel(
+    int32_t* const* __restrict__ rec_tab, uint16_t* const* __restrict__ items_tab,
+    const int64_t* __restrict__ doff, const int32_t* __restrict__ keep_all, unsigned long long* stat, int KS) {
+    const int k = blockIdx.x;
+    unsigned long long* cflag = stat + S_HEAD + 3 * KS;
+    if (stat[S_ABORT] || !cflag[k]) return;
+    __shared__ uint16_t sitems[kCompactItems];
+    __shared__ int32_t spos[kCompactThreads];
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t ctotal;
+    unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    const int64_t n = (int64_t)bn[k];
     const int32_t* keep = keep_all + doff[k];
     int32_t* rec = rec_tab[k];
     uint16_t* items = items_tab[k];
-    const int64_t per = (n + kCompactThreads - 1) / kCompactThreads;
-    const int64_t lo = min(n, per * threadIdx.x), hi = min(n, lo + per);
-    int64_t cnt = 0;
-    for (int64_t c = lo; c < hi; ++c) cnt += keep[c];
-    part[threadIdx.x] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        for (int i = 0; i < kCompactThreads; ++i) {
-            const int64_t v = part[i];
-            part[i] = acc;
-            acc += v;
+    const int E = min(kCompactThreads, kCompactItems / k);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t out = 0;
+    for (int64_t base = 0; base < n; base += E) {
+        const int cnt = (int)min((int64_t)E, n - base);
+        const int e = threadIdx.x;
+        const bool valid = e < cnt;
+        const int kp = valid ? keep[base + e] : 0;
+        const int32_t r = valid ? rec[base + e] : 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, kp);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        for (int j = threadIdx.x; j < cnt * k; j += kCompactThreads) sitems[j] = items[base * k + j];
+        __syncthreads();
+        if (wid == 0) {
+            const int v = wsum[lane];
+            int x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            wsum[lane] = x - v;  // exclusive
+            if (lane == 31) ctotal = x;
         }
-        stat[S_HEAD + 2 * KS + k] = (unsigned long long)acc;
+        __syncthreads();
+        const int pos = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+        spos[e] = kp ? pos : -1;
+        const int total = ctotal;
+        __syncthreads();
+        if (kp) rec[out + pos] = r;
+        for (int j = threadIdx.x; j < cnt * k; j += kCompactThreads) {
+            const int c = j / k;
+            const int p = spos[c];
+            if (p >= 0) items[(out + p) * k + (j - c * k)] = sitems[j];
+        }
+        __syncthreads();
+        out += total;
     }
-    __syncthreads();
-    int64_t d = part[threadIdx.x];
-    for (int64_t c = lo; c < hi; ++c) {
-        if (!keep[c]) continue;
-        rec_s[d] = rec[c];
-        for (int j = 0; j < k; ++j) items_s[d * k + j] = items[c * k + j];
-        ++d;
-    }
-    __syncthreads();
-    const int64_t kept = (int64_t)stat[S_HEAD + 2 * KS + k];
-    for (int64_t c = threadIdx.x; c < kept; c += kCompactThreads) {
-        rec[c] = rec_s[c];
-        for (int j = 0; j < k; ++j) items[c * k + j] = items_s[c * k + j];
+    if (threadIdx.x == 0) {
+        bn[k] = (unsigned long long)out;
+        stat[S_HEAD + k] = 0;  // removed: none left
+        cflag[k] = 0;
     }
 }
 
@@ -478,14 +505,17 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
     }
 }
 
-// The stop's status into its (host-mapped, pinned) ring slot: head words,
-// then removed[k], adm[k], bn[k] for k < kuse.
-// Then (unless the stop overflowed: the replay needs its counters) reset the
-// per-stop counters and compute the next stop's delta offsets from the
-// bucket fill.  slot == nullptr: reset only (engine seeding).
+// The stop's status into its (host-mapped, pinned) ring slot S_SEQ % kRing:
+// head words, then removed[k], adm[k], bn[k] for k < kuse.  Then, unless the
+// stop overflowed (the replay needs its counters; later stops are no-ops and
+// rewrite the same slot), advance S_SEQ, flag the buckets to compact at the
+// next stop (dead slots >= a quarter), reset the per-stop counters and
+// compute the next stop's delta offsets from the bucket fill.
+// ring == nullptr: reset only (engine seeding).
 __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int kuse,
-                              unsigned long long* __restrict__ slot, int64_t* __restrict__ doff) {
-    if (slot) {
+                              unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
+    if (ring) {
+        unsigned long long* slot = ring + (int64_t)(stat[S_SEQ] % kRing) * ring_words;
         for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
         for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
             slot[S_HEAD + 3 * k] = stat[S_HEAD + k];
@@ -495,8 +525,11 @@ __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int
     }
     __syncthreads();
     if (stat[S_ABORT]) return;
+    if (ring && threadIdx.x == 0) stat[S_SEQ] += 1;
     for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
     for (int k = threadIdx.x; k < KS && k < kDoffMax; k += blockDim.x) {
+        const unsigned long long rem = stat[S_HEAD + k], fill = stat[S_HEAD + 2 * KS + k];
+        stat[S_HEAD + 3 * KS + k] = (rem > 0 && (rem * 4 >= fill || rem == fill)) ? 1ull : 0ull;  // cflag
         stat[S_HEAD + k] = 0;       // removed
         stat[S_HEAD + KS + k] = 0;  // adm
     }
@@ -544,10 +577,25 @@ struct Bucket {
     uint16_t* items = nullptr;
     int64_t n = 0;     // filled slots (live + dead) at the last polled stop
     int64_t cap = 0;
-    int64_t dead = 0;  // slots known dead at the last polled stop
 };
 
-constexpr int kRing = 16;  // status slots (> max stops in flight)
+// Everything a captured stop graph bakes in: a change forces a re-capture.
+struct GraphKey {
+    Records R;
+    const int32_t* ht;
+    int64_t hcap;
+    int64_t kuse;
+    const unsigned long long* delta;
+    const int32_t* keep;
+    const int32_t* frontier;
+    const unsigned long long* tmp_mask;
+    int64_t tmp_cap;
+    int64_t kuse_status;
+    const int64_t* sched;
+    int64_t nsched;
+    int64_t sched_first, sched_last;  // chunk sizing the pair kernel's grid
+    bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
+};
 
 struct dic_engine {
     const uint32_t* tids;
@@ -576,10 +624,6 @@ struct dic_engine {
     int32_t* frontier = nullptr;
     int32_t* keep = nullptr;
     unsigned long long* delta = nullptr;
-    int32_t* scr_rec = nullptr;
-    uint16_t* scr_items = nullptr;
-    int64_t scr_rec_cap = 0, scr_items_cap = 0;
-    std::vector<char> compact_next;  // host decision: compact bucket k in the next issued stop
 
     unsigned long long* tmp_mask = nullptr;
     uint64_t* tmp_hash = nullptr;
@@ -607,6 +651,18 @@ struct dic_engine {
     int kuse_issue = 4;                  // kuse of the stop between issue_count and issue_checkpoint
     bool seeded = false;
     bool counted = false;                // issue_count done, issue_checkpoint pending
+
+    // stop graphs: count half (pair + count kernels, chunk read on the device
+    // from the schedule slot S_SEQ % nsched) and checkpoint half
+    int64_t* d_sched = nullptr;          // [nsched][2] local chunk per stop, rotated so slot = seq % nsched
+    std::vector<int64_t> h_sched;
+    int64_t nsched = 0;
+    cudaStream_t cap_stream = nullptr;   // private stream to capture on
+    cudaGraphExec_t gx_count = nullptr, gx_ckpt = nullptr;
+    long long nk_count = 0, nk_ckpt = 0; // kernels per graph launch
+    GraphKey key_count{}, key_ckpt{};
+    int64_t graphs_captured = 0, graph_launches = 0;
+    bool count_graphed = false;          // the pending count went through the graph
 };
 
 namespace {
@@ -766,29 +822,131 @@ int ensure_headroom(dic_engine* e) {
     return DIC_OK;
 }
 
-int candidate_step(dic_engine* e) {
+int candidate_step(dic_engine* e, cudaStream_t s) {
     const int G = sm_count() * 4;
     unsigned long long* st = e->d_stat;
-    eval_candidates_kernel<<<G, 256, 0, e->s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
+    eval_candidates_kernel<<<G, 256, 0, s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
                                                  (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
                                                  e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap);
     ::dic::note_launch();
-    insert_commit_kernel<<<G, 256, 0, e->s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht,
+    insert_commit_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht,
                                                (uint64_t)e->hcap - 1, st, e->KS, e->d_brec, e->d_bitems);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("candidate_step");
     return DIC_OK;
 }
 
-// status of the stop into ring slot `slot` (one kernel writing host-mapped
-// pinned memory), then an event
-int copy_status(dic_engine* e, int slot) {
-    status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev + (int64_t)slot * e->ring_words,
-                                            e->d_doff);
+// status of the stop into its ring slot (one kernel writing host-mapped
+// pinned memory; the slot is S_SEQ % kRing on the device)
+int launch_status(dic_engine* e, cudaStream_t s) {
+    status_kernel<<<1, kDoffMax, 0, s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev, e->ring_words, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
-    e->kuse_at[slot] = e->kuse;
-    DIC_CUDA(cudaEventRecord(e->ev[slot], e->s));
+    return DIC_OK;
+}
+
+// the checkpoint half of a stop: apply + prune + finalize over every slot,
+// compaction of the flagged buckets, make_candidates (device-sized,
+// all-or-nothing), status
+int launch_checkpoint(dic_engine* e, cudaStream_t s) {
+    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0};
+    apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, s>>>(
+        e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
+        e->keep, e->d_stat, pa, e->KS);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
+    compact_flagged_kernel<<<(unsigned)std::min(e->kuse_issue, e->KS), kCompactThreads, 0, s>>>(
+        e->d_brec, e->d_bitems, e->d_doff, e->keep, e->d_stat, e->KS);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("compact_flagged_kernel");
+    int rc;
+    if ((rc = candidate_step(e, s))) return rc;
+    return launch_status(e, s);
+}
+
+// the count half: the pair triangle and every dashed bucket over the chunk
+// [lfirst, llast]; sched != nullptr: the chunk is read on the device from the
+// schedule slot S_SEQ % nsched ([lfirst, llast] then only sizes the grid)
+int launch_count(dic_engine* e, int64_t lfirst, int64_t llast, const int64_t* sched, cudaStream_t s) {
+    const unsigned long long* abort_flag = e->d_stat + S_ABORT;
+    const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
+    const unsigned long long* seq = e->d_stat + S_SEQ;
+    const int ring = (int)e->nsched;
+    int rc;
+    if (e->tri) {
+        if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
+                                         e->tri_len, abort_flag, s, sched, seq, ring)))
+            return rc;
+    }
+    return count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse_issue, e->d_bitems, bn, e->d_doff,
+                            e->delta, abort_flag, e->tri ? e->tri_len : 0, s, sched, seq, ring);
+}
+
+GraphKey graph_key(const dic_engine* e, bool with_sched) {
+    GraphKey k;
+    memset(&k, 0, sizeof(k));
+    k.R = e->R;
+    k.ht = e->ht;
+    k.hcap = e->hcap;
+    k.kuse = e->kuse_issue;
+    k.delta = e->delta;
+    k.keep = e->keep;
+    k.frontier = e->frontier;
+    k.tmp_mask = e->tmp_mask;
+    k.tmp_cap = e->tmp_cap;
+    k.kuse_status = e->kuse;
+    if (with_sched) {
+        k.sched = e->d_sched;
+        k.nsched = e->nsched;
+        // the chunk with the most tiles sizes the pair kernel's grid
+        int64_t best = -1;
+        for (int64_t i = 0; i < e->nsched; ++i) {
+            const int64_t f = e->h_sched[2 * i], l = e->h_sched[2 * i + 1];
+            if (l < f) continue;
+            const int64_t nt = (l >> 5) - (f >> 5);
+            if (nt > best) {
+                best = nt;
+                k.sched_first = f;
+                k.sched_last = l;
+            }
+        }
+        if (best < 0) k.sched_last = -1;
+    }
+    return k;
+}
+
+// Capture `body` on the private stream into *gx (replacing it); the kernels it
+// noted are re-noted per graph launch instead.
+template <class F>
+int capture_graph(dic_engine* e, cudaGraphExec_t* gx, long long* nk, F body) {
+    const long long before = (long long)dic_launch_count();
+    DIC_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeRelaxed));
+    const int rc = body(e->cap_stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+    const long long n = (long long)dic_launch_count() - before;
+    ::dic::note_launches(-n);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    if (*gx) {
+        cudaGraphExecDestroy(*gx);
+        *gx = nullptr;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(gx, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
+    *nk = n;
+    ++e->graphs_captured;
+    return DIC_OK;
+}
+
+int launch_graph(dic_engine* e, cudaGraphExec_t gx, long long nk) {
+    DIC_CUDA(cudaGraphLaunch(gx, e->s));
+    ::dic::note_launches(nk);
+    ++e->graph_launches;
     return DIC_OK;
 }
 
@@ -814,13 +972,12 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->bound = prune_bound ? 1 : 0;
     e->s = as_stream(stream);
     e->buckets.resize(e->KS);
-    e->compact_next.assign(e->KS, 0);
     const int KS = e->KS;
     e->ring_words = S_HEAD + 3 * (int64_t)KS;
     int rc = 0;
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
-        (rc = dalloc(&e->d_stat, e->ring_words, e->s)) || (rc = dalloc(&e->level1, m, e->s))) {
+        (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s))) {
         delete e;
         return rc;
     }
@@ -836,7 +993,11 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
         cudaEventCreateWithFlags(&e->ev[i], cudaEventDisableTiming);
         e->kuse_at[i] = 0;
     }
-    cudaMemsetAsync(e->d_stat, 0, e->ring_words * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
+    if ((ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        delete e;
+        return cuda_fail(ce, "cudaStreamCreate(capture)");
+    }
     if ((rc = sync_bucket_tables(e))) {
         delete e;
         return rc;
@@ -856,13 +1017,16 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     for (Bucket& b : e->buckets) { dfree(b.rec, s); dfree(b.items, s); }
     dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_doff, s); dfree(e->d_stat, s);
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->delta, s);
-    dfree(e->scr_rec, s); dfree(e->scr_items, s);
+    dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s);
     cudaStreamSynchronize(s);
     for (int i = 0; i < kRing; ++i)
         if (e->ev[i]) cudaEventDestroy(e->ev[i]);
     if (e->ring) cudaFreeHost(e->ring);
+    if (e->gx_count) cudaGraphExecDestroy(e->gx_count);
+    if (e->gx_ckpt) cudaGraphExecDestroy(e->gx_ckpt);
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     delete e;
     return DIC_OK;
 }
@@ -945,7 +1109,7 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     }
     if ((rc = ensure_headroom(e))) return rc;
     // per-stop counters zero, first stop's delta offsets
-    status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, e->d_doff);
+    status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, 0, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
     if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
@@ -972,19 +1136,56 @@ extern "C" int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t lla
     e->cur_first = lfirst;
     e->cur_last = llast;
     e->kuse_issue = e->kuse;
-    if (llast >= lfirst) {
-        const unsigned long long* abort_flag = e->d_stat + S_ABORT;
-        const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
-        if (e->tri) {
-            if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
-                                             e->tri_len, abort_flag, e->s)))
+    const int64_t sl = e->nsched ? e->issued % e->nsched : 0;
+    const bool empty = llast < lfirst;
+    if (e->nsched && (empty ? e->h_sched[2 * sl + 1] < e->h_sched[2 * sl]
+                            : e->h_sched[2 * sl] == lfirst && e->h_sched[2 * sl + 1] == llast)) {
+        // the scheduled chunk: one graph launch (re-captured when its baked-in
+        // pointers / sizes changed)
+        const GraphKey k = graph_key(e, true);
+        if (!e->gx_count || !(k == e->key_count)) {
+            if ((rc = capture_graph(e, &e->gx_count, &e->nk_count, [&](cudaStream_t cs) {
+                     return launch_count(e, k.sched_first, k.sched_last, e->d_sched, cs);
+                 })))
                 return rc;
+            e->key_count = k;
         }
-        if ((rc = count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse, e->d_bitems, bn, e->d_doff,
-                                   e->delta, abort_flag, e->tri ? e->tri_len : 0, e->s)))
-            return rc;
+        if ((rc = launch_graph(e, e->gx_count, e->nk_count))) return rc;
+    } else if (!empty) {
+        if ((rc = launch_count(e, lfirst, llast, nullptr, e->s))) return rc;
     }
     e->counted = true;
+    return DIC_OK;
+}
+
+extern "C" int dic_engine_set_schedule(dic_engine* e, const int64_t* lfirst, const int64_t* llast, int64_t nstops) {
+    DIC_REQUIRE(e && lfirst && llast && nstops >= 1, "dic_engine_set_schedule: bad arguments");
+    for (int64_t i = 0; i < nstops; ++i)
+        DIC_REQUIRE(lfirst[i] >= 0 && (llast[i] < lfirst[i] || llast[i] < e->n_local),
+                    "dic_engine_set_schedule: chunk %lld [%lld, %lld] outside %lld local rows", (long long)i,
+                    (long long)lfirst[i], (long long)llast[i], (long long)e->n_local);
+    // rotate so that the stop with sequence number s reads slot s % nstops
+    std::vector<int64_t> h(2 * nstops);
+    for (int64_t i = 0; i < nstops; ++i) {
+        const int64_t sl = (e->issued + i) % nstops;
+        h[2 * sl] = lfirst[i];
+        h[2 * sl + 1] = llast[i];
+    }
+    int rc;
+    // in-flight stops may still read the old table: replace, never overwrite
+    dfree(e->d_sched, e->s);
+    if ((rc = dalloc(&e->d_sched, 2 * nstops, e->s))) return rc;
+    DIC_CUDA(cudaMemcpyAsync(e->d_sched, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));  // h dies at return
+    e->h_sched.swap(h);
+    e->nsched = nstops;
+    return DIC_OK;
+}
+
+extern "C" int dic_engine_graph_stats(dic_engine* e, int64_t* graphs_captured, int64_t* graph_launches) {
+    DIC_REQUIRE(e && graphs_captured && graph_launches, "dic_engine_graph_stats: null argument");
+    *graphs_captured = e->graphs_captured;
+    *graph_launches = e->graph_launches;
     return DIC_OK;
 }
 
@@ -1011,38 +1212,16 @@ extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     }
     e->counted = false;
     int rc;
-    const int KS = e->KS;
-    // 1. apply + prune + finalize over every slot
-    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0};
-    apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, e->s>>>(
-        e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
-        e->keep, e->d_stat, pa, e->KS);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
-    // 2. compaction the host scheduled from an earlier status
-    for (int k = 0; k < KS && k < e->kuse_issue; ++k) {
-        if (!e->compact_next[k]) continue;
-        e->compact_next[k] = 0;
-        const Bucket& b = e->buckets[k];
-        if (b.cap > e->scr_rec_cap) {
-            dfree(e->scr_rec, e->s);
-            if ((rc = dalloc(&e->scr_rec, b.cap, e->s))) return rc;
-            e->scr_rec_cap = b.cap;
-        }
-        if (b.cap * k > e->scr_items_cap) {
-            dfree(e->scr_items, e->s);
-            if ((rc = dalloc(&e->scr_items, b.cap * k, e->s))) return rc;
-            e->scr_items_cap = b.cap * k;
-        }
-        compact_bucket_kernel<<<1, kCompactThreads, 0, e->s>>>(k, e->d_brec, e->d_bitems, e->d_doff, e->keep,
-                                                               e->scr_rec, e->scr_items, e->d_stat, KS);
-        ::dic::note_launch();
-        DIC_CHECK_LAUNCH("compact_bucket_kernel");
+    const GraphKey k = graph_key(e, false);
+    if (!e->gx_ckpt || !(k == e->key_ckpt)) {
+        if ((rc = capture_graph(e, &e->gx_ckpt, &e->nk_ckpt, [&](cudaStream_t cs) { return launch_checkpoint(e, cs); })))
+            return rc;
+        e->key_ckpt = k;
     }
-    // 3. make_candidates from the frontier (device-sized; all-or-nothing)
-    if ((rc = candidate_step(e))) return rc;
+    if ((rc = launch_graph(e, e->gx_ckpt, e->nk_ckpt))) return rc;
     const int slot = (int)(e->issued % kRing);
-    if ((rc = copy_status(e, slot))) return rc;
+    e->kuse_at[slot] = e->kuse;
+    DIC_CUDA(cudaEventRecord(e->ev[slot], e->s));
     *seq = e->issued++;
     return DIC_OK;
 }
@@ -1091,9 +1270,10 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_ABORT, 0, u, e->s));
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
-        if ((rc = candidate_step(e))) return rc;
-        if ((rc = copy_status(e, slot))) return rc;
-        DIC_CUDA(cudaEventSynchronize(e->ev[slot]));
+        if ((rc = candidate_step(e, e->s))) return rc;
+        if ((rc = launch_status(e, e->s))) return rc;
+        e->kuse_at[slot] = e->kuse;
+        DIC_CUDA(cudaStreamSynchronize(e->s));
         ku = e->kuse_at[slot];
         // the skipped stops are re-issued by the caller
         e->issued = seq + 1;
@@ -1114,13 +1294,11 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
     st->dashed_at_end = e->live;
     e->nrec = (int64_t)h[S_NREC];
     st->records = e->nrec;
-    for (int k = 0; k < ku; ++k) {
-        Bucket& b = e->buckets[k];
-        b.n = (int64_t)h[S_HEAD + 3 * k + 2];
-        b.dead = (int64_t)h[S_HEAD + 3 * k];
-        // schedule a compaction when dead slots are a quarter of the bucket
-        if (b.n > 0 && b.dead > 0 && (b.dead * 4 >= b.n || b.dead == b.n)) e->compact_next[k] = 1;
+    if ((int64_t)h[S_SEQ] != seq) {
+        set_error("dic_engine_poll: status slot holds stop %lld, expected %lld", (long long)h[S_SEQ], (long long)seq);
+        return DIC_ESTATE;
     }
+    for (int k = 0; k < ku; ++k) e->buckets[k].n = (int64_t)h[S_HEAD + 3 * k + 2];
     // headroom for the stops issued next (growth is stream-ordered)
     if ((rc = ensure_headroom(e))) return rc;
     return DIC_OK;
@@ -1149,6 +1327,10 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     DIC_REQUIRE(stop_max >= 1 && depth >= 1 && depth < kRing, "dic_engine_run: bad stop_max/depth");
     if (!e->seeded) { set_error("dic_engine_run: engine not seeded"); return DIC_ESTATE; }
     memset(out, 0, sizeof(*out));
+    {
+        const int rc0 = dic_engine_set_schedule(e, lfirst, llast, stop_max);
+        if (rc0) return rc0;
+    }
     struct Flight { int64_t seq; int64_t stop; };
     std::deque<Flight> inflight;
     cudaEvent_t t0[kRing], t1[kRing];

@@ -30,9 +30,20 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
                                                                 int64_t row_splits, int nblk,
                                                                 unsigned long long* __restrict__ tri,
                                                                 const unsigned long long* bn2, int64_t tri_len,
-                                                                const unsigned long long* abort_flag) {
+                                                                const unsigned long long* abort_flag,
+                                                                const int64_t* chunk_ring,
+                                                                const unsigned long long* seq, int ring) {
     // engine use: skip while aborted, or once the pair bucket is mostly gone
     if (abort_flag && (*abort_flag || 2 * (int64_t)*bn2 < tri_len)) return;
+    if (chunk_ring) {
+        // engine graphs: the stop's chunk comes from the ring slot of *seq
+        const int64_t sl = (int64_t)(*seq % (unsigned long long)ring);
+        const int64_t f = chunk_ring[2 * sl], l = chunk_ring[2 * sl + 1];
+        if (l < f) return;
+        geom = chunk_geom(f, l);
+        t_first = geom.g_first / TW;
+        t_last = geom.g_last / TW;
+    }
     constexpr int RW = TW + 4;
     constexpr int RB = RW * 4;
     constexpr uint32_t BLK = kPairBlock * RB;
@@ -155,7 +166,10 @@ static int g_pair_slots[2] = {0, 0};  // resident CTAs per SM for TW = 16 / 32
 
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                        unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
-                       int64_t tri_len = 0, const unsigned long long* abort_flag = nullptr) {
+                       int64_t tri_len = 0, const unsigned long long* abort_flag = nullptr,
+                       const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
+                       int ring = 0) {
+    // with a chunk ring, [first, last] only sizes the grid (the largest chunk)
     if (last < first || m < 2) return DIC_OK;
     const int TW = tile_groups(m);
     const ChunkGeom geom = chunk_geom(first, last);
@@ -184,10 +198,10 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
     dim3 grid((unsigned)rs, (unsigned)blocks);
     if (TW == 32)
         pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
-                                                             tri_len, abort_flag);
+                                                             tri_len, abort_flag, chunk_ring, seq, ring);
     else
         pair_tri_kernel<16><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
-                                                             tri_len, abort_flag);
+                                                             tri_len, abort_flag, chunk_ring, seq, ring);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("pair_tri_kernel");
     return DIC_OK;
@@ -206,9 +220,11 @@ int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* ite
 // engine: pairs of the current stop into the delta slots of bucket 2
 int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                            unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
-                           const unsigned long long* abort_flag, cudaStream_t s) {
+                           const unsigned long long* abort_flag, cudaStream_t s,
+                           const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
+                           int ring = 0) {
     // tri is all-zero between stops: the gather re-zeroes every entry it reads
-    return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag);
+    return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag, chunk_ring, seq, ring);
 }
 
 

@@ -83,6 +83,17 @@ class DeviceEngine:
     def issue_count(self, lfirst: int, llast: int) -> None:
         _abi.call("dic_engine_issue_count", self.h, lfirst, llast)
 
+    def set_schedule(self, lfirst: np.ndarray, llast: np.ndarray) -> None:
+        """The chunk cycle of the coming stops (matching counts run as graphs)."""
+        lf = np.ascontiguousarray(lfirst, dtype=np.int64)
+        ll = np.ascontiguousarray(llast, dtype=np.int64)
+        _abi.call("dic_engine_set_schedule", self.h, lf.ctypes.data, ll.ctypes.data, len(lf))
+
+    def graph_stats(self) -> tuple[int, int]:
+        cap, lau = C.c_int64(), C.c_int64()
+        _abi.call("dic_engine_graph_stats", self.h, C.byref(cap), C.byref(lau))
+        return cap.value, lau.value
+
     def _device_view(self, fn: str):
         ptr, ln = C.c_void_p(), C.c_int64()
         _abi.call(fn, self.h, C.byref(ptr), C.byref(ln))
@@ -216,6 +227,13 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
         stop = 0
         live = npairs
         done = live == 0 or eng is None
+        if not done and hasattr(eng, "set_schedule"):
+            # the stops cycle through fixed chunks: declare them so each count
+            # is one graph launch
+            nst = params.intervals_per_pass
+            sched = [local_chunks[s] if local_chunks is not None else params.chunk_bounds(s + 1) for s in range(nst)]
+            eng.set_schedule(np.array([c[0] for c in sched], dtype=np.int64),
+                             np.array([c[1] for c in sched], dtype=np.int64))
         while True:
             while not done and len(inflight) < depth:
                 stop = stop + 1 if stop < params.intervals_per_pass else 1

@@ -260,3 +260,44 @@ def test_encoder_rejects_out_of_range_items():
     assert db.m == 3 and db.as_int_list() == [0x5, 0x0, 0x2]
     with pytest.raises(dic.EmptyDatabase):
         dic.database_from_transactions([])
+
+
+def test_stop_graphs_match_direct_launches():
+    """The Python pipelined loop (graph launches for scheduled chunks) and the
+    native loop agree with the oracle; an unscheduled loop (direct launches)
+    too, and the graphs are captured a handful of times, not per stop."""
+    from paper_1812_10959_b200.miner import DeviceEngine, run_engine
+
+    cfg = scaled(CONFIGS[2], 30_000, interval=1_500)
+    indptr, indices = generate_csr(cfg)
+    db = dic.BitDatabase.from_csr(indptr, indices, cfg.m)
+    p = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    seen = {}
+
+    class Recording(DeviceEngine):
+        def close(self):
+            if self.h:
+                seen[self.tag] = self.graph_stats()
+            super().close()
+
+    class Graphed(Recording):
+        tag = "graphed"
+
+    class Direct(Recording):
+        tag = "direct"
+
+        def set_schedule(self, lfirst, llast):  # never declared: every count launches directly
+            pass
+
+    tids = db.device_tids()
+    native = run_engine(tids, db.n, db.m, p)
+    graphed = run_engine(tids, db.n, db.m, p, engine_factory=Graphed)
+    direct = run_engine(tids, db.n, db.m, p, engine_factory=Direct)
+    want = O.mine(db.rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=8)
+    for res in (native, graphed, direct):
+        assert [(f.mask, f.size, f.support) for f in res.frequent] == want.frequent
+        assert stats(res) == stats(native)
+    cap, launches = seen["graphed"]
+    assert 2 <= cap <= 40 and launches > 4 * cap
+    cap_d, launches_d = seen["direct"]
+    assert launches_d > 0  # the checkpoint half is a graph either way
