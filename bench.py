@@ -88,14 +88,27 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def mark(self) -> None:
+        """Start of the timed region: summary() keeps the samples from here on
+        (and the one just before, so a short region has at least one)."""
+        self.t_mark = time.time()
+        self.n_mark = len(self._rows())
+
+    def _rows(self) -> list:
+        rows = []
+        if self.path:
+            for line in Path(self.path).read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        return rows
+
     def summary(self) -> dict:
         if self.proc is None or not self.path:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        for line in Path(self.path).read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+        rows = self._rows()
+        n0 = getattr(self, "n_mark", 0)
+        rows = rows[max(0, n0 - 1):]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -318,6 +331,9 @@ def main() -> None:
         torch.cuda.synchronize()
         return
 
+    # nvidia-smi starts (NVML init) before the warm-up, so its start-up does
+    # not land in the timed region; it keeps sampling through it
+    clocks = ClockSampler(local_rank, args.clock_ms).__enter__()
     for _ in range(args.warmup):
         one_run()
     trace = StopTrace()
@@ -331,15 +347,24 @@ def main() -> None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.dic_launch_count()
-    with ClockSampler(local_rank, args.clock_ms) as clocks:
-        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-        e0.record(stream)
-        step_ev[0].record(stream)
-        for i in range(args.steps):
-            res = one_run()
-            step_ev[i + 1].record(stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    # after setup, move the interpreter's long-lived objects (torch's import
+    # graph) out of the collector's generations: a gen-2 collection over them,
+    # triggered by the result objects, costs ~40 ms of host time in one step
+    gc_mode = os.environ.get("DIC_BENCH_GC", "freeze")
+    if gc_mode != "on":
+        import gc
+        gc.collect()
+        gc.freeze() if gc_mode == "freeze" else gc.disable()
+    clocks.mark()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0.record(stream)
+    step_ev[0].record(stream)
+    for i in range(args.steps):
+        res = one_run()
+        step_ev[i + 1].record(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
     step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     one_run(count_events=count_events)  # instrumented run (per-stop count timing), outside the timed region
     if world > 1:
@@ -432,6 +457,7 @@ def main() -> None:
                        "db_passes": s.db_passes, "candidates_generated": s.candidates_generated,
                        "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
             "step_ms": [round(x, 3) for x in step_ms], "host_loop": trace.native,
+            "host_phases_ms": {k: round(v, 3) for k, v in trace.phases.items()},
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
             "cpu_baseline": cpu, "kernel_microbench": kernel,
         }

@@ -42,6 +42,7 @@ class RunStats(C.Structure):
         ("replays", i64),
         ("issue_us", dbl),
         ("poll_us", dbl),
+        ("graphs_captured", i64),
     ]
 
 

@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <chrono>
 #include <deque>
+#include <mutex>
 #include <numeric>
 #include <vector>
 
@@ -550,6 +551,23 @@ __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int
     if (k == top - 1) doff[top] = sh[k];
 }
 
+struct TableUpdate {
+    static constexpr int kMax = 16;
+    int n;
+    int k[kMax];
+    int32_t* rec[kMax];
+    uint16_t* items[kMax];
+    int64_t cap[kMax];
+};
+
+__global__ void set_tables_kernel(int32_t** brec, uint16_t** bitems, int64_t* bcap, TableUpdate u) {
+    const int i = threadIdx.x;
+    if (i >= u.n) return;
+    brec[u.k[i]] = u.rec[i];
+    bitems[u.k[i]] = u.items[i];
+    bcap[u.k[i]] = u.cap[i];
+}
+
 __global__ void collect_frequent_kernel(Records R, int64_t nrec, int32_t* out, unsigned long long* nout) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nrec || R.shape[r] != SOLID_BOX) return;
@@ -575,6 +593,9 @@ using namespace dic;
 struct Bucket {
     int32_t* rec = nullptr;
     uint16_t* items = nullptr;
+    int32_t* dev_rec = nullptr;      // what the device tables hold
+    uint16_t* dev_items = nullptr;
+    int64_t dev_cap = 0;
     int64_t n = 0;     // filled slots (live + dead) at the last polled stop
     int64_t cap = 0;
 };
@@ -595,6 +616,18 @@ struct GraphKey {
     int64_t nsched;
     int64_t sched_first, sched_last;  // chunk sizing the pair kernel's grid
     bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+// Host-side resources of an engine (the mapped status ring, its events, the
+// capture stream) are pooled per process: creating them costs ~1-2 ms
+// (page pinning), more than a small mining run's whole checkpoint loop.
+struct HostRes {
+    unsigned long long* ring = nullptr;
+    unsigned long long* ring_dev = nullptr;
+    int64_t words = 0;
+    int device = -1;
+    cudaEvent_t ev[kRing] = {};
+    cudaStream_t cap = nullptr;
 };
 
 struct dic_engine {
@@ -639,9 +672,9 @@ struct dic_engine {
     int64_t tri_len = 0;
 
     // pipelining
-    unsigned long long* ring = nullptr;  // pinned, device-mapped [kRing][S_HEAD + 3*KS]
+    unsigned long long* ring = nullptr;  // pinned, device-mapped [kRing][S_HEAD + 3*KS] (from hres)
     unsigned long long* ring_dev = nullptr;
-    cudaEvent_t ev[kRing];
+    cudaEvent_t* ev = nullptr;           // [kRing] (from hres)
     int64_t ring_words = 0;
     int kuse_at[kRing];                  // kuse when the slot was written
     int64_t issued = 0;                  // stops issued (sequence numbers 0..issued-1)
@@ -657,15 +690,71 @@ struct dic_engine {
     int64_t* d_sched = nullptr;          // [nsched][2] local chunk per stop, rotated so slot = seq % nsched
     std::vector<int64_t> h_sched;
     int64_t nsched = 0;
-    cudaStream_t cap_stream = nullptr;   // private stream to capture on
+    cudaStream_t cap_stream = nullptr;   // private stream to capture on (from hres)
     cudaGraphExec_t gx_count = nullptr, gx_ckpt = nullptr;
     long long nk_count = 0, nk_ckpt = 0; // kernels per graph launch
     GraphKey key_count{}, key_ckpt{};
     int64_t graphs_captured = 0, graph_launches = 0;
     bool count_graphed = false;          // the pending count went through the graph
+
+    int32_t* res_ids = nullptr;          // result collection (dic_engine_num_frequent)
+    int64_t res_cap = 0, res_F = -1;
+    HostRes hres;
 };
 
 namespace {
+
+std::mutex g_res_mu;
+std::vector<HostRes> g_res_pool;
+
+void free_host_res(HostRes& r) {
+    for (int i = 0; i < kRing; ++i)
+        if (r.ev[i]) cudaEventDestroy(r.ev[i]);
+    if (r.ring) cudaFreeHost(r.ring);
+    if (r.cap) cudaStreamDestroy(r.cap);
+    r = HostRes();
+}
+
+int acquire_host_res(int64_t words, HostRes* out) {
+    int dev = 0;
+    DIC_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_res_mu);
+        for (size_t i = 0; i < g_res_pool.size(); ++i)
+            if (g_res_pool[i].device == dev && g_res_pool[i].words >= words) {
+                *out = g_res_pool[i];
+                g_res_pool.erase(g_res_pool.begin() + (long)i);
+                return DIC_OK;
+            }
+    }
+    HostRes r;
+    r.device = dev;
+    r.words = words;
+    // the ring, then 8 pinned scratch words
+    cudaError_t ce = cudaHostAlloc((void**)&r.ring, ((size_t)kRing * words + 8) * sizeof(unsigned long long),
+                                   cudaHostAllocMapped);
+    if (ce == cudaSuccess) ce = cudaHostGetDevicePointer((void**)&r.ring_dev, r.ring, 0);
+    for (int i = 0; i < kRing && ce == cudaSuccess; ++i) ce = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&r.cap, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) {
+        free_host_res(r);
+        return cuda_fail(ce, "engine host resources (mapped status ring, events, capture stream)");
+    }
+    memset(r.ring, 0, ((size_t)kRing * words + 8) * sizeof(unsigned long long));
+    *out = r;
+    return DIC_OK;
+}
+
+void release_host_res(HostRes& r) {
+    if (!r.ring) return;
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    if (g_res_pool.size() < 8) {
+        g_res_pool.push_back(r);
+        r = HostRes();
+    } else {
+        free_host_res(r);
+    }
+}
 
 template <class T>
 int dalloc(T** p, int64_t count, cudaStream_t s) {
@@ -732,21 +821,34 @@ int ensure_hash(dic_engine* e, int64_t nrec_after) {
     return DIC_OK;
 }
 
+// Push the bucket tables (record / item arrays, capacities) the device has
+// not seen yet, as kernel parameters: stream-ordered, no host buffer to keep
+// alive, no synchronisation.
 int sync_bucket_tables(dic_engine* e) {
-    std::vector<int32_t*> r(e->KS, nullptr);
-    std::vector<uint16_t*> it(e->KS, nullptr);
-    std::vector<int64_t> cap(e->KS, 0);
+    TableUpdate u;
+    u.n = 0;
+    auto flush = [&]() -> int {
+        if (!u.n) return DIC_OK;
+        set_tables_kernel<<<1, 32, 0, e->s>>>(e->d_brec, e->d_bitems, e->d_bcap, u);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("set_tables_kernel");
+        u.n = 0;
+        return DIC_OK;
+    };
+    int rc;
     for (int k = 0; k < e->KS; ++k) {
-        r[k] = e->buckets[k].rec;
-        it[k] = e->buckets[k].items;
-        cap[k] = e->buckets[k].cap;
+        Bucket& b = e->buckets[k];
+        if (b.rec == b.dev_rec && b.items == b.dev_items && b.cap == b.dev_cap) continue;
+        u.k[u.n] = k;
+        u.rec[u.n] = b.rec;
+        u.items[u.n] = b.items;
+        u.cap[u.n] = b.cap;
+        b.dev_rec = b.rec;
+        b.dev_items = b.items;
+        b.dev_cap = b.cap;
+        if (++u.n == TableUpdate::kMax && (rc = flush())) return rc;
     }
-    DIC_CUDA(cudaMemcpyAsync(e->d_brec, r.data(), r.size() * sizeof(int32_t*), cudaMemcpyHostToDevice, e->s));
-    DIC_CUDA(cudaMemcpyAsync(e->d_bitems, it.data(), it.size() * sizeof(uint16_t*), cudaMemcpyHostToDevice, e->s));
-    DIC_CUDA(cudaMemcpyAsync(e->d_bcap, cap.data(), cap.size() * sizeof(int64_t), cudaMemcpyHostToDevice, e->s));
-    // the host vectors die at return: make the copies complete first (rare: growth only)
-    DIC_CUDA(cudaStreamSynchronize(e->s));
-    return DIC_OK;
+    return flush();
 }
 
 // per-stop slot arrays (delta, keep, frontier) cover every bucket capacity
@@ -981,27 +1083,19 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
         delete e;
         return rc;
     }
-    cudaError_t ce = cudaHostAlloc((void**)&e->ring, (size_t)kRing * e->ring_words * sizeof(unsigned long long),
-                                   cudaHostAllocMapped);
-    if (ce == cudaSuccess) ce = cudaHostGetDevicePointer((void**)&e->ring_dev, e->ring, 0);
-    if (ce != cudaSuccess) {
-        delete e;
-        return cuda_fail(ce, "cudaHostAlloc(mapped status ring)");
-    }
-    memset(e->ring, 0, (size_t)kRing * e->ring_words * sizeof(unsigned long long));
-    for (int i = 0; i < kRing; ++i) {
-        cudaEventCreateWithFlags(&e->ev[i], cudaEventDisableTiming);
-        e->kuse_at[i] = 0;
-    }
-    cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
-    if ((ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
-        delete e;
-        return cuda_fail(ce, "cudaStreamCreate(capture)");
-    }
-    if ((rc = sync_bucket_tables(e))) {
+    if ((rc = acquire_host_res(e->ring_words, &e->hres))) {
         delete e;
         return rc;
     }
+    e->ring = e->hres.ring;
+    e->ring_dev = e->hres.ring_dev;
+    e->ev = e->hres.ev;
+    e->cap_stream = e->hres.cap;
+    for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
+    cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
+    cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
+    cudaMemsetAsync(e->d_bcap, 0, KS * sizeof(int64_t), e->s);
     *out = e;
     return DIC_OK;
 }
@@ -1019,14 +1113,10 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->delta, s);
     dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
-    dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s);
-    cudaStreamSynchronize(s);
-    for (int i = 0; i < kRing; ++i)
-        if (e->ev[i]) cudaEventDestroy(e->ev[i]);
-    if (e->ring) cudaFreeHost(e->ring);
+    dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s); dfree(e->res_ids, s);
     if (e->gx_count) cudaGraphExecDestroy(e->gx_count);
     if (e->gx_ckpt) cudaGraphExecDestroy(e->gx_ckpt);
-    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    release_host_res(e->hres);  // the stream was synchronised above: no stop reads the ring any more
     delete e;
     return DIC_OK;
 }
@@ -1112,7 +1202,8 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
     status_kernel<<<1, kDoffMax, 0, e->s>>>(e->d_stat, e->KS, e->kuse, nullptr, 0, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("status_kernel");
-    if ((rc = sync_bucket_tables(e))) return rc;  // synchronises (the host vectors above die at return)
+    if ((rc = sync_bucket_tables(e))) return rc;
+    DIC_CUDA(cudaStreamSynchronize(e->s));  // the host vectors above die at return
     e->live = npairs;
     e->seeded = true;
     if (n_level1) *n_level1 = L;
@@ -1327,6 +1418,7 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     DIC_REQUIRE(stop_max >= 1 && depth >= 1 && depth < kRing, "dic_engine_run: bad stop_max/depth");
     if (!e->seeded) { set_error("dic_engine_run: engine not seeded"); return DIC_ESTATE; }
     memset(out, 0, sizeof(*out));
+    const int64_t captured0 = e->graphs_captured;
     {
         const int rc0 = dic_engine_set_schedule(e, lfirst, llast, stop_max);
         if (rc0) return rc0;
@@ -1387,6 +1479,7 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
         }
         if (st.dashed_at_end == 0) done = true;
     }
+    out->graphs_captured = e->graphs_captured - captured0;
     if (timed)
         for (int i = 0; i < kRing; ++i) {
             cudaEventDestroy(t0[i]);
@@ -1395,25 +1488,28 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     return rc;
 }
 
+// Collect the SOLID_BOX record ids into res_ids (kept for dic_engine_frequent).
 extern "C" int dic_engine_num_frequent(dic_engine* e, int64_t* F) {
     DIC_REQUIRE(e && F, "dic_engine_num_frequent: null argument");
+    unsigned long long* pin = e->hres.ring + kRing * e->hres.words;  // pinned scratch words past the ring
+    DIC_CUDA(cudaMemcpyAsync(pin, e->d_stat + S_NREC, sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->s));
     DIC_CUDA(cudaStreamSynchronize(e->s));
-    unsigned long long nrec_d = 0;
-    DIC_CUDA(cudaMemcpy(&nrec_d, e->d_stat + S_NREC, sizeof(nrec_d), cudaMemcpyDeviceToHost));
-    e->nrec = (int64_t)nrec_d;
-    int32_t* ids = nullptr;
-    int rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s);
-    if (rc) return rc;
+    e->nrec = (int64_t)pin[0];
+    int rc;
+    if (e->nrec > e->res_cap) {
+        dfree(e->res_ids, e->s);
+        if ((rc = dalloc(&e->res_ids, e->nrec, e->s))) return rc;
+        e->res_cap = e->nrec;
+    }
     unsigned long long* cnt = e->d_stat + S_SCRATCH;
     DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
+    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, e->res_ids, cnt);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("collect_frequent_kernel");
-    unsigned long long hF = 0;
-    DIC_CUDA(cudaMemcpyAsync(&hF, cnt, sizeof(hF), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaMemcpyAsync(pin, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->s));
     DIC_CUDA(cudaStreamSynchronize(e->s));
-    dfree(ids, e->s);
-    *F = (int64_t)hF;
+    e->res_F = (int64_t)pin[0];
+    *F = e->res_F;
     return DIC_OK;
 }
 
@@ -1421,58 +1517,57 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
                                    int64_t F) {
     DIC_REQUIRE(e && masks_host && sizes_host && supports_host, "dic_engine_frequent: null argument");
     int rc;
-    int32_t* ids = nullptr;
+    if (e->res_F < 0) {
+        int64_t F2 = 0;
+        if ((rc = dic_engine_num_frequent(e, &F2))) return rc;
+    }
+    if (F != e->res_F) {
+        set_error("dic_engine_frequent: F=%lld but %lld frequent records", (long long)F, (long long)e->res_F);
+        return DIC_EINVAL;
+    }
+    e->res_F = -1;  // ids consumed
+    const int W = e->W;
+    if (F == 0) return DIC_OK;
     unsigned long long* dm = nullptr;
     int32_t* dsz = nullptr;
     int64_t* dsu = nullptr;
-    const int64_t F1 = std::max<int64_t>(F, 1);
-    if ((rc = dalloc(&ids, std::max<int64_t>(e->nrec, 1), e->s)) || (rc = dalloc(&dm, F1 * e->W, e->s)) ||
-        (rc = dalloc(&dsz, F1, e->s)) || (rc = dalloc(&dsu, F1, e->s)))
-        return rc;
-    unsigned long long* cnt = e->d_stat + S_SCRATCH;
-    DIC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->s));
-    collect_frequent_kernel<<<nblk(e->nrec), 256, 0, e->s>>>(e->R, e->nrec, ids, cnt);
+    if ((rc = dalloc(&dm, F * W, e->s)) || (rc = dalloc(&dsz, F, e->s)) || (rc = dalloc(&dsu, F, e->s))) return rc;
+    gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, W, e->res_ids, F, dm, dsz, dsu);
     ::dic::note_launch();
-    unsigned long long hF = 0;
-    DIC_CUDA(cudaMemcpyAsync(&hF, cnt, sizeof(hF), cudaMemcpyDeviceToHost, e->s));
-    DIC_CUDA(cudaStreamSynchronize(e->s));
-    if ((int64_t)hF != F) {
-        set_error("dic_engine_frequent: F=%lld but %llu frequent records", (long long)F, hF);
-        return DIC_EINVAL;
-    }
-    if (F > 0) {
-        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->W, ids, F, dm, dsz, dsu);
-        ::dic::note_launch();
-        DIC_CHECK_LAUNCH("gather_frequent_kernel");
-        DIC_CUDA(cudaMemcpyAsync(masks_host, dm, F * e->W * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s));
-        DIC_CUDA(cudaMemcpyAsync(sizes_host, dsz, F * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));
-        DIC_CUDA(cudaMemcpyAsync(supports_host, dsu, F * sizeof(int64_t), cudaMemcpyDeviceToHost, e->s));
-    }
-    dfree(ids, e->s); dfree(dm, e->s); dfree(dsz, e->s); dfree(dsu, e->s);
+    DIC_CHECK_LAUNCH("gather_frequent_kernel");
+    std::vector<uint64_t> m1((size_t)F * W);
+    std::vector<int32_t> s1(F);
+    std::vector<int64_t> p1(F);
+    DIC_CUDA(cudaMemcpyAsync(m1.data(), dm, F * W * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaMemcpyAsync(s1.data(), dsz, F * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaMemcpyAsync(p1.data(), dsu, F * sizeof(int64_t), cudaMemcpyDeviceToHost, e->s));
+    dfree(dm, e->s); dfree(dsz, e->s); dfree(dsu, e->s);
     DIC_CUDA(cudaStreamSynchronize(e->s));
     // canonical order of the reference's result (engine.py:446-455): by size,
-    // then by the mask as an integer, i.e. most significant word first
-    const int W = e->W;
+    // then by the mask as an integer, i.e. most significant word first.  Keys
+    // are byte strings (size, then the words MSW first, all big-endian), so
+    // one memcmp decides each comparison.
+    const size_t kb = 4 + 8 * (size_t)W;
+    std::vector<uint8_t> keys((size_t)F * kb);
+    for (int64_t i = 0; i < F; ++i) {
+        uint8_t* k = keys.data() + (size_t)i * kb;
+        const uint32_t sz = (uint32_t)s1[i];
+        k[0] = (uint8_t)(sz >> 24); k[1] = (uint8_t)(sz >> 16); k[2] = (uint8_t)(sz >> 8); k[3] = (uint8_t)sz;
+        for (int w = 0; w < W; ++w) {
+            const uint64_t x = __builtin_bswap64(m1[(size_t)i * W + (W - 1 - w)]);
+            memcpy(k + 4 + 8 * w, &x, 8);
+        }
+    }
     std::vector<int64_t> idx(F);
     std::iota(idx.begin(), idx.end(), 0);
-    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
-        if (sizes_host[a] != sizes_host[b]) return sizes_host[a] < sizes_host[b];
-        for (int w = W - 1; w >= 0; --w) {
-            const uint64_t x = masks_host[a * W + w], y = masks_host[b * W + w];
-            if (x != y) return x < y;
-        }
-        return false;
-    });
-    std::vector<uint64_t> m2((size_t)F * W);
-    std::vector<int32_t> s2(F);
-    std::vector<int64_t> p2(F);
+    const uint8_t* kp = keys.data();
+    std::sort(idx.begin(), idx.end(),
+              [&](int64_t a, int64_t b) { return memcmp(kp + (size_t)a * kb, kp + (size_t)b * kb, kb) < 0; });
     for (int64_t i = 0; i < F; ++i) {
-        std::copy(masks_host + idx[i] * W, masks_host + idx[i] * W + W, m2.begin() + i * W);
-        s2[i] = sizes_host[idx[i]];
-        p2[i] = supports_host[idx[i]];
+        const int64_t j = idx[i];
+        memcpy(masks_host + (size_t)i * W, m1.data() + (size_t)j * W, W * sizeof(uint64_t));
+        sizes_host[i] = s1[j];
+        supports_host[i] = p1[j];
     }
-    std::copy(m2.begin(), m2.end(), masks_host);
-    std::copy(s2.begin(), s2.end(), sizes_host);
-    std::copy(p2.begin(), p2.end(), supports_host);
     return DIC_OK;
 }

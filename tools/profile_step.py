@@ -48,6 +48,25 @@ def main() -> None:
         a[1] += ev.device_time_total / 1000.0  # us -> ms
         busy += ev.device_time_total / 1000.0
     rows = sorted(agg.items(), key=lambda kv: -kv[1][1])
+    # timeline: idle gaps between consecutive device activities
+    acts = sorted((ev.time_range.start, ev.time_range.end, ev.name[:40]) for ev in prof.events()
+                  if ev.device_type.name == "CUDA")
+    gaps = []
+    for (s0, e0, n0), (s1, e1, n1) in zip(acts, acts[1:]):
+        if s1 > e0:
+            gaps.append((s1 - e0, n0, n1))
+    span = (acts[-1][1] - acts[0][0]) / 1000.0 if acts else 0.0
+    idle = sum(g for g, _, _ in gaps) / 1000.0
+    print(f"device span {span:.1f} ms, idle inside the span {idle:.1f} ms over {len(gaps)} gaps")
+    hist = defaultdict(lambda: [0, 0.0])
+    for g, n0, n1 in gaps:
+        key = (n0.split("(")[0][-28:], n1.split("(")[0][-28:])
+        hist[key][0] += 1
+        hist[key][1] += g / 1000.0
+    for (n0, n1), (c, ms) in sorted(hist.items(), key=lambda kv: -kv[1][1])[:12]:
+        print(f"  gap {ms:7.3f} ms {c:5d} x {ms / c * 1000:8.2f} us  {n0} -> {n1}")
+    top = sorted(gaps, reverse=True)[:8]
+    print("  largest:", [(round(g / 1000.0, 3), a.split("(")[0][-24:], b.split("(")[0][-24:]) for g, a, b in top])
     print(f"{cfg.name}: wall {wall * 1000:.1f} ms, GPU busy {busy:.1f} ms, frequent {len(res.frequent)}")
     for name, (n, ms) in rows[:25]:
         print(f"{ms:9.3f} ms {n:6d} x {ms / n * 1000:9.2f} us  {name}")
