@@ -75,7 +75,7 @@ struct BucketDesc {
 struct StreamArgs {
     const uint32_t* tids;
     int32_t m, TW;
-    int32_t rowlanes;  // TW == 32: use the conflict-free row-lane units
+    int32_t rowlanes;  // use the row-lane units for sizes <= 8
     uint32_t tile_bytes;
     int64_t t_first, t_last;  // inclusive tile range of the chunk
     int64_t row_splits;
@@ -184,27 +184,29 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     }
 }
 
-// Row-lane variant (TW = 32): 8 lanes share a candidate, lane `sub` reading
-// 16-byte chunk `sub` of each item row, so a quarter-warp always reads one
-// contiguous 128-byte row — conflict-free whatever the items are (random
-// candidates, e.g. cfg5).  Item ids stay packed two per register (the row
-// offset is one IMAD away) so a CTA still holds 64 x R candidates; each
-// lane's partial count is reduced over its 8 lanes once per unit.
+// Row-lane variant: SUB = TW/4 lanes share a candidate, lane `sub` reading
+// 16-byte chunk `sub` of each item row, so SUB adjacent lanes always read one
+// contiguous row (128 B at TW = 32, 64 B at TW = 16): conflict-free or nearly
+// so whatever the items are (random candidates, e.g. cfg5), where one
+// candidate per lane scatters 32 rows over the banks.  Item ids stay packed
+// two per register (the row offset is one IMAD away) so a CTA still holds
+// rl_slots x R candidates; each lane's partial count is reduced over its SUB
+// lanes once per unit.
 __host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 24 : (K <= 6 ? 16 : 12)); }
-constexpr int kRLSlots = kStreamThreads / 8;  // candidate slots per CTA row
+__host__ __device__ constexpr int rl_slots(int TW) { return kStreamThreads / (TW / 4); }  // candidate slots per CTA row
 
-template <int K>
+template <int K, int TW>
 __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids, int m, uint32_t tb,
                                                const ChunkGeom& geom, const uint16_t* __restrict__ items, int64_t C,
                                                unsigned long long* __restrict__ out, int64_t blk, int64_t t0,
                                                int64_t t1, uint8_t* smem, uint32_t (&uses)[2]) {
-    constexpr int TW = 32, RB = (TW + 4) * 4, R = rl_regs(K), KP = (K + 1) / 2;
+    constexpr int RB = (TW + 4) * 4, R = rl_regs(K), KP = (K + 1) / 2, SUB = TW / 4;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
-    const int sub = threadIdx.x & 7, slot = threadIdx.x >> 3;
+    const int sub = threadIdx.x & (SUB - 1), slot = threadIdx.x / SUB;
     // a thread owns R CONSECUTIVE candidates: in a sorted bucket they mostly
     // share their first item, whose chunk is then loaded once per tile
-    const int64_t cbase = blk * (int64_t)kRLSlots * R + (int64_t)slot * R;
+    const int64_t cbase = blk * (int64_t)rl_slots(TW) * R + (int64_t)slot * R;
     if (threadIdx.x == 0) {
         fence_proxy_async();
         issue_tile(smem, tids, tb, t0, 0);
@@ -270,33 +272,33 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         uint32_t x = cnt[r];
-        x += __shfl_xor_sync(0xFFFFFFFFu, x, 1);
-        x += __shfl_xor_sync(0xFFFFFFFFu, x, 2);
-        x += __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+#pragma unroll
+        for (int o = 1; o < SUB; o <<= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
         const int64_t c = cbase + r;
         if (sub == 0 && c < C && x) atomicAdd(out + c, (unsigned long long)x);
     }
 }
 
+template <int TW>
 __device__ __forceinline__ void dispatch_unit_rl(int k, const uint32_t* tids, int m, uint32_t tb,
                                                  const ChunkGeom& geom, const uint16_t* items, int64_t C,
                                                  unsigned long long* out, int64_t blk, int64_t t0, int64_t t1,
                                                  uint8_t* smem, uint32_t (&uses)[2]) {
     switch (k) {
-        case 1: stream_unit_rl<1>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 2: stream_unit_rl<2>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 3: stream_unit_rl<3>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 4: stream_unit_rl<4>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 5: stream_unit_rl<5>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 6: stream_unit_rl<6>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        case 7: stream_unit_rl<7>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
-        default: stream_unit_rl<8>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 1: stream_unit_rl<1, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 2: stream_unit_rl<2, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 3: stream_unit_rl<3, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 4: stream_unit_rl<4, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 5: stream_unit_rl<5, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 6: stream_unit_rl<6, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        case 7: stream_unit_rl<7, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
+        default: stream_unit_rl<8, TW>(tids, m, tb, geom, items, C, out, blk, t0, t1, smem, uses); break;
     }
 }
 
 // candidates per block of the unit kind used for (TW, k)
 __host__ __device__ inline int64_t cands_per_block(int TW, int k, bool rowlanes) {
-    if (rowlanes && TW == 32 && k <= 8) return (int64_t)kRLSlots * rl_regs(k);
+    if (rowlanes && k <= 8) return (int64_t)rl_slots(TW) * rl_regs(k);
     return (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
 }
 
@@ -345,8 +347,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const _
     if (t0 >= t1) return;
     init_barriers(smem);
     uint32_t uses[2] = {0u, 0u};
-    if (TW == 32 && a.rowlanes && B.k <= 8)
-        dispatch_unit_rl(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
+    if (a.rowlanes && B.k <= 8)
+        dispatch_unit_rl<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
     else
         dispatch_unit<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
 }
@@ -374,6 +376,7 @@ struct DevCountArgs {
     const int64_t* chunk_ring;
     const unsigned long long* seq;
     int32_t ring;
+    int64_t small_max;  // at most this many sparse candidates: the unstaged path
 };
 
 // The chunk geometry of this launch (host-given, or read from the ring).
@@ -393,30 +396,84 @@ __device__ __forceinline__ bool dev_chunk(const DevCountArgs& a, ChunkGeom& geom
     return true;
 }
 
+// Few candidates: staging whole tiles (all m item rows) costs more than the
+// count.  SUB = TW/4 lanes per (candidate, tile range) load the candidate's
+// item rows of each tile straight from global memory (16 B per lane, one
+// contiguous row segment per lane group; the chunk is L2-resident), AND them,
+// and popcount; partial counts are reduced over the group once.
+template <int TW>
+__device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const ChunkGeom& geom, int64_t t_first,
+                                                int64_t nt, const int64_t* cpref, int kuse) {
+    constexpr int SUB = TW / 4, RW = TW + 4;
+    const int64_t tile_words = (int64_t)a.m * RW;
+    const int lane = threadIdx.x & 31, sub = lane & (SUB - 1);
+    const unsigned gmask = ((1u << SUB) - 1u) << (lane & ~(SUB - 1));
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SUB;
+    const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / SUB;
+    const int64_t Ctot = cpref[kuse];
+    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, ngroups / std::max<int64_t>(Ctot, 1)));
+    const int64_t W = Ctot * rs;
+    for (int64_t w = gid; w < W; w += ngroups) {
+        const int64_t cg = w / rs, r = w - cg * rs;
+        int k = 1;
+        while (cpref[k + 1] <= cg) ++k;
+        const int64_t c = cg - cpref[k];
+        const uint16_t* it = a.items_tab[k] + c * k;
+        const int64_t t0 = t_first + nt * r / rs, t1 = t_first + nt * (r + 1) / rs;
+        uint32_t cnt = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const uint32_t* base = a.tids + t * tile_words + sub * 4;
+            uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)__ldg(it) * RW));
+            for (int j = 1; j < k; ++j)
+                v = and4(v, __ldg(reinterpret_cast<const uint4*>(base + (int64_t)__ldg(it + j) * RW)));
+            if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
+                const int64_t g = t * TW + sub * 4;
+                v.x &= group_mask(geom, g);
+                v.y &= group_mask(geom, g + 1);
+                v.z &= group_mask(geom, g + 2);
+                v.w &= group_mask(geom, g + 3);
+            }
+            cnt += popc4(v);
+        }
+#pragma unroll
+        for (int o = 1; o < SUB; o <<= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
+        if (sub == 0 && cnt) atomicAdd(a.delta + a.doff[k] + c, (unsigned long long)cnt);
+    }
+}
+
 template <int TW>
 __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __grid_constant__ DevCountArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int64_t pref[kDevMaxK + 1];
+    __shared__ int64_t cpref[kDevMaxK + 1];
     if (*a.abort) return;
     ChunkGeom geom;
     int64_t t_first, t_last;
     if (!dev_chunk(a, geom, t_first, t_last)) return;
     if (threadIdx.x == 0) {
         const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
-        int64_t acc = 0;
+        int64_t acc = 0, cacc = 0;
         pref[0] = 0;
+        cpref[0] = 0;
         for (int k = 1; k < a.kuse; ++k) {
             int64_t C = (int64_t)a.bn[k];
             if (k == 2 && dense) C = 0;
-            const int64_t per = (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
+            const int64_t per = cands_per_block(TW, k, true);
             pref[k] = acc;
+            cpref[k] = cacc;
             acc += (C + per - 1) / per;
+            cacc += C;
         }
         pref[a.kuse] = acc;
+        cpref[a.kuse] = cacc;
     }
     __syncthreads();
     const int64_t B = pref[a.kuse];
     if (B == 0) return;
+    if (cpref[a.kuse] <= a.small_max) {
+        count_dev_small<TW>(a, geom, t_first, t_last - t_first + 1, cpref, a.kuse);
+        return;
+    }
     const int64_t nt = t_last - t_first + 1;
     const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)gridDim.x / B));
     const int64_t U = B * rs;
@@ -428,9 +485,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __gr
         int k = 1;
         while (pref[k + 1] <= gb) ++k;
         const int64_t t0 = t_first + nt * r / rs, t1 = t_first + nt * (r + 1) / rs;
-        if (t0 < t1)
-            dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
-                              a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+        if (t0 < t1) {
+            if (k <= 8)
+                dispatch_unit_rl<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
+                                     a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+            else
+                dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
+                                  a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+        }
         __syncthreads();
     }
 }
@@ -621,6 +683,12 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
     a.chunk_ring = chunk_ring;
     a.seq = seq;
     a.ring = ring;
+    static int64_t small_max = -1;
+    if (small_max < 0) {
+        const char* e = getenv("DIC_COUNT_SMALL_MAX");
+        small_max = e ? atoll(e) : 2048;  // measured crossover on cfg4
+    }
+    a.small_max = small_max;
     const size_t smem = 128 + 2 * (size_t)a.tile_bytes;
     // the kernel's static shared memory (the unit prefix table) shares the budget
     static size_t static_smem = 0;

@@ -24,15 +24,40 @@ __host__ __device__ inline int64_t tri_index(int64_t a, int64_t b, int64_t m) {
     return a * m - a * (a + 1) / 2 + (b - a - 1);
 }
 
-template <int TW>
-__global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
-                                                                ChunkGeom geom, int64_t t_first, int64_t t_last,
-                                                                int64_t row_splits, int nblk,
-                                                                unsigned long long* __restrict__ tri,
-                                                                const unsigned long long* bn2, int64_t tri_len,
-                                                                const unsigned long long* abort_flag,
-                                                                const int64_t* chunk_ring,
-                                                                const unsigned long long* seq, int ring) {
+// Block pair bi (row-major over the upper triangle of nblk x nblk item
+// blocks) -> item ranges.
+struct PairBlock {
+    int a0, b0, na, nb;
+    bool diag;
+};
+__device__ __forceinline__ PairBlock pair_block(int64_t bi, int nblk, int m) {
+    int y = (int)bi, I = 0;
+    while (y >= nblk - I) {
+        y -= nblk - I;
+        ++I;
+    }
+    PairBlock p;
+    p.a0 = I * kPairBlock;
+    p.b0 = (I + y) * kPairBlock;
+    p.na = min(kPairBlock, m - p.a0);
+    p.nb = min(kPairBlock, m - p.b0);
+    p.diag = y == 0;
+    return p;
+}
+
+// Persistent: the (block pair, tile) units of the chunk, block-pair major, are
+// split evenly over the grid, so every CTA walks a contiguous run of tiles of
+// one or two block pairs (counters flushed with atomics when the pair
+// changes) and all SMs finish together.  Tiles arrive by TMA bulk copies
+// into a 2-stage ring.
+template <int TW, int MINB>
+__global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
+                                                                   ChunkGeom geom, int64_t t_first, int64_t t_last,
+                                                                   int nblk, unsigned long long* __restrict__ tri,
+                                                                   const unsigned long long* bn2, int64_t tri_len,
+                                                                   const unsigned long long* abort_flag,
+                                                                   const int64_t* chunk_ring,
+                                                                   const unsigned long long* seq, int ring) {
     // engine use: skip while aborted, or once the pair bucket is mostly gone
     if (abort_flag && (*abort_flag || 2 * (int64_t)*bn2 < tri_len)) return;
     if (chunk_ring) {
@@ -51,56 +76,68 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* buf = smem + 128;  // [2 stages][A block, B block]
 
-    int y = blockIdx.y, I = 0;
-    while (y >= nblk - I) {
-        y -= nblk - I;
-        ++I;
-    }
-    const int J = I + y;
-    const bool diag = I == J;
-    const int a0 = I * kPairBlock, b0 = J * kPairBlock;
-    const int na = min(kPairBlock, m - a0), nb = min(kPairBlock, m - b0);
-    const uint32_t abytes = (uint32_t)na * RB, bbytes = (uint32_t)nb * RB;
     const int64_t tile_words = (int64_t)m * RW;
     const int64_t nt = t_last - t_first + 1;
-    const int64_t t0 = t_first + nt * blockIdx.x / row_splits;
-    const int64_t t1 = t_first + nt * (blockIdx.x + 1) / row_splits;
-    if (t0 >= t1) return;
+    const int64_t U = (int64_t)nblk * (nblk + 1) / 2 * nt;
+    const int64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
 
-    auto issue = [&](int64_t t, int s) {
+    auto issue = [&](int64_t u, int s) {
+        const int64_t bi = u / nt;
+        const int64_t t = t_first + (u - bi * nt);
+        const PairBlock pb = pair_block(bi, nblk, m);
+        const uint32_t ab = (uint32_t)pb.na * RB, bb = (uint32_t)pb.nb * RB;
         uint8_t* dst = buf + (size_t)s * 2 * BLK;
         const uint32_t* src = tids + t * tile_words;
-        mbar_expect_tx(&bar[s], abytes + (diag ? 0u : bbytes));
-        bulk_g2s(dst, src + (int64_t)a0 * RW, abytes, &bar[s]);
-        if (!diag) bulk_g2s(dst + BLK, src + (int64_t)b0 * RW, bbytes, &bar[s]);
+        mbar_expect_tx(&bar[s], ab + (pb.diag ? 0u : bb));
+        bulk_g2s(dst, src + (int64_t)pb.a0 * RW, ab, &bar[s]);
+        if (!pb.diag) bulk_g2s(dst + BLK, src + (int64_t)pb.b0 * RW, bb, &bar[s]);
     };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
-        issue(t0, 0);
-        if (t0 + 1 < t1) issue(t0 + 1, 1);
+        issue(u0, 0);
+        if (u0 + 1 < u1) issue(u0 + 1, 1);
     }
     __syncthreads();
 
     const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
     uint32_t cnt[4][4];
+    int64_t cur = -1;
+    PairBlock pb{0, 0, 0, 0, true};
+    auto flush = [&]() {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cnt[i][j] = 0;
+            for (int j = 0; j < 4; ++j) {
+                const int a = pb.a0 + ta + 16 * i, b = pb.b0 + tb + 16 * j;
+                if (a < b && b < m && cnt[i][j]) atomicAdd(tri + tri_index(a, b, m), (unsigned long long)cnt[i][j]);
+            }
+    };
 
-    for (int64_t t = t0; t < t1; ++t) {
-        const int s = (int)((t - t0) & 1);
-        mbar_wait(&bar[s], (uint32_t)(((t - t0) >> 1) & 1));
+    for (int64_t u = u0; u < u1; ++u) {
+        const int s = (int)((u - u0) & 1);
+        const int64_t bi = u / nt;
+        const int64_t t = t_first + (u - bi * nt);
+        if (bi != cur) {
+            if (cur >= 0) flush();
+            cur = bi;
+            pb = pair_block(bi, nblk, m);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cnt[i][j] = 0;
+        }
+        mbar_wait(&bar[s], (uint32_t)(((u - u0) >> 1) & 1));
         uint8_t* A = buf + (size_t)s * 2 * BLK;
-        uint8_t* B = diag ? A : A + BLK;
+        uint8_t* B = pb.diag ? A : A + BLK;
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             // chunk edge inside this tile: zero the rows outside [first, last]
-            const int rows = diag ? na : 2 * kPairBlock;
+            const int rows = pb.diag ? pb.na : 2 * kPairBlock;
             for (int idx = threadIdx.x; idx < rows * RW; idx += kPairThreads) {
                 const int r = idx / RW, slot = idx - r * RW;
-                if (slot >= TW || (r < kPairBlock ? r >= na : r - kPairBlock >= nb)) continue;
+                if (slot >= TW || (r < kPairBlock ? r >= pb.na : r - kPairBlock >= pb.nb)) continue;
                 uint32_t* w = reinterpret_cast<uint32_t*>(A + (size_t)r * RB) + slot;
                 *w &= group_mask(geom, t * TW + slot);
             }
@@ -112,7 +149,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
         // the bound from the POPC pipe (16 lanes/SM/clk) to LOP3 (64)
 #pragma unroll
         for (int q = 0; q < TW / 4; q += 2) {
-            uint4 av0[4], av1[4], bv0[4], bv1[4];
+            uint4 av0[4], av1[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
@@ -120,27 +157,19 @@ __global__ void __launch_bounds__(kPairThreads) pair_tri_kernel(const uint32_t* 
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                bv0[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
-                bv1[j] = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
+                const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
+                const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cnt[i][j] += and_popc8(av0[i], av1[i], bv0, bv1);
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) cnt[i][j] += and_popc8(av0[i], av1[i], bv0[j], bv1[j]);
         }
         __syncthreads();  // stage s consumed
-        if (threadIdx.x == 0 && t + 2 < t1) {
+        if (threadIdx.x == 0 && u + 2 < u1) {
             fence_proxy_async();
-            issue(t + 2, s);
+            issue(u + 2, s);
         }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int a = a0 + ta + 16 * i, b = b0 + tb + 16 * j;
-            if (a < b && b < m && cnt[i][j]) atomicAdd(tri + tri_index(a, b, m), (unsigned long long)cnt[i][j]);
-        }
+    flush();
 }
 
 // Bit-sliced copy restricted to the selected items (in the given order).
@@ -161,8 +190,37 @@ __global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, 
     }
 }
 
-static int g_pair_attr = 0;
-static int g_pair_slots[2] = {0, 0};  // resident CTAs per SM for TW = 16 / 32
+static int g_pair_slots[4] = {0, 0, 0, 0};  // resident CTAs per SM for (TW = 16 / 32) x (MINB = 3 / 4)
+
+template <int TW, int MINB>
+int pair_launch(const uint32_t* tids, int m, ChunkGeom geom, int64_t t_first, int64_t t_last, int nblk,
+                int64_t units, size_t smem, unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
+                const unsigned long long* abort_flag, const int64_t* chunk_ring, const unsigned long long* seq,
+                int ring, cudaStream_t s) {
+    int& per_sm = g_pair_slots[(TW == 32 ? 1 : 0) + (MINB == 4 ? 2 : 0)];
+    if (per_sm == 0) {
+        DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<TW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      64 * 1024));
+        DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<TW, MINB>, kPairThreads, smem));
+        per_sm = std::max(per_sm, 1);
+    }
+    // persistent: one CTA per resident slot (fewer when the chunk is small)
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sm_count()));
+    pair_tri_kernel<TW, MINB><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, nblk, tri, bn2,
+                                                                tri_len, abort_flag, chunk_ring, seq, ring);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("pair_tri_kernel");
+    return DIC_OK;
+}
+
+static int pair_minb() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("DIC_PAIR_MINB");
+        v = (e && atoi(e) == 4) ? 4 : 3;
+    }
+    return v;
+}
 
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                        unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
@@ -176,35 +234,18 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
     const int64_t t_first = geom.g_first / TW, t_last = geom.g_last / TW;
     const int64_t nt = t_last - t_first + 1;
     const int nblk = (m + kPairBlock - 1) / kPairBlock;
-    const int64_t blocks = (int64_t)nblk * (nblk + 1) / 2;
-    DIC_REQUIRE(blocks <= 65535, "count_pairs: %lld block pairs exceed one launch", (long long)blocks);
+    const int64_t units = (int64_t)nblk * (nblk + 1) / 2 * nt;
     const size_t smem = 128 + 2 * 2 * (size_t)kPairBlock * row_words(TW) * 4;
-    if (!g_pair_attr) {
-        DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        g_pair_attr = 1;
-    }
-    // one full wave: as many row splits as the resident CTA slots allow
-    int& per_sm = g_pair_slots[TW == 32 ? 1 : 0];
-    if (per_sm == 0) {
-        if (TW == 32)
-            DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<32>, kPairThreads, smem));
-        else
-            DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<16>, kPairThreads, smem));
-        per_sm = std::max(per_sm, 1);
-    }
-    const int64_t slots = (int64_t)per_sm * sm_count();
-    int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, slots / blocks));
-    dim3 grid((unsigned)rs, (unsigned)blocks);
+    const bool b4 = pair_minb() == 4;
     if (TW == 32)
-        pair_tri_kernel<32><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
-                                                             tri_len, abort_flag, chunk_ring, seq, ring);
-    else
-        pair_tri_kernel<16><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, rs, nblk, tri, bn2,
-                                                             tri_len, abort_flag, chunk_ring, seq, ring);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("pair_tri_kernel");
-    return DIC_OK;
+        return b4 ? pair_launch<32, 4>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
+                                       chunk_ring, seq, ring, s)
+                  : pair_launch<32, 3>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
+                                       chunk_ring, seq, ring, s);
+    return b4 ? pair_launch<16, 4>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
+                                   chunk_ring, seq, ring, s)
+              : pair_launch<16, 3>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
+                                   chunk_ring, seq, ring, s);
 }
 
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,

@@ -17,7 +17,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 import paper_1812_10959_b200 as dic  # noqa: E402
 from paper_1812_10959_b200 import device as D  # noqa: E402
-from paper_1812_10959_b200.miner import run_engine  # noqa: E402
+from paper_1812_10959_b200.miner import StopTrace, run_engine  # noqa: E402
 from paper_1812_10959_b200.workloads import CONFIGS, generate_csr  # noqa: E402
 
 
@@ -35,7 +35,8 @@ def main() -> None:
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         t = time.perf_counter()
-        res = run_engine(tids, cfg.n, cfg.m, params, depth=depth)
+        trace = StopTrace()
+        res = run_engine(tids, cfg.n, cfg.m, params, depth=depth, trace=trace)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t
     agg = defaultdict(lambda: [0, 0.0])
@@ -65,6 +66,17 @@ def main() -> None:
         hist[key][1] += g / 1000.0
     for (n0, n1), (c, ms) in sorted(hist.items(), key=lambda kv: -kv[1][1])[:12]:
         print(f"  gap {ms:7.3f} ms {c:5d} x {ms / c * 1000:8.2f} us  {n0} -> {n1}")
+    # per-launch duration series of the per-stop kernels (stop order)
+    series = defaultdict(list)
+    for s0, e0, n0 in acts:
+        for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "insert_commit", "compact", "status"):
+            if key in n0:
+                series[key].append(round(e0 - s0, 1))
+    for key, v in series.items():
+        chunks = [v[i:i + 25] for i in range(0, len(v), 25)]
+        print(f"  {key:12s} us per 25-stop window (mean):", [round(sum(c) / len(c), 1) for c in chunks])
+    d = [st["dashed_at_start"] for st in trace.stops]
+    print("  dashed       per 25-stop window (mean):", [round(sum(d[i:i + 25]) / len(d[i:i + 25])) for i in range(0, len(d), 25)])
     top = sorted(gaps, reverse=True)[:8]
     print("  largest:", [(round(g / 1000.0, 3), a.split("(")[0][-24:], b.split("(")[0][-24:]) for g, a, b in top])
     print(f"{cfg.name}: wall {wall * 1000:.1f} ms, GPU busy {busy:.1f} ms, frequent {len(res.frequent)}")
