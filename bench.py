@@ -52,6 +52,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--no-kernel-bench", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=500, help="nvidia-smi sampling period in the timed region")
     ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
+    ap.add_argument("--step-trace", action="store_true", help="per-step host phase / loop diagnostics in the JSON")
     return ap.parse_args()
 
 
@@ -316,9 +317,11 @@ def main() -> None:
     n_local = int(indptr.size - 1)
 
     # pinned host CSR (the e2e input) and the HBM-resident bit-sliced copy
+    # pinned host CSR (the e2e input): item ids as uint16 (the universe is
+    # < 65536), the form BitDatabase.from_csr streams to the encoder
     h_indptr = torch.from_numpy(indptr).pin_memory()
-    h_indices = torch.from_numpy(indices).pin_memory()
-    db = dic.BitDatabase.from_csr(h_indptr.cuda(), h_indices.cuda(), cfg.m)
+    h_indices = torch.from_numpy(indices.astype(np.uint16)).pin_memory()
+    db = dic.BitDatabase.from_csr(h_indptr, h_indices, cfg.m)
     tids = db.device_tids()
     torch.cuda.synchronize()
 
@@ -359,8 +362,14 @@ def main() -> None:
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
     step_ev[0].record(stream)
+    step_diag = []
     for i in range(args.steps):
-        res = one_run()
+        if args.step_trace:
+            tr = StopTrace()
+            res = one_run(trace=tr)
+            step_diag.append({"phases": {k: round(v, 2) for k, v in tr.phases.items()}, "loop": tr.native})
+        else:
+            res = one_run()
         step_ev[i + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -406,7 +415,7 @@ def main() -> None:
     # end to end through the public API from pinned host CSR
     e2e = None
     if not args.no_e2e:
-        h2d = int(h_indptr.numel() * 8 + h_indices.numel() * 4)
+        h2d = int(h_indptr.numel() * h_indptr.element_size() + h_indices.numel() * h_indices.element_size())
         W = dic.bits.words_for(cfg.m)
         d2h = int(len(ref.frequent) * (W * 8 + 4 + 8) + 4 * 8)
         if world > 1:
@@ -416,7 +425,7 @@ def main() -> None:
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
-            dbe = dic.BitDatabase.from_csr(h_indptr.cuda(non_blocking=True), h_indices.cuda(non_blocking=True),
+            dbe = dic.BitDatabase.from_csr(h_indptr, h_indices,
                                            cfg.m)
             out = run_engine(dbe.device_tids(), n_local, cfg.m, params, plan=plan if world > 1 else None,
                              group=group)
@@ -458,6 +467,7 @@ def main() -> None:
                        "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
             "step_ms": [round(x, 3) for x in step_ms], "host_loop": trace.native,
             "host_phases_ms": {k: round(v, 3) for k, v in trace.phases.items()},
+            **({"step_diag": step_diag} if step_diag else {}),
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
             "cpu_baseline": cpu, "kernel_microbench": kernel,
         }

@@ -89,6 +89,25 @@ int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int64_t n,
  * the dic_tids_words(n, m) buffer is written.                             */
 int dic_rows_to_tids(const uint64_t* rows, int64_t n, int32_t m,
                      uint32_t* tids, void* stream);
+/* CSR item lists straight into the bit-sliced tiles, rows [row_begin,
+ * row_end) only (tile-aligned: multiples of 32*dic_tids_tile_groups(m) rows,
+ * row_end may be n), so a loader can encode each slab as soon as its H2D
+ * copy lands.  indices are uint16 (index_bytes 2) or int32 (4); indptr is the
+ * GLOBAL int64 [n+1] offset array.  status[4] (device int64) accumulates
+ * across slabs between dic_encode_status_init and dic_encode_status_finish
+ * and then holds what dic_encode_csr reports.  Replaces the same place in
+ * the reference as dic_encode_csr (bitops.py:24-37, database.py:13-86).     */
+int dic_encode_status_init(int64_t* status, void* stream);
+int dic_encode_csr_tids(const int64_t* indptr, const void* indices,
+                        int32_t index_bytes, int64_t n, int32_t m,
+                        int64_t row_begin, int64_t row_end, uint32_t* tids,
+                        int64_t* status, void* stream);
+int dic_encode_status_finish(const int64_t* indptr, int64_t n, int64_t* status,
+                             void* stream);
+/* Inverse transform: bit-sliced tiles -> row bitmap uint64 [n][W] (the host
+ * view BitDatabase.masks of a database encoded straight to tiles).        */
+int dic_tids_to_rows(const uint32_t* tids, int64_t n, int32_t m, uint64_t* rows,
+                     void* stream);
 /* Layout helpers (host functions).                                         */
 int64_t dic_tids_words(int64_t n, int32_t m);
 int dic_tids_tile_groups(int32_t m);

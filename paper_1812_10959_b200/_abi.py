@@ -70,6 +70,10 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_delta": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_checkpoint": (C.c_int, [vp, P(StopStatus)]),
     "dic_engine_issue_count": (C.c_int, [vp, i64, i64]),
+    "dic_encode_status_init": (C.c_int, [vp, vp]),
+    "dic_encode_csr_tids": (C.c_int, [vp, vp, i32, i64, i32, i64, i64, vp, vp, vp]),
+    "dic_encode_status_finish": (C.c_int, [vp, i64, vp, vp]),
+    "dic_tids_to_rows": (C.c_int, [vp, i64, i32, vp, vp]),
     "dic_engine_set_schedule": (C.c_int, [vp, vp, vp, i64]),
     "dic_engine_graph_stats": (C.c_int, [vp, P(i64), P(i64)]),
     "dic_engine_pair_counts": (C.c_int, [vp, P(vp), P(i64)]),

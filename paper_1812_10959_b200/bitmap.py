@@ -9,8 +9,8 @@ the reference's.
 Device residency: ``device_rows()`` is the row bitmap uint64 [n][W] in HBM,
 ``device_tids()`` the tiled bit-sliced copy the support-count kernel streams
 (include/dic_b200.h).  A database built with ``from_csr`` is encoded on the
-GPU (dic_encode_csr) and only copied back to the host if host masks are
-asked for.
+GPU straight into the tiles (dic_encode_csr_tids); rows and host masks are
+derived from them only if asked for.
 """
 
 from __future__ import annotations
@@ -80,9 +80,14 @@ class BitDatabase:
 
     # -- construction on the device --------------------------------------
     @classmethod
-    def from_csr(cls, indptr, indices, m: int) -> "BitDatabase":
-        """Encode CSR item lists (host or device arrays) on the GPU.
+    def from_csr(cls, indptr, indices, m: int, *, slabs: int = 8) -> "BitDatabase":
+        """Encode CSR item lists (host or device arrays) on the GPU, straight
+        into the bit-sliced tiles the count kernels stream.
 
+        ``indptr`` int64 [n+1]; ``indices`` uint16 (any universe up to
+        MAX_ITEMS fits) or int32 ids.  Host inputs are copied in ``slabs``
+        tile-aligned row slabs on a side stream, each slab encoded as soon as
+        it lands (pinned host tensors make the copies asynchronous).
         Duplicate ids collapse; an id outside [0, m) raises
         ItemOutOfRange(item, line=row) for the first one in row-major order,
         as encode_transaction would (bitops.py:24-37)."""
@@ -93,16 +98,64 @@ class BitDatabase:
         D.require_cuda()
         if not 1 <= m <= MAX_ITEMS:
             raise ValueError(f"item universe size must be in [1, {MAX_ITEMS}], got {m}")
-        ip = torch.as_tensor(indptr, dtype=torch.int64).cuda()
-        ix = torch.as_tensor(indices, dtype=torch.int32).cuda()
+        ip = indptr if isinstance(indptr, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(indptr))
+        ix = indices if isinstance(indices, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(indices))
+        if ip.dtype != torch.int64:
+            ip = ip.to(torch.int64)
+        if ix.dtype not in (torch.uint16, torch.int32):
+            ix = ix.to(torch.int32)
         n = int(ip.numel()) - 1
         if n < 1:
             raise EmptyDatabase("database holds zero transactions")
-        rows, status = D.encode_csr(ip, ix, n, m)
+        tids = torch.empty(max(D.tids_words(n, m), 1), dtype=torch.int32, device="cuda")
+        status = torch.empty(4, dtype=torch.int64, device="cuda")
+        D.encode_status_init(status)
+        if ix.is_cuda:
+            dip = ip.cuda(non_blocking=True)
+            D.encode_csr_tids(dip, ix, n, m, 0, n, tids, status)
+            dix = ix
+        else:
+            # slab pipeline: H2D of slab i+1 on a copy stream overlaps the
+            # encode of slab i on the current stream
+            host_ip = ip.numpy() if not ip.is_cuda else ip.cpu().numpy()
+            dip = ip.cuda(non_blocking=True)
+            dix = torch.empty(max(int(ix.numel()), 1), dtype=ix.dtype, device="cuda")
+            rpt = D.tile_groups(m) * 32
+            per = -(-n // max(slabs, 1))  # ceil(n / slabs) rows, rounded up to whole tiles
+            step = -(-per // rpt) * rpt
+            main = torch.cuda.current_stream()
+            copy = torch.cuda.Stream()
+            copy.wait_stream(main)  # dix / dip allocated on main
+            for r0 in range(0, n, step):
+                r1 = min(n, r0 + step)
+                p0, p1 = int(host_ip[r0]), int(host_ip[r1])
+                with torch.cuda.stream(copy):
+                    if p1 > p0:
+                        dix[p0:p1].copy_(ix[p0:p1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                main.wait_event(ev)
+                D.encode_csr_tids(dip, dix, n, m, r0, r1, tids, status)
+            dix.record_stream(copy)
+        D.encode_status_finish(dip, n, status)
         st = status.cpu().numpy()
         if st[1] >= 0:
-            raise ItemOutOfRange(int(ix[int(st[1])].item()), line=int(st[2]), universe=m)
-        return cls.from_device_rows(rows, m)
+            raise ItemOutOfRange(int(dix[int(st[1])].item()), line=int(st[2]), universe=m)
+        return cls.from_device_tids(tids, n, m)
+
+    @classmethod
+    def from_device_tids(cls, tids, n: int, m: int) -> "BitDatabase":
+        """Wrap HBM-resident bit-sliced tiles (no host copy; rows on demand)."""
+        if n < 1:
+            raise EmptyDatabase("database holds zero transactions")
+        self = object.__new__(cls)
+        self._rows = None
+        self._n = int(n)
+        self._m = int(m)
+        self._ints = None
+        self._dev_rows = None
+        self._dev_tids = tids
+        return self
 
     @classmethod
     def from_device_rows(cls, rows, m: int) -> "BitDatabase":
@@ -121,7 +174,7 @@ class BitDatabase:
     # -- host view ---------------------------------------------------------
     def _host_rows(self) -> np.ndarray:
         if self._rows is None:
-            rows = self._dev_rows.cpu().numpy().view(np.uint64).copy()
+            rows = self.device_rows().cpu().numpy().view(np.uint64).copy()
             rows.setflags(write=False)
             self._rows = rows
         return self._rows
@@ -164,7 +217,10 @@ class BitDatabase:
             from . import device as D
 
             D.require_cuda()
-            self._dev_rows = torch.from_numpy(np.ascontiguousarray(self._host_rows())).cuda()
+            if self._rows is None and self._dev_tids is not None:
+                self._dev_rows = D.tids_to_rows(self._dev_tids, self._n, self._m)
+            else:
+                self._dev_rows = torch.from_numpy(np.ascontiguousarray(self._host_rows())).cuda()
         return self._dev_rows
 
     def device_tids(self):

@@ -149,9 +149,151 @@ __global__ void __launch_bounds__(256) rows_to_tids_kernel(
     }
 }
 
+// CSR item lists -> bit-sliced tiles directly, for tiles [t_begin, t_end).
+// A CTA builds one tile image at a time in shared memory (zeroed, then one
+// warp per row OR-ing the row's bit into each item's group word with a
+// shared-memory atomic — the returned old word flags duplicates), then
+// streams the image (pad words included) to HBM with 16-byte stores.  Tiles
+// too large for shared memory are built in place with global atomics.
+// Ids are uint16 or int32 (IDX); the first out-of-range id in row-major order
+// is recorded as in encode_csr_kernel.
+constexpr int kEncThreads = 512;
+template <typename IDX>
+__global__ void __launch_bounds__(kEncThreads) encode_tids_kernel(const int64_t* __restrict__ indptr,
+                                                                  const IDX* __restrict__ indices, int64_t n,
+                                                                  int32_t m, int64_t t_begin, int64_t t_end,
+                                                                  uint32_t* __restrict__ tids,
+                                                                  unsigned long long* __restrict__ status,
+                                                                  int use_smem) {
+    extern __shared__ __align__(16) uint32_t img[];
+    const int TW = tile_groups(m), RW = row_words(TW);
+    const int64_t tw = (int64_t)m * RW;  // multiple of 4 (RW is)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kEncThreads / 32;
+    unsigned long long dup = 0;
+    for (int64_t t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
+        uint32_t* dst = use_smem ? img : tids + t * tw;
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (int64_t i = threadIdx.x; i < tw / 4; i += kEncThreads) d4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        const int64_t r0 = t * TW * 32, r1 = min(n, r0 + (int64_t)TW * 32);
+        for (int64_t r = r0 + warp; r < r1; r += nwarps) {
+            const int64_t b = __ldg(indptr + r), e = __ldg(indptr + r + 1);
+            const int gl = (int)((r - r0) >> 5);
+            const uint32_t bit = 1u << (r & 31);
+            for (int64_t q = b + lane; q < e; q += 32) {
+                const int64_t it = (int64_t)__ldg(indices + q);
+                if (it < 0 || it >= m) {
+                    atomicMin(status + 1, (unsigned long long)q);
+                    continue;
+                }
+                const uint32_t old = atomicOr(dst + it * RW + gl, bit);
+                dup += (old & bit) ? 1u : 0u;
+            }
+        }
+        __syncthreads();
+        if (use_smem) {
+            uint4* o4 = reinterpret_cast<uint4*>(tids + t * tw);
+            for (int64_t i = threadIdx.x; i < tw / 4; i += kEncThreads) o4[i] = d4[i];
+            __syncthreads();
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) dup += __shfl_down_sync(0xFFFFFFFFu, dup, o);
+    if (lane == 0 && dup) atomicAdd(status, dup);
+}
+
+// Bit-sliced tiles -> row bitmap (the inverse transform; the host view of a
+// database encoded straight to tiles).  Thread per (row, 64-bit word).
+__global__ void tids_to_rows_kernel(const uint32_t* __restrict__ tids, int64_t n, int32_t m, int W,
+                                    unsigned long long* __restrict__ rows) {
+    const int TW = tile_groups(m);
+    const int64_t total = n * W;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = x / W;
+        const int w = (int)(x - r * W);
+        const int64_t g = r >> 5;
+        const uint32_t sh = (uint32_t)(r & 31);
+        unsigned long long v = 0;
+        const int top = min(64, m - w * 64);
+        for (int b = 0; b < top; ++b)
+            v |= (unsigned long long)((__ldg(tids + tids_index(m, TW, (uint32_t)(w * 64 + b), g)) >> sh) & 1u) << b;
+        rows[x] = v;
+    }
+}
+
 }  // namespace dic
 
 using namespace dic;
+
+extern "C" int dic_encode_status_init(int64_t* status, void* stream) {
+    DIC_REQUIRE(status, "dic_encode_status_init: null status");
+    init_status_kernel<<<1, 1, 0, as_stream(stream)>>>(reinterpret_cast<unsigned long long*>(status));
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("init_status_kernel");
+    return DIC_OK;
+}
+
+extern "C" int dic_encode_status_finish(const int64_t* indptr, int64_t n, int64_t* status, void* stream) {
+    DIC_REQUIRE(indptr && status && n >= 1, "dic_encode_status_finish: bad arguments");
+    finish_status_kernel<<<1, 1, 0, as_stream(stream)>>>(indptr, n, reinterpret_cast<unsigned long long*>(status));
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("finish_status_kernel");
+    return DIC_OK;
+}
+
+extern "C" int dic_encode_csr_tids(const int64_t* indptr, const void* indices, int32_t index_bytes, int64_t n,
+                                   int32_t m, int64_t row_begin, int64_t row_end, uint32_t* tids, int64_t* status,
+                                   void* stream) {
+    DIC_REQUIRE(n >= 1 && m >= 1 && m <= 65535, "dic_encode_csr_tids: need n >= 1 and 1 <= m <= 65535");
+    DIC_REQUIRE(indptr && tids && status && (indices || row_end <= row_begin), "dic_encode_csr_tids: null pointer");
+    DIC_REQUIRE(index_bytes == 2 || index_bytes == 4, "dic_encode_csr_tids: index_bytes must be 2 or 4, got %d",
+                index_bytes);
+    const int64_t rows_per_tile = (int64_t)tile_groups(m) * 32;
+    DIC_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= n && row_begin % rows_per_tile == 0 &&
+                    (row_end % rows_per_tile == 0 || row_end == n),
+                "dic_encode_csr_tids: rows [%lld, %lld) must be tile-aligned (%lld rows) within %lld",
+                (long long)row_begin, (long long)row_end, (long long)rows_per_tile, (long long)n);
+    if (row_end == row_begin) return DIC_OK;
+    cudaStream_t s = as_stream(stream);
+    const int64_t t_begin = row_begin / rows_per_tile, t_end = (row_end + rows_per_tile - 1) / rows_per_tile;
+    const size_t img = (size_t)tile_words(m) * 4;
+    static int max_smem = 0;
+    if (!max_smem) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        DIC_CUDA(cudaFuncSetAttribute(encode_tids_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_smem));
+        DIC_CUDA(cudaFuncSetAttribute(encode_tids_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_smem));
+    }
+    const int use_smem = img <= (size_t)max_smem ? 1 : 0;
+    const size_t smem = use_smem ? img : 0;
+    // persistent: resident CTAs only (shared-memory bound), tiles strided over them
+    const int per_sm = use_smem ? std::max(1, (int)((size_t)(228 * 1024) / (img + 1024))) : 4;
+    const int64_t grid = std::min<int64_t>(t_end - t_begin, (int64_t)sm_count() * per_sm);
+    auto* st = reinterpret_cast<unsigned long long*>(status);
+    if (index_bytes == 2)
+        encode_tids_kernel<uint16_t><<<(unsigned)grid, kEncThreads, smem, s>>>(
+            indptr, static_cast<const uint16_t*>(indices), n, m, t_begin, t_end, tids, st, use_smem);
+    else
+        encode_tids_kernel<int32_t><<<(unsigned)grid, kEncThreads, smem, s>>>(
+            indptr, static_cast<const int32_t*>(indices), n, m, t_begin, t_end, tids, st, use_smem);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("encode_tids_kernel");
+    return DIC_OK;
+}
+
+extern "C" int dic_tids_to_rows(const uint32_t* tids, int64_t n, int32_t m, uint64_t* rows, void* stream) {
+    DIC_REQUIRE(n >= 1 && m >= 1 && tids && rows, "dic_tids_to_rows: need n >= 1, m >= 1 and buffers");
+    const int W = (m + 63) / 64;
+    const int64_t total = n * W;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+    tids_to_rows_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, as_stream(stream)>>>(
+        tids, n, m, W, reinterpret_cast<unsigned long long*>(rows));
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("tids_to_rows_kernel");
+    return DIC_OK;
+}
 
 extern "C" int dic_encode_csr(const int64_t* indptr, const int32_t* indices, int64_t n,
                               int32_t m, uint64_t* rows, int64_t* status, void* stream) {

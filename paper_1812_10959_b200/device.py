@@ -54,6 +54,32 @@ def encode_csr(indptr: torch.Tensor, indices: torch.Tensor, n: int, m: int) -> t
     return rows[:n], status
 
 
+def encode_status_init(status: torch.Tensor) -> None:
+    _abi.call("dic_encode_status_init", _ptr(status), _stream())
+
+
+def encode_csr_tids(indptr: torch.Tensor, indices: torch.Tensor, n: int, m: int, row_begin: int, row_end: int,
+                    tids: torch.Tensor, status: torch.Tensor) -> None:
+    """Rows [row_begin, row_end) of a device CSR (int64 indptr[n+1], uint16 or
+    int32 indices) straight into the bit-sliced tiles ``tids``."""
+    ib = 2 if indices.dtype in (torch.uint16, torch.int16) else 4
+    if ib == 4 and indices.dtype != torch.int32:
+        raise TypeError(f"indices must be uint16 or int32, got {indices.dtype}")
+    _abi.call("dic_encode_csr_tids", _ptr(indptr), _ptr(indices) if indices.numel() else None, ib, n, m,
+              row_begin, row_end, _ptr(tids), _ptr(status), _stream())
+
+
+def encode_status_finish(indptr: torch.Tensor, n: int, status: torch.Tensor) -> None:
+    _abi.call("dic_encode_status_finish", _ptr(indptr), n, _ptr(status), _stream())
+
+
+def tids_to_rows(tids: torch.Tensor, n: int, m: int) -> torch.Tensor:
+    """Bit-sliced tiles -> row bitmap uint64 [n][W] (the inverse transform)."""
+    rows = torch.empty((max(n, 1), words_for(m)), dtype=torch.uint64, device=tids.device)
+    _abi.call("dic_tids_to_rows", _ptr(tids), n, m, _ptr(rows), _stream())
+    return rows[:n]
+
+
 def rows_to_tids(rows: torch.Tensor, n: int, m: int) -> torch.Tensor:
     """Row bitmap -> the tiled bit-sliced layout (int32 words, see dic_b200.h)."""
     tids = torch.empty(max(tids_words(n, m), 1), dtype=torch.int32, device=rows.device)

@@ -86,6 +86,72 @@ def test_encode_reports_first_bad_item():
     assert st[1] == 3 and st[2] == 2
 
 
+@pytest.mark.parametrize("m,n,idx,slabs", [
+    (1, 700, "i32", 1), (64, 5000, "u16", 3), (300, 20000, "i32", 4), (1000, 9000, "u16", 2),
+    (1000, 513, "i32", 1), (3000, 2100, "u16", 2), (777, 1, "i32", 1)])
+def test_encode_straight_to_tiles(m, n, idx, slabs):
+    """dic_encode_csr_tids (slab by slab; shared-memory tiles, and the
+    global-atomic path at m=3000) == encode_csr + rows_to_tids, same status;
+    dic_tids_to_rows inverts it."""
+    rng = np.random.default_rng(m + n)
+    lens = rng.integers(0, min(m, 25) + 1, size=n)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(lens)
+    ids = rng.integers(0, m, size=int(indptr[-1]))  # duplicates on purpose
+    indices = ids.astype(np.uint16 if idx == "u16" else np.int32)
+    rows, st_ref = D.encode_csr(to_dev(indptr), to_dev(ids.astype(np.int32)), n, m)
+    want = D.rows_to_tids(rows, n, m).cpu().numpy()
+    dip, dix = to_dev(indptr), to_dev(indices)
+    tids = torch.full((max(D.tids_words(n, m), 1),), -1, dtype=torch.int32, device="cuda")
+    status = torch.empty(4, dtype=torch.int64, device="cuda")
+    D.encode_status_init(status)
+    rpt = D.tile_groups(m) * 32
+    per = -(-n // slabs)
+    step = -(-per // rpt) * rpt
+    for r0 in range(0, n, step):
+        D.encode_csr_tids(dip, dix, n, m, r0, min(n, r0 + step), tids, status)
+    D.encode_status_finish(dip, n, status)
+    assert np.array_equal(tids.cpu().numpy(), want)
+    assert np.array_equal(status.cpu().numpy(), st_ref.cpu().numpy())
+    assert np.array_equal(D.tids_to_rows(tids, n, m).cpu().numpy(), rows.cpu().numpy())
+
+
+def test_encode_tiles_first_bad_item_and_alignment():
+    indptr = np.array([0, 2, 2, 5, 6], dtype=np.int64)
+    indices = np.array([1, 3, 0, 70, 99, 64], dtype=np.int32)
+    tids = torch.empty(D.tids_words(4, 64), dtype=torch.int32, device="cuda")
+    status = torch.empty(4, dtype=torch.int64, device="cuda")
+    D.encode_status_init(status)
+    D.encode_csr_tids(to_dev(indptr), to_dev(indices), 4, 64, 0, 4, tids, status)
+    D.encode_status_finish(to_dev(indptr), 4, status)
+    st = status.cpu().numpy()
+    assert st[1] == 3 and st[2] == 2
+    from paper_1812_10959_b200._abi import DicError
+    with pytest.raises(DicError):  # slab start not on a tile boundary
+        D.encode_csr_tids(to_dev(indptr), to_dev(indices), 4, 64, 1, 4, tids, status)
+
+
+def test_from_csr_host_slabs_equal_device_path():
+    import paper_1812_10959_b200 as dic
+
+    rng = np.random.default_rng(11)
+    n, m = 50_000, 1000
+    lens = rng.integers(1, 30, size=n)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(lens)
+    ids = rng.integers(0, m, size=int(indptr[-1])).astype(np.uint16)
+    host = dic.BitDatabase.from_csr(torch.from_numpy(indptr).pin_memory(), torch.from_numpy(ids).pin_memory(), m,
+                                    slabs=7)
+    dev = dic.BitDatabase.from_csr(to_dev(indptr), to_dev(ids.astype(np.int32)), m)
+    assert torch.equal(host.device_tids(), dev.device_tids())
+    assert np.array_equal(host.rows, dev.rows)
+    with pytest.raises(dic.ItemOutOfRange) as ei:
+        bad = ids.copy()
+        bad[int(indptr[4321]) + 1] = 1000
+        dic.BitDatabase.from_csr(indptr, bad, m, slabs=3)
+    assert ei.value.item == 1000 and ei.value.line == 4321
+
+
 @pytest.mark.parametrize("m,n,first,last", [
     (64, 4000, 0, 3999), (64, 4000, 17, 2049), (130, 3001, 5, 5), (1000, 10000, 999, 8190),
     (512, 70000, 123, 69999), (33, 1, 0, 0)])

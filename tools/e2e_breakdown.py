@@ -45,8 +45,10 @@ def main() -> None:
     res["item_support_ms"], _ = timed(lambda: D.item_support(tids, cfg.n, cfg.m, 0, cfg.n - 1))
     res["dic_ms"], out = timed(lambda: run_engine(tids, cfg.n, cfg.m, params))
     res["frequent"] = len(out.frequent)
-    res["from_csr_total_ms"], _ = timed(lambda: dic.BitDatabase.from_csr(hip.cuda(non_blocking=True),
-                                                                      hix.cuda(non_blocking=True), cfg.m).device_tids())
+    res["from_csr_i32_ms"], _ = timed(lambda: dic.BitDatabase.from_csr(hip, hix, cfg.m).device_tids())
+    hix16 = torch.from_numpy(ix.astype("uint16")).pin_memory()
+    res["h2d_u16_ms"], _ = timed(lambda: (hip.cuda(non_blocking=True), hix16.cuda(non_blocking=True)))
+    res["from_csr_u16_ms"], _ = timed(lambda: dic.BitDatabase.from_csr(hip, hix16, cfg.m).device_tids())
     print(json.dumps(res))
 
 
