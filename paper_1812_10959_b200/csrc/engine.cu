@@ -628,6 +628,9 @@ struct HostRes {
     int device = -1;
     cudaEvent_t ev[kRing] = {};
     cudaStream_t cap = nullptr;
+    uint8_t* stage = nullptr;  // pinned staging for the result copies (grown on demand)
+    size_t stage_bytes = 0;
+    cudaGraphExec_t gx[2] = {nullptr, nullptr};  // stop graphs, updated in place by the next engine
 };
 
 struct dic_engine {
@@ -711,6 +714,9 @@ void free_host_res(HostRes& r) {
     for (int i = 0; i < kRing; ++i)
         if (r.ev[i]) cudaEventDestroy(r.ev[i]);
     if (r.ring) cudaFreeHost(r.ring);
+    if (r.stage) cudaFreeHost(r.stage);
+    for (cudaGraphExec_t& g : r.gx)
+        if (g) cudaGraphExecDestroy(g);
     if (r.cap) cudaStreamDestroy(r.cap);
     r = HostRes();
 }
@@ -1034,6 +1040,16 @@ int capture_graph(dic_engine* e, cudaGraphExec_t* gx, long long* nk, F body) {
     }
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
     if (*gx) {
+        // same topology (the usual case): update the executable graph's
+        // parameters in place, far cheaper than a new instantiation
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(*gx, g, &info) == cudaSuccess) {
+            cudaGraphDestroy(g);
+            *nk = n;
+            ++e->graphs_captured;
+            return DIC_OK;
+        }
+        cudaGetLastError();  // clear the update failure
         cudaGraphExecDestroy(*gx);
         *gx = nullptr;
     }
@@ -1091,6 +1107,9 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->ring_dev = e->hres.ring_dev;
     e->ev = e->hres.ev;
     e->cap_stream = e->hres.cap;
+    e->gx_count = e->hres.gx[0];  // stale until the first capture updates them
+    e->gx_ckpt = e->hres.gx[1];
+    e->hres.gx[0] = e->hres.gx[1] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
@@ -1114,8 +1133,8 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s); dfree(e->res_ids, s);
-    if (e->gx_count) cudaGraphExecDestroy(e->gx_count);
-    if (e->gx_ckpt) cudaGraphExecDestroy(e->gx_ckpt);
+    e->hres.gx[0] = e->gx_count;  // pooled with the host resources
+    e->hres.gx[1] = e->gx_ckpt;
     release_host_res(e->hres);  // the stream was synchronised above: no stop reads the ring any more
     delete e;
     return DIC_OK;
@@ -1528,44 +1547,68 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
     e->res_F = -1;  // ids consumed
     const int W = e->W;
     if (F == 0) return DIC_OK;
-    unsigned long long* dm = nullptr;
-    int32_t* dsz = nullptr;
-    int64_t* dsu = nullptr;
-    if ((rc = dalloc(&dm, F * W, e->s)) || (rc = dalloc(&dsz, F, e->s)) || (rc = dalloc(&dsu, F, e->s))) return rc;
+    // one device buffer and one pinned staging buffer: masks | sizes | supports
+    const size_t mb = (size_t)F * W * 8, sb = (size_t)F * 4, pb = (size_t)F * 8;
+    const size_t total = mb + pb + sb;
+    uint8_t* dbuf = nullptr;
+    if ((rc = dalloc(&dbuf, (int64_t)total, e->s))) return rc;
+    auto* dm = reinterpret_cast<unsigned long long*>(dbuf);
+    auto* dsu = reinterpret_cast<int64_t*>(dbuf + mb);
+    auto* dsz = reinterpret_cast<int32_t*>(dbuf + mb + pb);
     gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, W, e->res_ids, F, dm, dsz, dsu);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("gather_frequent_kernel");
-    std::vector<uint64_t> m1((size_t)F * W);
-    std::vector<int32_t> s1(F);
-    std::vector<int64_t> p1(F);
-    DIC_CUDA(cudaMemcpyAsync(m1.data(), dm, F * W * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s));
-    DIC_CUDA(cudaMemcpyAsync(s1.data(), dsz, F * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));
-    DIC_CUDA(cudaMemcpyAsync(p1.data(), dsu, F * sizeof(int64_t), cudaMemcpyDeviceToHost, e->s));
-    dfree(dm, e->s); dfree(dsz, e->s); dfree(dsu, e->s);
+    HostRes& hr = e->hres;
+    if (hr.stage_bytes < total) {
+        if (hr.stage) cudaFreeHost(hr.stage);
+        hr.stage = nullptr;
+        hr.stage_bytes = 0;
+        const size_t want = std::max(total, (size_t)1 << 20);
+        DIC_CUDA(cudaHostAlloc((void**)&hr.stage, want, cudaHostAllocDefault));
+        hr.stage_bytes = want;
+    }
+    DIC_CUDA(cudaMemcpyAsync(hr.stage, dbuf, total, cudaMemcpyDeviceToHost, e->s));
+    dfree(dbuf, e->s);
     DIC_CUDA(cudaStreamSynchronize(e->s));
+    const uint64_t* m1 = reinterpret_cast<const uint64_t*>(hr.stage);
+    const int64_t* p1 = reinterpret_cast<const int64_t*>(hr.stage + mb);
+    const int32_t* s1 = reinterpret_cast<const int32_t*>(hr.stage + mb + pb);
     // canonical order of the reference's result (engine.py:446-455): by size,
-    // then by the mask as an integer, i.e. most significant word first.  Keys
-    // are byte strings (size, then the words MSW first, all big-endian), so
-    // one memcmp decides each comparison.
-    const size_t kb = 4 + 8 * (size_t)W;
-    std::vector<uint8_t> keys((size_t)F * kb);
+    // then by the mask as an integer.  For masks of equal size that order is
+    // the lexicographic order of their item ids listed from the highest down,
+    // so each key is (size, item ids descending, 4 x 16 bits per word) and a
+    // comparison touches ceil(k/4) + 1 words.
+    int kmax = 1;
+    for (int64_t i = 0; i < F; ++i) kmax = std::max(kmax, (int)s1[i]);
+    const int KW = 1 + (kmax + 3) / 4;
+    std::vector<uint64_t> keys((size_t)F * KW, 0);
     for (int64_t i = 0; i < F; ++i) {
-        uint8_t* k = keys.data() + (size_t)i * kb;
-        const uint32_t sz = (uint32_t)s1[i];
-        k[0] = (uint8_t)(sz >> 24); k[1] = (uint8_t)(sz >> 16); k[2] = (uint8_t)(sz >> 8); k[3] = (uint8_t)sz;
-        for (int w = 0; w < W; ++w) {
-            const uint64_t x = __builtin_bswap64(m1[(size_t)i * W + (W - 1 - w)]);
-            memcpy(k + 4 + 8 * w, &x, 8);
+        uint64_t* k = keys.data() + (size_t)i * KW;
+        k[0] = (uint64_t)(uint32_t)s1[i];
+        int j = 0;
+        for (int w = W - 1; w >= 0; --w) {
+            uint64_t x = m1[(size_t)i * W + w];
+            while (x) {
+                const int b = 63 - __builtin_clzll(x);
+                x &= ~(1ull << b);
+                k[1 + j / 4] |= (uint64_t)(uint16_t)(w * 64 + b) << (48 - 16 * (j % 4));
+                ++j;
+            }
         }
     }
     std::vector<int64_t> idx(F);
     std::iota(idx.begin(), idx.end(), 0);
-    const uint8_t* kp = keys.data();
-    std::sort(idx.begin(), idx.end(),
-              [&](int64_t a, int64_t b) { return memcmp(kp + (size_t)a * kb, kp + (size_t)b * kb, kb) < 0; });
+    const uint64_t* kp = keys.data();
+    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+        const uint64_t* x = kp + (size_t)a * KW;
+        const uint64_t* y = kp + (size_t)b * KW;
+        for (int q = 0; q < KW; ++q)
+            if (x[q] != y[q]) return x[q] < y[q];
+        return false;
+    });
     for (int64_t i = 0; i < F; ++i) {
         const int64_t j = idx[i];
-        memcpy(masks_host + (size_t)i * W, m1.data() + (size_t)j * W, W * sizeof(uint64_t));
+        memcpy(masks_host + (size_t)i * W, m1 + (size_t)j * W, W * sizeof(uint64_t));
         sizes_host[i] = s1[j];
         supports_host[i] = p1[j];
     }
