@@ -173,6 +173,19 @@ int dic_candidate_admission(const uint64_t* src_masks, int64_t S,
                             const uint64_t* box_masks, int64_t B,
                             uint8_t* admit, void* stream);
 
+/* Pattern containment (DicMiner.transform, estimator.py:90-99) ------------
+ * P patterns as concatenated ascending item ids items[offs[p] .. offs[p+1])
+ * (device uint16 / int64 [P+1]; an empty pattern is in every row, one with an
+ * item >= m in none).  dic_containment writes the row-major bool matrix
+ * out[n][P] (uint8 0/1); dic_containment_packed the bit matrix out[G][P]
+ * (uint32, G = ceil(n/32)): bit r of word (g, p) = row 32g + r contains p. */
+int dic_containment(const uint32_t* tids, int64_t n, int32_t m,
+                    const uint16_t* items, const int64_t* offs, int64_t P,
+                    uint8_t* out, void* stream);
+int dic_containment_packed(const uint32_t* tids, int64_t n, int32_t m,
+                           const uint16_t* items, const int64_t* offs, int64_t P,
+                           uint32_t* out, void* stream);
+
 /* Device-resident DIC engine ---------------------------------------------
  * The checkpoint loop of _run (engine.py:398-458) with the catalog
  * (itemsets.py:88-136) held on the device as structure-of-arrays plus a
@@ -305,6 +318,28 @@ int dic_csr_info(const dic_csr* c, int64_t* n, int64_t* nnz);
 /* host arrays: indptr[n+1], indices[nnz]                                  */
 int dic_csr_export(const dic_csr* c, int64_t* indptr, int32_t* indices);
 void dic_csr_free(dic_csr* c);
+
+/* Transaction text format (datasets.py:150-209) --------------------------
+ * Parse a whole file image into CSR (threads workers).  On a bad token the
+ * call returns DIC_EDATA with st->kind 1 (not an integer) or 2 (outside
+ * [0, max_item)), st->line its 1-based line (blank and comment lines
+ * counted, as the reference's enumerate(fh, 1)), st->offset / length the
+ * token's bytes; kind 3 = a non-ASCII byte (the caller decodes in Python).
+ * On success st->line = lines read.                                        */
+typedef struct dic_parse_status {
+    int32_t kind;
+    int32_t reserved;
+    int64_t line;
+    int64_t offset;
+    int64_t length;
+} dic_parse_status;
+int dic_parse_transactions(const char* text, int64_t len, int32_t max_item,
+                           int32_t threads, dic_csr** out, dic_parse_status* st);
+/* Canonical text of rows [n][W] (ascending ids, one newline per row) in a malloc'd
+ * buffer the caller releases with dic_free_buffer.                        */
+int dic_format_transactions(const uint64_t* rows, int64_t n, int32_t W,
+                            int32_t threads, char** out, int64_t* len);
+void dic_free_buffer(char* p);
 /* cfg5: row bitmap rows[n][W] of i.i.d. Bernoulli(p) bits, generated on the
  * device; and C candidates (host arrays) with k ~ U{kmin..kmax} items drawn
  * uniformly without replacement: cand_k[C], cand_items[C][kmax] ascending,

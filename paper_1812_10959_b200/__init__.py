@@ -19,6 +19,9 @@ from .miner import mine_parallel, mine_serial, run_engine
 from .phases import (FrequentItemset, MiningResult, MiningStats, check_full_pass, count_support_interval,
                      first_pass, make_candidates, prune)
 from .sharding import ShardPlan
+from .datasets import (LoadReport, item_frequencies, load_bitdb, load_transactions, load_transactions_with_report,
+                       parse_transactions, save_bitdb, save_transactions, sniff_format)
+from .estimator import DicMiner, as_bit_database, resolve_thread_count
 
 __version__ = "0.1.0"
 
@@ -30,4 +33,7 @@ __all__ = [
     "count_support_interval", "database_from_transactions", "default_interval", "encode_transaction",
     "first_pass", "immediate_subsets", "items_of", "join", "make_candidates", "mine_parallel", "mine_serial",
     "popcounts", "prune", "run_engine",
+    "DicMiner", "LoadReport", "as_bit_database", "item_frequencies", "load_bitdb", "load_transactions",
+    "load_transactions_with_report", "parse_transactions", "resolve_thread_count", "save_bitdb",
+    "save_transactions", "sniff_format",
 ]

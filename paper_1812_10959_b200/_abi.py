@@ -31,6 +31,10 @@ class StopStatus(C.Structure):
     ]
 
 
+class ParseStatus(C.Structure):
+    _fields_ = [("kind", i32), ("reserved", i32), ("line", i64), ("offset", i64), ("length", i64)]
+
+
 class RunStats(C.Structure):
     _fields_ = [
         ("stops", i64),
@@ -70,6 +74,8 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_delta": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_checkpoint": (C.c_int, [vp, P(StopStatus)]),
     "dic_engine_issue_count": (C.c_int, [vp, i64, i64]),
+    "dic_containment": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
+    "dic_containment_packed": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
     "dic_encode_status_init": (C.c_int, [vp, vp]),
     "dic_encode_csr_tids": (C.c_int, [vp, vp, i32, i64, i32, i64, i64, vp, vp, vp]),
     "dic_encode_status_finish": (C.c_int, [vp, i64, vp, vp]),
@@ -89,6 +95,9 @@ SIGNATURES: dict[str, tuple] = {
     "dic_csr_info": (C.c_int, [vp, P(i64), P(i64)]),
     "dic_csr_export": (C.c_int, [vp, vp, vp]),
     "dic_csr_free": (None, [vp]),
+    "dic_parse_transactions": (C.c_int, [vp, i64, i32, i32, P(vp), P(ParseStatus)]),
+    "dic_format_transactions": (C.c_int, [vp, i64, i32, i32, P(vp), P(i64)]),
+    "dic_free_buffer": (None, [vp]),
     "dic_synth_bernoulli_rows": (C.c_int, [i64, i32, dbl, u64, vp, vp]),
     "dic_synth_candidates": (C.c_int, [i64, i32, i32, i32, u64, vp, vp]),
     "dic_probe_int_pipe": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, vp, P(dbl), P(C.c_float), vp]),

@@ -25,8 +25,8 @@ NVCC_FLAGS = ARCH + [
 ]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function"]
 
-CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "probe.cu"]
-CPP_SOURCES = ["synth.cpp"]
+CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "containment.cu", "probe.cu"]
+CPP_SOURCES = ["synth.cpp", "textio.cpp"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -38,7 +38,7 @@ def _run(cmd: list[str]) -> None:
 def _stale(obj: Path, src: Path) -> bool:
     if not obj.exists():
         return True
-    deps = [src, *CSRC.glob("*.cuh"), PKG.parent / "include" / "dic_b200.h", Path(__file__)]
+    deps = [src, *CSRC.glob("*.cuh"), *CSRC.glob("*.hpp"), PKG.parent / "include" / "dic_b200.h", Path(__file__)]
     t = obj.stat().st_mtime
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 

@@ -80,7 +80,7 @@ class BitDatabase:
 
     # -- construction on the device --------------------------------------
     @classmethod
-    def from_csr(cls, indptr, indices, m: int, *, slabs: int = 8) -> "BitDatabase":
+    def from_csr(cls, indptr, indices, m: int, *, slabs: int = 8, return_dedup: bool = False):
         """Encode CSR item lists (host or device arrays) on the GPU, straight
         into the bit-sliced tiles the count kernels stream.
 
@@ -90,7 +90,8 @@ class BitDatabase:
         it lands (pinned host tensors make the copies asynchronous).
         Duplicate ids collapse; an id outside [0, m) raises
         ItemOutOfRange(item, line=row) for the first one in row-major order,
-        as encode_transaction would (bitops.py:24-37)."""
+        as encode_transaction would (bitops.py:24-37).  ``return_dedup``:
+        also return the number of duplicate ids dropped (LoadReport)."""
         import torch
 
         from . import device as D
@@ -141,7 +142,8 @@ class BitDatabase:
         st = status.cpu().numpy()
         if st[1] >= 0:
             raise ItemOutOfRange(int(dix[int(st[1])].item()), line=int(st[2]), universe=m)
-        return cls.from_device_tids(tids, n, m)
+        db = cls.from_device_tids(tids, n, m)
+        return (db, int(st[0])) if return_dedup else db
 
     @classmethod
     def from_device_tids(cls, tids, n: int, m: int) -> "BitDatabase":

@@ -10,6 +10,7 @@
 // from a stream keyed by the seed alone.  Output is therefore identical for
 // any thread count and for any split of the rows into ranges — which is what
 // lets each rank of a sharded run generate only its own slices.
+#include "csr.hpp"
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -90,11 +91,6 @@ struct Ranges {
 
 }  // namespace
 
-struct dic_csr {
-    int64_t n = 0;
-    std::vector<int64_t> indptr;
-    std::vector<int32_t> indices;
-};
 
 namespace {
 

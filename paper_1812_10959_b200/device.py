@@ -80,6 +80,36 @@ def tids_to_rows(tids: torch.Tensor, n: int, m: int) -> torch.Tensor:
     return rows[:n]
 
 
+def patterns_to_device(masks) -> tuple[torch.Tensor, torch.Tensor]:
+    """Python-int masks -> (uint16 items, int64 offsets[P+1]) on the device,
+    each pattern's ids ascending (the containment kernel's input)."""
+    from .bits import items_of
+
+    lens, flat = [], []
+    for mk in masks:
+        its = list(items_of(int(mk)))
+        lens.append(len(its))
+        flat.extend(its)
+    offs = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    items = np.asarray(flat if flat else [0], dtype=np.uint16)
+    return torch.from_numpy(items).cuda(), torch.from_numpy(offs).cuda()
+
+
+def containment(tids: torch.Tensor, n: int, m: int, items: torch.Tensor, offs: torch.Tensor,
+                packed: bool = False) -> torch.Tensor:
+    """Pattern containment over the bit-sliced rows: bool [n][P] (or the
+    packed uint32 [ceil(n/32)][P] bit matrix)."""
+    P = int(offs.numel()) - 1
+    if packed:
+        out = torch.empty(((n + 31) // 32, max(P, 1)), dtype=torch.int32, device=tids.device)
+        _abi.call("dic_containment_packed", _ptr(tids), n, m, _ptr(items), _ptr(offs), P, _ptr(out), _stream())
+        return out[:, :P]
+    out = torch.empty((n, max(P, 1)), dtype=torch.uint8, device=tids.device)
+    _abi.call("dic_containment", _ptr(tids), n, m, _ptr(items), _ptr(offs), P, _ptr(out), _stream())
+    return out[:, :P].view(torch.bool)
+
+
 def rows_to_tids(rows: torch.Tensor, n: int, m: int) -> torch.Tensor:
     """Row bitmap -> the tiled bit-sliced layout (int32 words, see dic_b200.h)."""
     tids = torch.empty(max(tids_words(n, m), 1), dtype=torch.int32, device=rows.device)
