@@ -9,6 +9,7 @@ exists:
                   reference loader's masks and LoadReport, or its error
                   (type, line, token/item); binary caches written by the
                   reference's save_bitdb (hex) with their masks
+                  and the reference's seeded generator (sha256 of the masks)
   estimator.json  DicMiner fit / transform / feature names on the reference
                   tests' examples and a few seeded random inputs
 
@@ -117,10 +118,27 @@ def estimator_cases() -> list[dict]:
     return out
 
 
+SYNTH_SPECS = [(500, 64, 40.0, 42, 0.9), (2000, 20, 5.0, 7, 0.8), (100, 10, 3.5, 1, 0.9), (300, 64, 12.25, 3, 1.0),
+               (40000, 64, 12.0, 7, 0.9), (17, 1, 1.0, 5, 0.5)]
+
+
+def synthetic_cases() -> list[dict]:
+    import hashlib
+
+    out = []
+    for n, m, avg, seed, skew in SYNTH_SPECS:
+        db = ref_ds.generate_synthetic(ref_ds.DatasetSpec(n=n, m=m, avg_len=avg, seed=seed, skew=skew))
+        raw = np.asarray(db.masks, dtype="<u8").tobytes()
+        out.append({"n": n, "m": m, "avg_len": avg, "seed": seed, "skew": skew, "db_m": db.m,
+                    "sha256": hashlib.sha256(raw).hexdigest(), "head": [int(x) for x in db.masks[:5]]})
+    return out
+
+
 def main() -> None:
     rng = random.Random(0x10AD)
     cases = [text_case(t) for t in TEXT_CASES] + [text_case(random_text(rng)) for _ in range(40)]
-    (HERE / "io.json").write_text(json.dumps({"text": cases, "binary": binary_cases()}, indent=0))
+    (HERE / "io.json").write_text(json.dumps({"text": cases, "binary": binary_cases(),
+                                              "synthetic": synthetic_cases()}, indent=0))
     (HERE / "estimator.json").write_text(json.dumps(estimator_cases(), indent=0))
     print("wrote io.json, estimator.json")
 

@@ -142,3 +142,25 @@ def test_binary_cache_wide_and_errors(tmp_path):
     with pytest.raises(dic.FormatError, match="beyond declared universe"):
         ds.load_bitdb(p)
     assert ds.sniff_format(tmp_path / "x.bin") == "binary" and ds.sniff_format(tmp_path / "x.txt") == "text"
+
+
+@pytest.mark.parametrize("case", GOLD["synthetic"], ids=lambda c: f"{c['n']}x{c['m']}s{c['seed']}")
+def test_synthetic_generator_is_the_reference_stream(case):
+    import hashlib
+
+    from paper_1812_10959_b200.synthetic import DatasetSpec, generate_synthetic
+
+    db = generate_synthetic(DatasetSpec(n=case["n"], m=case["m"], avg_len=case["avg_len"], seed=case["seed"],
+                                        skew=case["skew"]))
+    masks = np.asarray(db.masks, dtype="<u8")
+    assert db.m == case["db_m"] and masks[:5].tolist() == case["head"]
+    assert hashlib.sha256(masks.tobytes()).hexdigest() == case["sha256"]
+
+
+def test_synthetic_spec_validation():
+    from paper_1812_10959_b200.synthetic import DatasetSpec, generate_synthetic
+
+    for bad in [DatasetSpec(0, 8, 2, 1), DatasetSpec(5, 65, 2, 1), DatasetSpec(5, 8, 0, 1), DatasetSpec(5, 8, 9, 1),
+                DatasetSpec(5, 8, 2, 1, skew=0.0)]:
+        with pytest.raises(dic.SpecError):
+            generate_synthetic(bad)
