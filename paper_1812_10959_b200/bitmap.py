@@ -222,7 +222,7 @@ class BitDatabase:
             if self._rows is None and self._dev_tids is not None:
                 self._dev_rows = D.tids_to_rows(self._dev_tids, self._n, self._m)
             else:
-                self._dev_rows = torch.from_numpy(np.ascontiguousarray(self._host_rows())).cuda()
+                self._dev_rows = torch.from_numpy(np.array(self._host_rows(), dtype=np.uint64)).cuda()
         return self._dev_rows
 
     def device_tids(self):
