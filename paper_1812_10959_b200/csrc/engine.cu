@@ -72,6 +72,15 @@ __host__ __device__ inline uint64_t zob(uint32_t item) {
 
 constexpr int32_t kEmpty = -1;
 constexpr int32_t kTempFlag = 0x40000000;
+// Hash-index entries: (upper 32 bits of the mask's hash) << 32 | record id, so
+// a probe reads one word and only a tag match touches the record's mask.
+typedef unsigned long long hent_t;
+constexpr hent_t kEmptyEnt = ~0ull;
+__host__ __device__ __forceinline__ hent_t hent(uint64_t h, int32_t id) {
+    return ((hent_t)(uint32_t)(h >> 32) << 32) | (uint32_t)id;
+}
+__host__ __device__ __forceinline__ int32_t hent_id(hent_t x) { return (int32_t)(uint32_t)x; }
+__host__ __device__ __forceinline__ uint32_t hent_tag(hent_t x) { return (uint32_t)(x >> 32); }
 
 // Status words (device, one contiguous u64 array).
 enum : int {
@@ -124,13 +133,43 @@ __device__ __forceinline__ bool mask_eq(const unsigned long long* a, const MaskV
     return true;
 }
 
-__device__ __forceinline__ int32_t ht_lookup(const int32_t* __restrict__ ht, uint64_t hmask, const Records& R,
+__device__ __forceinline__ int32_t ht_lookup(const hent_t* __restrict__ ht, uint64_t hmask, const Records& R,
                                              int W, uint64_t h, const MaskView& v) {
     uint64_t slot = mix64(h) & hmask;
+    const uint32_t tag = (uint32_t)(h >> 32);
     while (true) {
-        int32_t e = ht[slot];
+        const hent_t x = ht[slot];
+        const int32_t e = hent_id(x);
         if (e == kEmpty) return -1;
-        if (R.hash[e] == h && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
+        if (hent_tag(x) == tag && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
+        slot = (slot + 1) & hmask;
+    }
+}
+
+// Lookup of the set its[0..k) + {add} - {drop} (add/drop = -1: none) of
+// `size` items.  A tag match is confirmed without reading the whole W-word
+// mask: a record of the same size holding every item of the set IS the set.
+// The per-item bit loads are independent, so a confirmation costs one memory
+// latency instead of W dependent word compares.
+constexpr int kEvalK = 24;  // frontier itemsets up to this size take the item-list path
+__device__ __forceinline__ int32_t ht_find_items(const hent_t* __restrict__ ht, uint64_t hmask, const Records& R,
+                                                 int W, uint64_t h, const int* its, int k, int add, int drop,
+                                                 int size) {
+    uint64_t slot = mix64(h) & hmask;
+    const uint32_t tag = (uint32_t)(h >> 32);
+    while (true) {
+        const hent_t x = ht[slot];
+        const int32_t e = hent_id(x);
+        if (e == kEmpty) return -1;
+        if (hent_tag(x) == tag && R.size[e] == size) {
+            const unsigned long long* rm = R.mask + (int64_t)e * W;
+            bool ok = add < 0 || ((rm[add >> 6] >> (add & 63)) & 1ull);
+            for (int q = 0; q < k; ++q) {
+                const int it = its[q];
+                if (it != drop) ok &= ((rm[it >> 6] >> (it & 63)) & 1ull) != 0;
+            }
+            if (ok) return e;
+        }
         slot = (slot + 1) & hmask;
     }
 }
@@ -138,18 +177,19 @@ __device__ __forceinline__ int32_t ht_lookup(const int32_t* __restrict__ ht, uin
 // ---------------------------------------------------------------------------
 // seeding / rehash
 // ---------------------------------------------------------------------------
-__global__ void ht_clear_kernel(int32_t* ht, int64_t cap) {
+__global__ void ht_clear_kernel(hent_t* ht, int64_t cap) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
-        ht[i] = kEmpty;
+        ht[i] = kEmptyEnt;
 }
 
 // Insert records [0, *nrec) — the device count, so a rebuild enqueued behind
 // in-flight stops sees their records too.
-__global__ void ht_insert_records_kernel(int32_t* ht, uint64_t hmask, Records R, const unsigned long long* nrec) {
+__global__ void ht_insert_records_kernel(hent_t* ht, uint64_t hmask, Records R, const unsigned long long* nrec) {
     const int64_t n = (int64_t)*nrec;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t slot = mix64(R.hash[r]) & hmask;
-        while (atomicCAS(ht + slot, kEmpty, (int32_t)r) != kEmpty) slot = (slot + 1) & hmask;
+        const uint64_t h = R.hash[r];
+        uint64_t slot = mix64(h) & hmask;
+        while (atomicCAS(ht + slot, kEmptyEnt, hent(h, (int32_t)r)) != kEmptyEnt) slot = (slot + 1) & hmask;
     }
 }
 
@@ -364,7 +404,7 @@ __device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap
                                const int64_t* __restrict__ bcap);
 
 __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, const int32_t* __restrict__ level1,
-                                       int64_t L, int W, Records R, const int32_t* __restrict__ ht, uint64_t hmask,
+                                       int64_t L, int W, Records R, const hent_t* __restrict__ ht, uint64_t hmask,
                                        unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
                                        int32_t* __restrict__ tmp_size, int64_t tmp_cap,
                                        unsigned long long* __restrict__ stat, int KS, int64_t rec_cap, int64_t hcap,
@@ -381,8 +421,31 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
         if ((sm[l >> 6] >> (l & 63)) & 1ull) continue;  // cand == base
         const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
         const MaskView cand{sm, l, -1};
-        if (ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
+        const int ks = R.size[src];
         bool ok = true;
+        if (ks < kEvalK && W <= 16) {
+            // item-list path: src's words loaded together, its ids extracted once
+            unsigned long long wv[16];
+#pragma unroll
+            for (int w = 0; w < 16; ++w) wv[w] = w < W ? sm[w] : 0ull;
+            int its[kEvalK];
+            int k = 0;
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+                unsigned long long x = wv[w];
+                while (x && k < kEvalK) {
+                    its[k++] = w * 64 + __ffsll((long long)x) - 1;
+                    x &= x - 1;
+                }
+            }
+            if (ht_find_items(ht, hmask, R, W, hc, its, k, l, -1, k + 1) >= 0) continue;  // already known
+            for (int q = 0; q < k && ok; ++q) {
+                const int d = its[q];
+                const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, k, l, d, k);
+                ok = e >= 0 && is_box(R.shape[e]);
+            }
+        } else {
+        if (ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
         for (int w = 0; w < W && ok; ++w) {
             unsigned long long x = cand.word(w);
             while (x) {
@@ -396,6 +459,7 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                     break;
                 }
             }
+        }
         }
         if (!ok) continue;
         const unsigned long long pos = atomicAdd(&stat[S_NADM], 1ull);
@@ -455,7 +519,7 @@ __device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap
 // read through L2 (__ldcg): L1 is not coherent within a launch.
 __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
                                      const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
-                                     Records R, int32_t* ht, uint64_t hmask, unsigned long long* stat, int KS,
+                                     Records R, hent_t* ht, uint64_t hmask, unsigned long long* stat, int KS,
                                      int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
     if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t na = (int64_t)stat[S_NADM];
@@ -465,8 +529,8 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
         const unsigned long long* mk = tmp_mask + t * W;
         uint64_t slot = mix64(h) & hmask;
         while (true) {
-            const int32_t prev = atomicCAS(ht + slot, kEmpty, kTempFlag | (int32_t)t);
-            if (prev == kEmpty) {
+            const hent_t pe = atomicCAS(ht + slot, kEmptyEnt, hent(h, kTempFlag | (int32_t)t));
+            if (pe == kEmptyEnt) {
                 const int64_t r = (int64_t)atomicAdd(&stat[S_NREC], 1ull);
                 atomicAdd(&stat[S_NINS], 1ull);
                 const int sz = tmp_size[t];
@@ -488,16 +552,16 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
                     }
                 }
                 __threadfence();
-                atomicExch(ht + slot, (int32_t)r);
+                atomicExch(ht + slot, hent(h, (int32_t)r));
                 break;
             }
-            bool same;
-            if (prev & kTempFlag) {
+            const int32_t prev = hent_id(pe);
+            bool same = hent_tag(pe) == (uint32_t)(h >> 32);
+            if (same && (prev & kTempFlag)) {
                 const int64_t o = prev & ~kTempFlag;
                 same = tmp_hash[o] == h;
                 for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
-            } else {
-                same = __ldcg(R.hash + prev) == h;
+            } else if (same) {
                 for (int w = 0; same && w < W; ++w) same = __ldcg(R.mask + (int64_t)prev * W + w) == mk[w];
             }
             if (same) break;  // duplicate of a join admitted by another thread
@@ -603,7 +667,7 @@ struct Bucket {
 // Everything a captured stop graph bakes in: a change forces a re-capture.
 struct GraphKey {
     Records R;
-    const int32_t* ht;
+    const hent_t* ht;
     int64_t hcap;
     int64_t kuse;
     const unsigned long long* delta;
@@ -643,7 +707,7 @@ struct dic_engine {
 
     Records R;
     int64_t nrec = 0;  // at the last polled stop
-    int32_t* ht = nullptr;
+    hent_t* ht = nullptr;  // hash index (entries: tag << 32 | record id)
     int64_t hcap = 0;
 
     std::vector<Bucket> buckets;  // index = itemset size
