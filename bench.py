@@ -325,9 +325,14 @@ def main() -> None:
     tids = db.device_tids()
     torch.cuda.synchronize()
 
+    # N > 1: the library's own NCCL communicator, the whole loop native
+    # (DIC_COLLECTIVE=torch: torch.distributed all_reduce from the Python loop)
+    collective = None if world == 1 else ("native" if os.environ.get("DIC_COLLECTIVE", "native") == "native"
+                                          else True)
+
     def one_run(trace=None, count_events=None):
         return run_engine(tids, n_local, cfg.m, params, plan=plan if world > 1 else None, group=group,
-                          trace=trace, count_events=count_events)
+                          trace=trace, count_events=count_events, collective=collective)
 
     if args.profile:
         one_run()
@@ -428,7 +433,7 @@ def main() -> None:
             dbe = dic.BitDatabase.from_csr(h_indptr, h_indices,
                                            cfg.m)
             out = run_engine(dbe.device_tids(), n_local, cfg.m, params, plan=plan if world > 1 else None,
-                             group=group)
+                             group=group, collective=collective)
             del dbe
         f1.record(stream)
         torch.cuda.synchronize()

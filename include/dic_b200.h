@@ -285,6 +285,19 @@ int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_t* llast,
                    const int64_t* rows, int64_t stop_max, int32_t depth,
                    dic_run_stats* out, float* count_ms, int64_t* dashed,
                    int64_t max_stops);
+/* Multi-GPU without a Python framework in the loop: an NCCL communicator
+ * built here (rank 0 draws the 128-byte id, every rank passes it to
+ * dic_nccl_comm_init, which blocks until all ranks joined) and attached to the
+ * engine BEFORE dic_engine_item_counts.  The engine then sum-allreduces the
+ * item counts and, per stop between the count and checkpoint halves, the
+ * delta buffer (and the pair triangle while it is dense) on its own stream —
+ * the per-checkpoint int64 allreduce of SURVEY §8(e), also inside
+ * dic_engine_run.                                                          */
+int dic_nccl_unique_id(uint8_t* out /* [128] */);
+int dic_nccl_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, void** comm);
+int dic_nccl_comm_destroy(void* comm);
+int dic_engine_set_comm(dic_engine* e, void* comm);
+
 /* Results: number of SOLID_BOX records, then copy them out to HOST arrays
  * masks[F][W] (uint64), sizes[F], supports[F] in the reference's canonical
  * order (engine.py:446-455): by size, then mask as an integer (MSW first).

@@ -74,6 +74,10 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_delta": (C.c_int, [vp, P(vp), P(i64)]),
     "dic_engine_checkpoint": (C.c_int, [vp, P(StopStatus)]),
     "dic_engine_issue_count": (C.c_int, [vp, i64, i64]),
+    "dic_nccl_unique_id": (C.c_int, [vp]),
+    "dic_nccl_comm_init": (C.c_int, [vp, i32, i32, P(vp)]),
+    "dic_nccl_comm_destroy": (C.c_int, [vp]),
+    "dic_engine_set_comm": (C.c_int, [vp, vp]),
     "dic_containment": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
     "dic_containment_packed": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
     "dic_encode_status_init": (C.c_int, [vp, vp]),

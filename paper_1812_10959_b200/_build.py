@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
                     print(" ".join(cmd), file=sys.stderr)
     if force or jobs or not LIB.exists():
         tmp = LIB.with_suffix(".so.tmp")
-        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", "-lnccl"])
         os.replace(tmp, LIB)
     return LIB
 

@@ -39,6 +39,8 @@
 // engine omits it; the API-level prune on host catalogs keeps it.
 #include "common.cuh"
 
+#include <nccl.h>
+
 #include <algorithm>
 #include <chrono>
 #include <deque>
@@ -682,6 +684,8 @@ struct GraphKey {
     bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
+static int nccl_fail(ncclResult_t r, const char* what);
+
 // Host-side resources of an engine (the mapped status ring, its events, the
 // capture stream) are pooled per process: creating them costs ~1-2 ms
 // (page pinning), more than a small mining run's whole checkpoint loop.
@@ -767,6 +771,12 @@ struct dic_engine {
     int32_t* res_ids = nullptr;          // result collection (dic_engine_num_frequent)
     int64_t res_cap = 0, res_F = -1;
     HostRes hres;
+
+    // multi-GPU: per-stop sum-allreduce of the count deltas (and of the pair
+    // triangle while it is dense) on the engine's stream, between the count
+    // and checkpoint halves
+    ncclComm_t comm = nullptr;
+    bool tri_live = true;                // host view: the pair triangle may still be dense
 };
 
 namespace {
@@ -1209,9 +1219,50 @@ extern "C" int dic_engine_words(dic_engine* e) { return e ? e->W : DIC_EINVAL; }
 extern "C" int dic_engine_item_counts(dic_engine* e, int64_t* counts) {
     DIC_REQUIRE(e && counts, "dic_engine_item_counts: null argument");
     DIC_CUDA(cudaMemsetAsync(counts, 0, (size_t)e->m * sizeof(int64_t), e->s));
-    if (e->n_local > 0)
-        return item_support_launch(e->tids, e->n_local, e->m, 0, e->n_local - 1,
-                                   reinterpret_cast<unsigned long long*>(counts), e->s);
+    int rc;
+    if (e->n_local > 0 && (rc = item_support_launch(e->tids, e->n_local, e->m, 0, e->n_local - 1,
+                                                     reinterpret_cast<unsigned long long*>(counts), e->s)))
+        return rc;
+    if (e->comm) {  // first_pass over the global database
+        const ncclResult_t r = ncclAllReduce(counts, counts, (size_t)e->m, ncclInt64, ncclSum, e->comm, e->s);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(item counts)");
+    }
+    return DIC_OK;
+}
+
+extern "C" int dic_nccl_unique_id(uint8_t* out) {
+    DIC_REQUIRE(out, "dic_nccl_unique_id: null buffer");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return DIC_OK;
+}
+
+extern "C" int dic_nccl_comm_init(const uint8_t* id_bytes, int32_t nranks, int32_t rank, void** comm) {
+    DIC_REQUIRE(id_bytes && comm && nranks >= 1 && 0 <= rank && rank < nranks, "dic_nccl_comm_init: bad arguments");
+    ncclUniqueId id;
+    memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&c, nranks, id, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+    *comm = c;
+    return DIC_OK;
+}
+
+extern "C" int dic_nccl_comm_destroy(void* comm) {
+    if (!comm) return DIC_OK;
+    const ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
+    return r == ncclSuccess ? DIC_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+extern "C" int dic_engine_set_comm(dic_engine* e, void* comm) {
+    DIC_REQUIRE(e, "dic_engine_set_comm: null engine");
+    if (e->seeded) {
+        set_error("dic_engine_set_comm: set the communicator before dic_engine_item_counts / seed");
+        return DIC_ESTATE;
+    }
+    e->comm = static_cast<ncclComm_t>(comm);
     return DIC_OK;
 }
 
@@ -1377,6 +1428,25 @@ extern "C" int dic_engine_pair_counts(dic_engine* e, void** ptr, int64_t* len) {
     return DIC_OK;
 }
 
+static int nccl_fail(ncclResult_t r, const char* what) {
+    set_error("%s: %s", what, ncclGetErrorString(r));
+    return DIC_ECUDA;
+}
+
+// The stop's cross-rank reduction (sharded engines): every rank enqueues the
+// same calls in the same order (the state machine and hence slot_cap /
+// tri_live are replicated), so the collectives always match.
+static int reduce_stop(dic_engine* e) {
+    if (!e->comm) return DIC_OK;
+    ncclResult_t r = ncclAllReduce(e->delta, e->delta, (size_t)e->slot_cap, ncclUint64, ncclSum, e->comm, e->s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(delta)");
+    if (e->tri && e->tri_live) {
+        r = ncclAllReduce(e->tri, e->tri, (size_t)e->tri_len, ncclUint64, ncclSum, e->comm, e->s);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(pair triangle)");
+    }
+    return DIC_OK;
+}
+
 extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     DIC_REQUIRE(e && seq, "dic_engine_issue_checkpoint: null argument");
     if (!e->counted) { set_error("dic_engine_issue_checkpoint: no count issued"); return DIC_ESTATE; }
@@ -1386,6 +1456,7 @@ extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     }
     e->counted = false;
     int rc;
+    if ((rc = reduce_stop(e))) return rc;
     const GraphKey k = graph_key(e, false);
     if (!e->gx_ckpt || !(k == e->key_ckpt)) {
         if ((rc = capture_graph(e, &e->gx_ckpt, &e->nk_ckpt, [&](cudaStream_t cs) { return launch_checkpoint(e, cs); })))
@@ -1473,6 +1544,9 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         return DIC_ESTATE;
     }
     for (int k = 0; k < ku; ++k) e->buckets[k].n = (int64_t)h[S_HEAD + 3 * k + 2];
+    // the pair bucket only shrinks after seeding: once the device's dense test
+    // (2*bn[2] >= tri_len) fails it fails for every later stop
+    if (e->tri && ku > 2 && 2 * (int64_t)h[S_HEAD + 3 * 2 + 2] < e->tri_len) e->tri_live = false;
     // headroom for the stops issued next (growth is stream-ordered)
     if ((rc = ensure_headroom(e))) return rc;
     return DIC_OK;

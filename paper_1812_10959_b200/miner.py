@@ -85,6 +85,11 @@ class DeviceEngine:
     def issue_count(self, lfirst: int, llast: int) -> None:
         _abi.call("dic_engine_issue_count", self.h, lfirst, llast)
 
+    def set_comm(self, comm) -> None:
+        """Attach a native NCCL communicator (native_comm): the engine then
+        allreduces the item counts and every stop's counts itself."""
+        _abi.call("dic_engine_set_comm", self.h, comm)
+
     def set_schedule(self, lfirst: np.ndarray, llast: np.ndarray) -> None:
         """The chunk cycle of the coming stops (matching counts run as graphs)."""
         lf = np.ascontiguousarray(lfirst, dtype=np.int64)
@@ -152,6 +157,34 @@ class DeviceEngine:
 _new_frequent = partial(tuple.__new__, FrequentItemset)
 
 
+_COMMS: dict = {}
+
+
+def native_comm(group=None) -> C.c_void_p:
+    """An NCCL communicator over the ranks of a torch.distributed group, built
+    by the library (dic_nccl_comm_init; rank 0's unique id is broadcast once
+    through the group) and cached per group.  Engines that use it run the
+    whole sharded checkpoint loop natively (dic_engine_run)."""
+    import torch
+    import torch.distributed as dist
+
+    key = id(group)
+    if key in _COMMS:
+        return _COMMS[key]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        _abi.call("dic_nccl_unique_id", uid)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ids = (C.c_uint8 * 128)(*t.cpu().tolist())
+    comm = C.c_void_p()
+    _abi.call("dic_nccl_comm_init", ids, world, rank, C.byref(comm))
+    _COMMS[key] = comm
+    return comm
+
+
 def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray,
                     presorted: bool = False) -> tuple[FrequentItemset, ...]:
     """Canonical (size, mask) order (engine.py:446-455) with masks compared as
@@ -171,7 +204,7 @@ def sorted_frequent(masks: np.ndarray, sizes: np.ndarray, sups: np.ndarray,
 def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound: bool = True,
                plan: ShardPlan | None = None, group=None, trace: StopTrace | None = None,
                t0: float | None = None, count_events: list | None = None,
-               engine_factory=None, depth: int = 4, collective: bool | None = None) -> MiningResult:
+               engine_factory=None, depth: int = 4, collective: bool | str | None = None) -> MiningResult:
     """The checkpoint loop of _run over one rank's local rows.
 
     ``plan``/``group``: chunk-sliced sharding (sharding.py) with a
@@ -180,14 +213,18 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
     are appended around every count launch (the bench's roofline figures).
     ``depth``: stops in flight (1 = the reference's strictly sequential loop).
     ``engine_factory``: test seam (a CPU stand-in engine for the gloo
-    multi-rank tests); the product always uses DeviceEngine."""
+    multi-rank tests); the product always uses DeviceEngine.
+    ``collective="native"``: the per-stop allreduces run inside the library on
+    its own NCCL communicator (native_comm) and the whole loop is
+    dic_engine_run; ``True``: torch.distributed all_reduce from this loop."""
     import torch
     import torch.distributed as dist
 
     t0 = time.perf_counter() if t0 is None else t0
     # per-stop collectives: whenever sharded (collective=True forces the
     # collective loop even for one rank, e.g. to test the NCCL path on one GPU)
-    sharded = (plan is not None and plan.world > 1) if collective is None else collective
+    sharded = (plan is not None and plan.world > 1) if collective is None else bool(collective)
+    native = collective == "native" and engine_factory is None
     local_chunks = plan.local_chunks() if plan is not None else None
     tp = [time.perf_counter()]
 
@@ -197,24 +234,28 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
             trace.phases[name] = (tp[-1] - tp[-2]) * 1e3
 
     eng = (engine_factory or DeviceEngine)(tids, n_local, m, params, prune_bound)
+    if native:
+        eng.set_comm(native_comm(group))
     phase("create")
     try:
         stats = MiningStats()
         counts = eng.item_counts()
-        if sharded:
+        if sharded and not native:
             dist.all_reduce(counts, group=group)
         _, npairs = eng.seed(counts)
         phase("first_pass")
         stats.candidates_generated = npairs
         stats.peak_dashed = npairs
         scanned = params.n
-        if engine_factory is None and not sharded:
+        if engine_factory is None and (not sharded or native):
             # the whole loop natively: no Python on the per-stop path
             nst = params.intervals_per_pass
             bounds = [params.chunk_bounds(s) for s in range(1, nst + 1)]
+            rows = np.array([b[1] - b[0] + 1 for b in bounds], dtype=np.int64)  # global rows per stop
+            if local_chunks is not None:
+                bounds = local_chunks  # this rank's slice of each chunk
             lf = np.array([b[0] for b in bounds], dtype=np.int64)
             ll = np.array([b[1] for b in bounds], dtype=np.int64)
-            rows = ll - lf + 1
             out, cms, dashed = eng.run(lf, ll, rows, nst, depth, count_events is not None)
             phase("loop")
             if trace is not None:

@@ -52,3 +52,21 @@ def test_collective_loop_matches_oracle(nccl_group, idx, n, interval):
     # and the native single-GPU loop agrees with it
     res2 = run_engine(db.device_tids(), cfg.n, cfg.m, params)
     assert [(f.mask, f.support) for f in res2.frequent] == [(f.mask, f.support) for f in res.frequent]
+
+
+@pytest.mark.parametrize("idx,n,interval", [(4, 60_000, 6_000), (3, 30_000, 3_000), (2, 20_000, 2_000)])
+def test_native_nccl_loop_matches_oracle(nccl_group, idx, n, interval):
+    """The library's own NCCL communicator (dic_nccl_comm_init) on 1 rank:
+    item counts, per-stop deltas and the dense pair triangle allreduced inside
+    dic_engine_run, the loop fully native."""
+    cfg = scaled(CONFIGS[idx], n, interval=interval)
+    indptr, indices = generate_csr(cfg)
+    db = dic.BitDatabase.from_csr(indptr, indices, cfg.m)
+    params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    plan = dic.ShardPlan.for_params(params, 1, 0)
+    res = run_engine(db.device_tids(), cfg.n, cfg.m, params, plan=plan, group=nccl_group, collective="native")
+    want = O.mine(db.rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=8)
+    assert [(f.mask, f.size, f.support) for f in res.frequent] == want.frequent
+    s = res.stats
+    assert (s.db_passes, s.peak_dashed, s.candidates_generated, s.candidates_pruned, s.interval_counts) == (
+        want.db_passes, want.peak_dashed, want.candidates_generated, want.candidates_pruned, want.interval_counts)
