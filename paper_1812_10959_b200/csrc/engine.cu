@@ -59,7 +59,7 @@ int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, i
 int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                            unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
                            const unsigned long long* abort_flag, cudaStream_t s, const int64_t* chunk_ring,
-                           const unsigned long long* seq, int ring);
+                           const unsigned long long* seq, int ring, unsigned long long* sched);
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
                        cudaStream_t s);
 
@@ -1056,8 +1056,9 @@ int launch_count(dic_engine* e, int64_t lfirst, int64_t llast, const int64_t* sc
     const int ring = (int)e->nsched;
     int rc;
     if (e->tri) {
+        // the pair kernel's grain counters live past the triangle (tri[tri_len..+2))
         if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
-                                         e->tri_len, abort_flag, s, sched, seq, ring)))
+                                         e->tri_len, abort_flag, s, sched, seq, ring, e->tri + e->tri_len)))
             return rc;
     }
     return count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse_issue, e->d_bitems, bn, e->d_doff,
@@ -1328,8 +1329,9 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
             e->pair_tids = e->pair_tids_own;
         }
         e->tri_len = npairs;
-        if ((rc = dalloc(&e->tri, npairs, e->s))) return rc;
-        DIC_CUDA(cudaMemsetAsync(e->tri, 0, npairs * sizeof(unsigned long long), e->s));  // gather re-zeroes
+        // + 2 words: the pair kernel's grain counters (it re-zeroes them itself)
+        if ((rc = dalloc(&e->tri, npairs + 2, e->s))) return rc;
+        DIC_CUDA(cudaMemsetAsync(e->tri, 0, (npairs + 2) * sizeof(unsigned long long), e->s));  // gather re-zeroes
     }
     if ((rc = ensure_headroom(e))) return rc;
     // per-stop counters zero, first stop's delta offsets

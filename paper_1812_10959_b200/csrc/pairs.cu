@@ -14,6 +14,9 @@
 // operand block arrives by one bulk async copy (TMA engine), double-buffered.
 #include "async.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace dic {
 
 constexpr int kPairBlock = 64;
@@ -45,11 +48,49 @@ __device__ __forceinline__ PairBlock pair_block(int64_t bi, int nblk, int m) {
     return p;
 }
 
-// Persistent: the (block pair, tile) units of the chunk, block-pair major, are
-// split evenly over the grid, so every CTA walks a contiguous run of tiles of
-// one or two block pairs (counters flushed with atomics when the pair
-// changes) and all SMs finish together.  Tiles arrive by TMA bulk copies
-// into a 2-stage ring.
+// One (block pair, tile) unit, decoded once by the producer thread into the
+// stage's descriptor so the consumers do no 64-bit division per tile.
+struct PairUnit {
+    int64_t bi;  // block pair; < 0: no unit (end of the CTA's work)
+    int64_t t;   // tile
+    int a0, b0, na, nb;
+    int diag, edge;
+};
+constexpr int kPairStages = 3;
+
+// The 4 x 4 register tile over one 8-word step.  DIAG: register groups i > j
+// of a diagonal block hold no pair (a = ta + 16i >= 16i > tb + 16j), so they
+// are not emitted — 6 of 16 and_popc8 per step.
+template <bool DIAG>
+__device__ __forceinline__ void pair_step(const uint8_t* A, const uint8_t* B, int RB, int ta, int tb, int q,
+                                          uint32_t (&cnt)[4][4], uint32_t one) {
+    uint4 av0[4], av1[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
+        av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16 + 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
+        const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (DIAG && i > j) continue;
+            cnt[i][j] = and_popc8_acc(av0[i], av1[i], bv0, bv1, cnt[i][j], one);
+        }
+    }
+}
+
+// Persistent: the (block pair, tile) units of the chunk, block-pair major.
+// The first static_pct % are split evenly over the grid (each CTA walks a
+// contiguous run of tiles of one or two block pairs, so counters are flushed
+// with atomics rarely); the rest is claimed in grains of `grain` units from
+// sched[0], so CTAs that ran slower than their SM-mates (the warp scheduler
+// does not share an SM evenly between CTAs) do not leave a tail.  The last
+// CTA to finish re-zeroes sched[] for the next launch on the stream.  Thread
+// 0 is the producer: it decodes units into a 3-stage ring of descriptors
+// and issues each unit's A and B row blocks as bulk async copies (TMA).
 template <int TW, int MINB>
 __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
                                                                    ChunkGeom geom, int64_t t_first, int64_t t_last,
@@ -57,8 +98,11 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
                                                                    const unsigned long long* bn2, int64_t tri_len,
                                                                    const unsigned long long* abort_flag,
                                                                    const int64_t* chunk_ring,
-                                                                   const unsigned long long* seq, int ring) {
+                                                                   const unsigned long long* seq, int ring,
+                                                                   unsigned long long* __restrict__ sched,
+                                                                   int static_pct, int grain, uint32_t one) {
     // engine use: skip while aborted, or once the pair bucket is mostly gone
+    // (every CTA reads the same values, so either all return here or none)
     if (abort_flag && (*abort_flag || 2 * (int64_t)*bn2 < tri_len)) return;
     if (chunk_ring) {
         // engine graphs: the stop's chunk comes from the ring slot of *seq
@@ -73,103 +117,134 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
     constexpr int RB = RW * 4;
     constexpr uint32_t BLK = kPairBlock * RB;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    uint8_t* buf = smem + 128;  // [2 stages][A block, B block]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);                  // [kPairStages]
+    PairUnit* desc = reinterpret_cast<PairUnit*>(smem + 32);              // [kPairStages]
+    uint8_t* buf = smem + 256;                                            // [stage][A block, B block]
 
     const int64_t tile_words = (int64_t)m * RW;
     const int64_t nt = t_last - t_first + 1;
     const int64_t U = (int64_t)nblk * (nblk + 1) / 2 * nt;
-    const int64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
-    if (u0 >= u1) return;
-
-    auto issue = [&](int64_t u, int s) {
+    const int64_t US = U * static_pct / 100;
+    // producer state (thread 0 only)
+    int64_t icur = US * blockIdx.x / gridDim.x, iend = US * (blockIdx.x + 1) / gridDim.x;
+    bool dry = false;
+    auto next_unit = [&]() -> int64_t {
+        if (dry) return -1;
+        if (icur == iend) {
+            icur = US + (int64_t)atomicAdd(sched, 1ull) * grain;
+            iend = icur + grain < U ? icur + grain : U;
+            if (icur >= U) {
+                dry = true;
+                return -1;
+            }
+        }
+        return icur++;
+    };
+    auto issue = [&](int s) {
+        PairUnit& d = desc[s];
+        const int64_t u = next_unit();
+        if (u < 0) {
+            d.bi = -1;
+            mbar_arrive(&full[s]);
+            return;
+        }
         const int64_t bi = u / nt;
         const int64_t t = t_first + (u - bi * nt);
         const PairBlock pb = pair_block(bi, nblk, m);
+        d.bi = bi;
+        d.t = t;
+        d.a0 = pb.a0;
+        d.b0 = pb.b0;
+        d.na = pb.na;
+        d.nb = pb.nb;
+        d.diag = pb.diag;
+        d.edge = (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last);
         const uint32_t ab = (uint32_t)pb.na * RB, bb = (uint32_t)pb.nb * RB;
         uint8_t* dst = buf + (size_t)s * 2 * BLK;
         const uint32_t* src = tids + t * tile_words;
-        mbar_expect_tx(&bar[s], ab + (pb.diag ? 0u : bb));
-        bulk_g2s(dst, src + (int64_t)pb.a0 * RW, ab, &bar[s]);
-        if (!pb.diag) bulk_g2s(dst + BLK, src + (int64_t)pb.b0 * RW, bb, &bar[s]);
+        mbar_expect_tx(&full[s], ab + (pb.diag ? 0u : bb));
+        bulk_g2s(dst, src + (int64_t)pb.a0 * RW, ab, &full[s]);
+        if (!pb.diag) bulk_g2s(dst + BLK, src + (int64_t)pb.b0 * RW, bb, &full[s]);
     };
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int s = 0; s < kPairStages; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
-        issue(u0, 0);
-        if (u0 + 1 < u1) issue(u0 + 1, 1);
+        for (int s = 0; s < kPairStages; ++s) issue(s);
     }
     __syncthreads();
 
     const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
     uint32_t cnt[4][4];
     int64_t cur = -1;
-    PairBlock pb{0, 0, 0, 0, true};
+    int a0 = 0, b0 = 0;
     auto flush = [&]() {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int a = pb.a0 + ta + 16 * i, b = pb.b0 + tb + 16 * j;
+                const int a = a0 + ta + 16 * i, b = b0 + tb + 16 * j;
                 if (a < b && b < m && cnt[i][j]) atomicAdd(tri + tri_index(a, b, m), (unsigned long long)cnt[i][j]);
             }
     };
 
-    for (int64_t u = u0; u < u1; ++u) {
-        const int s = (int)((u - u0) & 1);
-        const int64_t bi = u / nt;
-        const int64_t t = t_first + (u - bi * nt);
+    for (int64_t k = 0;; ++k) {
+        const int s = (int)(k % kPairStages);
+        mbar_wait(&full[s], (uint32_t)((k / kPairStages) & 1));
+        const PairUnit& d = desc[s];
+        const int64_t bi = d.bi;
+        if (bi < 0) break;
+        const bool diag = d.diag;
         if (bi != cur) {
             if (cur >= 0) flush();
             cur = bi;
-            pb = pair_block(bi, nblk, m);
+            a0 = d.a0;
+            b0 = d.b0;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) cnt[i][j] = 0;
         }
-        mbar_wait(&bar[s], (uint32_t)(((u - u0) >> 1) & 1));
         uint8_t* A = buf + (size_t)s * 2 * BLK;
-        uint8_t* B = pb.diag ? A : A + BLK;
-        if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
+        uint8_t* B = diag ? A : A + BLK;
+        if (d.edge) {
             // chunk edge inside this tile: zero the rows outside [first, last]
-            const int rows = pb.diag ? pb.na : 2 * kPairBlock;
+            const int na = d.na, nb = d.nb;
+            const int64_t g0 = d.t * TW;
+            const int rows = diag ? na : 2 * kPairBlock;
             for (int idx = threadIdx.x; idx < rows * RW; idx += kPairThreads) {
                 const int r = idx / RW, slot = idx - r * RW;
-                if (slot >= TW || (r < kPairBlock ? r >= pb.na : r - kPairBlock >= pb.nb)) continue;
+                if (slot >= TW || (r < kPairBlock ? r >= na : r - kPairBlock >= nb)) continue;
                 uint32_t* w = reinterpret_cast<uint32_t*>(A + (size_t)r * RB) + slot;
-                *w &= group_mask(geom, t * TW + slot);
+                *w &= group_mask(geom, g0 + slot);
             }
             __syncthreads();
         }
         // two 16-byte chunks (8 words = 256 rows) per step; per pair the 8
         // AND'ed words go through a carry-save tree (7 -> ones/twos/fours,
-        // plus one leftover): 4 POPC + 8 LOP3 instead of 8 POPC, which moves
-        // the bound from the POPC pipe (16 lanes/SM/clk) to LOP3 (64)
+        // plus one leftover): 16 LOP3 + 4 POPC instead of 8 LOP3 + 8 POPC,
+        // which balances the ALU (64 lanes/SM/clk) and POPC (16) pipes
+        if (diag) {
 #pragma unroll
-        for (int q = 0; q < TW / 4; q += 2) {
-            uint4 av0[4], av1[4];
+            for (int q = 0; q < TW / 4; q += 2) pair_step<true>(A, B, RB, ta, tb, q, cnt, one);
+        } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
-                av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16 + 16);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
-                const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) cnt[i][j] += and_popc8(av0[i], av1[i], bv0, bv1);
-            }
+            for (int q = 0; q < TW / 4; q += 2) pair_step<false>(A, B, RB, ta, tb, q, cnt, one);
         }
         __syncthreads();  // stage s consumed
-        if (threadIdx.x == 0 && u + 2 < u1) {
+        if (threadIdx.x == 0) {
             fence_proxy_async();
-            issue(u + 2, s);
+            issue(s);
         }
     }
-    flush();
+    if (cur >= 0) flush();
+    if (threadIdx.x == 0) {
+        // the last CTA out re-arms the grain counter for the next launch
+        __threadfence();
+        if (atomicAdd(sched + 1, 1ull) == gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+        }
+    }
 }
 
 // Bit-sliced copy restricted to the selected items (in the given order).
@@ -192,60 +267,97 @@ __global__ void tids_select_kernel(const uint32_t* __restrict__ src, int64_t n, 
 
 static int g_pair_slots[4] = {0, 0, 0, 0};  // resident CTAs per SM for (TW = 16 / 32) x (MINB = 3 / 4)
 
+static int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* e = getenv(name);
+    if (!e || !*e) return dflt;
+    return std::min(hi, std::max(lo, atoi(e)));
+}
+// hybrid schedule: the statically split share (percent) and the grain (units)
+// of the dynamically claimed rest (tools/lab/pairlab.cu measured 70 / 2)
+static int pair_static_pct() {
+    static const int v = env_int("DIC_PAIR_STATIC_PCT", 70, 0, 100);
+    return v;
+}
+static int pair_grain() {
+    static const int v = env_int("DIC_PAIR_GRAIN", 2, 1, 1 << 20);
+    return v;
+}
+static int pair_minb() {
+    static const int v = env_int("DIC_PAIR_MINB", 3, 3, 4) == 4 ? 4 : 3;
+    return v;
+}
+
+// grain counters for launches without an engine-owned pair (the C-ABI entry):
+// one 2-word device buffer per (device, stream), kept for the process
+static unsigned long long* stream_sched(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, unsigned long long*> bufs;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& p = bufs[{dev, s}];
+    if (!p) {
+        void* q = nullptr;
+        if (cudaMalloc(&q, 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        if (cudaMemsetAsync(q, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) {
+            cudaFree(q);
+            return nullptr;
+        }
+        p = static_cast<unsigned long long*>(q);
+    }
+    return p;
+}
+
 template <int TW, int MINB>
 int pair_launch(const uint32_t* tids, int m, ChunkGeom geom, int64_t t_first, int64_t t_last, int nblk,
-                int64_t units, size_t smem, unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
+                int64_t units, unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
                 const unsigned long long* abort_flag, const int64_t* chunk_ring, const unsigned long long* seq,
-                int ring, cudaStream_t s) {
+                int ring, unsigned long long* sched, cudaStream_t s) {
+    const size_t smem = 256 + (size_t)kPairStages * 2 * kPairBlock * row_words(TW) * 4;
     int& per_sm = g_pair_slots[(TW == 32 ? 1 : 0) + (MINB == 4 ? 2 : 0)];
     if (per_sm == 0) {
         DIC_CUDA(cudaFuncSetAttribute(pair_tri_kernel<TW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      64 * 1024));
+                                      (int)smem));
         DIC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_tri_kernel<TW, MINB>, kPairThreads, smem));
         per_sm = std::max(per_sm, 1);
     }
     // persistent: one CTA per resident slot (fewer when the chunk is small)
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sm_count()));
     pair_tri_kernel<TW, MINB><<<grid, kPairThreads, smem, s>>>(tids, m, geom, t_first, t_last, nblk, tri, bn2,
-                                                                tri_len, abort_flag, chunk_ring, seq, ring);
+                                                                tri_len, abort_flag, chunk_ring, seq, ring, sched,
+                                                                pair_static_pct(), pair_grain(), 1u);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("pair_tri_kernel");
     return DIC_OK;
-}
-
-static int pair_minb() {
-    static int v = 0;
-    if (!v) {
-        const char* e = getenv("DIC_PAIR_MINB");
-        v = (e && atoi(e) == 4) ? 4 : 3;
-    }
-    return v;
 }
 
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                        unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
                        int64_t tri_len = 0, const unsigned long long* abort_flag = nullptr,
                        const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
-                       int ring = 0) {
+                       int ring = 0, unsigned long long* sched = nullptr) {
     // with a chunk ring, [first, last] only sizes the grid (the largest chunk)
     if (last < first || m < 2) return DIC_OK;
+    if (!sched && !(sched = stream_sched(s))) {
+        set_error("dic_count_pairs: no device memory for the grain counters");
+        return DIC_ENOMEM;
+    }
     const int TW = tile_groups(m);
     const ChunkGeom geom = chunk_geom(first, last);
     const int64_t t_first = geom.g_first / TW, t_last = geom.g_last / TW;
     const int64_t nt = t_last - t_first + 1;
     const int nblk = (m + kPairBlock - 1) / kPairBlock;
     const int64_t units = (int64_t)nblk * (nblk + 1) / 2 * nt;
-    const size_t smem = 128 + 2 * 2 * (size_t)kPairBlock * row_words(TW) * 4;
     const bool b4 = pair_minb() == 4;
     if (TW == 32)
-        return b4 ? pair_launch<32, 4>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
-                                       chunk_ring, seq, ring, s)
-                  : pair_launch<32, 3>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
-                                       chunk_ring, seq, ring, s);
-    return b4 ? pair_launch<16, 4>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
-                                   chunk_ring, seq, ring, s)
-              : pair_launch<16, 3>(tids, m, geom, t_first, t_last, nblk, units, smem, tri, bn2, tri_len, abort_flag,
-                                   chunk_ring, seq, ring, s);
+        return b4 ? pair_launch<32, 4>(tids, m, geom, t_first, t_last, nblk, units, tri, bn2, tri_len, abort_flag,
+                                       chunk_ring, seq, ring, sched, s)
+                  : pair_launch<32, 3>(tids, m, geom, t_first, t_last, nblk, units, tri, bn2, tri_len, abort_flag,
+                                       chunk_ring, seq, ring, sched, s);
+    return b4 ? pair_launch<16, 4>(tids, m, geom, t_first, t_last, nblk, units, tri, bn2, tri_len, abort_flag,
+                                   chunk_ring, seq, ring, sched, s)
+              : pair_launch<16, 3>(tids, m, geom, t_first, t_last, nblk, units, tri, bn2, tri_len, abort_flag,
+                                   chunk_ring, seq, ring, sched, s);
 }
 
 int tids_select_launch(const uint32_t* src, int64_t n, int m, const int32_t* items, int L, uint32_t* dst,
@@ -263,9 +375,10 @@ int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first
                            unsigned long long* tri, const unsigned long long* bn2, int64_t tri_len,
                            const unsigned long long* abort_flag, cudaStream_t s,
                            const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
-                           int ring = 0) {
+                           int ring = 0, unsigned long long* sched = nullptr) {
     // tri is all-zero between stops: the gather re-zeroes every entry it reads
-    return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag, chunk_ring, seq, ring);
+    return count_pairs_launch(tids, n, m, first, last, tri, s, bn2, tri_len, abort_flag, chunk_ring, seq, ring,
+                              sched);
 }
 
 
