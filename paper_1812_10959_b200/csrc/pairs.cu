@@ -60,8 +60,10 @@ constexpr int kPairStages = 3;
 
 // The 4 x 4 register tile over one 8-word step.  DIAG: register groups i > j
 // of a diagonal block hold no pair (a = ta + 16i >= 16i > tb + 16j), so they
-// are not emitted — 6 of 16 and_popc8 per step.
-template <bool DIAG>
+// are not emitted — 6 of 16 and_popc8 per step.  NJ: register columns
+// j >= NJ lie past the last item of a partial B block (nb <= 16 NJ) and are
+// not emitted either (cfg4: the 40-item last block, 15 of 136 block pairs).
+template <bool DIAG, int NJ = 4>
 __device__ __forceinline__ void pair_step(const uint8_t* A, const uint8_t* B, int RB, int ta, int tb, int q,
                                           uint32_t (&cnt)[4][4], uint32_t one) {
     uint4 av0[4], av1[4];
@@ -71,7 +73,7 @@ __device__ __forceinline__ void pair_step(const uint8_t* A, const uint8_t* B, in
         av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16 + 16);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
         const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
         const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
 #pragma unroll
@@ -82,15 +84,26 @@ __device__ __forceinline__ void pair_step(const uint8_t* A, const uint8_t* B, in
     }
 }
 
+// Producer state, in shared memory: whichever warp refills a stage runs it.
+struct PairProd {
+    int64_t icur, iend;  // claimed unit range
+    int dry;             // no units left
+};
+
 // Persistent: the (block pair, tile) units of the chunk, block-pair major.
 // The first static_pct % are split evenly over the grid (each CTA walks a
 // contiguous run of tiles of one or two block pairs, so counters are flushed
 // with atomics rarely); the rest is claimed in grains of `grain` units from
 // sched[0], so CTAs that ran slower than their SM-mates (the warp scheduler
 // does not share an SM evenly between CTAs) do not leave a tail.  The last
-// CTA to finish re-zeroes sched[] for the next launch on the stream.  Thread
-// 0 is the producer: it decodes units into a 3-stage ring of descriptors
-// and issues each unit's A and B row blocks as bulk async copies (TMA).
+// CTA to finish re-zeroes sched[] for the next launch on the stream.
+//
+// Stages: a 3-deep ring of (descriptor, A row block, B row block), each
+// filled by bulk async copies (TMA) that complete on the stage's mbarrier.
+// There is no CTA-wide barrier per tile: every warp counts its arrival on
+// the stage it consumed, and the LAST warp to arrive refills it (decodes the
+// next unit into the descriptor and issues its copies), so no warp waits for
+// a designated producer and the refill starts the moment the stage is free.
 template <int TW, int MINB>
 __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint32_t* __restrict__ tids, int m,
                                                                    ChunkGeom geom, int64_t t_first, int64_t t_last,
@@ -116,33 +129,31 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
     constexpr int RW = TW + 4;
     constexpr int RB = RW * 4;
     constexpr uint32_t BLK = kPairBlock * RB;
+    constexpr int NW = kPairThreads / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);                  // [kPairStages]
-    PairUnit* desc = reinterpret_cast<PairUnit*>(smem + 32);              // [kPairStages]
+    uint32_t* arrived = reinterpret_cast<uint32_t*>(smem + 24);           // [kPairStages]
+    PairProd* prod = reinterpret_cast<PairProd*>(smem + 40);
+    PairUnit* desc = reinterpret_cast<PairUnit*>(smem + 64);              // [kPairStages]
     uint8_t* buf = smem + 256;                                            // [stage][A block, B block]
 
     const int64_t tile_words = (int64_t)m * RW;
     const int64_t nt = t_last - t_first + 1;
     const int64_t U = (int64_t)nblk * (nblk + 1) / 2 * nt;
     const int64_t US = U * static_pct / 100;
-    // producer state (thread 0 only)
-    int64_t icur = US * blockIdx.x / gridDim.x, iend = US * (blockIdx.x + 1) / gridDim.x;
-    bool dry = false;
-    auto next_unit = [&]() -> int64_t {
-        if (dry) return -1;
-        if (icur == iend) {
-            icur = US + (int64_t)atomicAdd(sched, 1ull) * grain;
-            iend = icur + grain < U ? icur + grain : U;
-            if (icur >= U) {
-                dry = true;
-                return -1;
-            }
-        }
-        return icur++;
-    };
+    // the refilling lane: decode the next unit into desc[s] and issue it
     auto issue = [&](int s) {
+        PairProd& P = *prod;
         PairUnit& d = desc[s];
-        const int64_t u = next_unit();
+        int64_t u = -1;
+        if (!P.dry) {
+            if (P.icur == P.iend) {
+                P.icur = US + (int64_t)atomicAdd(sched, 1ull) * grain;
+                P.iend = P.icur + grain < U ? P.icur + grain : U;
+                if (P.icur >= U) P.dry = 1;
+            }
+            if (!P.dry) u = P.icur++;
+        }
         if (u < 0) {
             d.bi = -1;
             mbar_arrive(&full[s]);
@@ -167,13 +178,20 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
         if (!pb.diag) bulk_g2s(dst + BLK, src + (int64_t)pb.b0 * RW, bb, &full[s]);
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kPairStages; ++s) mbar_init(&full[s], 1);
+        prod->icur = US * blockIdx.x / gridDim.x;
+        prod->iend = US * (blockIdx.x + 1) / gridDim.x;
+        prod->dry = 0;
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);
+            arrived[s] = 0;
+        }
         fence_mbar_init();
         for (int s = 0; s < kPairStages; ++s) issue(s);
     }
     __syncthreads();
 
     const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
+    const int lane = threadIdx.x & 31;
     uint32_t cnt[4][4];
     int64_t cur = -1;
     int a0 = 0, b0 = 0;
@@ -208,6 +226,7 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
         uint8_t* B = diag ? A : A + BLK;
         if (d.edge) {
             // chunk edge inside this tile: zero the rows outside [first, last]
+            // (every warp meets this barrier for the same tile)
             const int na = d.na, nb = d.nb;
             const int64_t g0 = d.t * TW;
             const int rows = diag ? na : 2 * kPairBlock;
@@ -226,17 +245,27 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
         if (diag) {
 #pragma unroll
             for (int q = 0; q < TW / 4; q += 2) pair_step<true>(A, B, RB, ta, tb, q, cnt, one);
+        } else if (d.nb <= 48) {
+#pragma unroll
+            for (int q = 0; q < TW / 4; q += 2) pair_step<false, 3>(A, B, RB, ta, tb, q, cnt, one);
         } else {
 #pragma unroll
             for (int q = 0; q < TW / 4; q += 2) pair_step<false>(A, B, RB, ta, tb, q, cnt, one);
         }
-        __syncthreads();  // stage s consumed
-        if (threadIdx.x == 0) {
-            fence_proxy_async();
-            issue(s);
+        // stage s consumed by this warp; the last warp refills it
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&arrived[s], 1u) == NW - 1) {
+                arrived[s] = 0;
+                __threadfence_block();
+                fence_proxy_async();
+                issue(s);
+            }
         }
     }
     if (cur >= 0) flush();
+    __syncthreads();
     if (threadIdx.x == 0) {
         // the last CTA out re-arms the grain counter for the next launch
         __threadfence();
@@ -273,13 +302,13 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
     return std::min(hi, std::max(lo, atoi(e)));
 }
 // hybrid schedule: the statically split share (percent) and the grain (units)
-// of the dynamically claimed rest (tools/lab/pairlab.cu measured 70 / 2)
+// of the dynamically claimed rest (cfg4 chunks: 50 / 4, tools/lab/sweep_pair.sh)
 static int pair_static_pct() {
-    static const int v = env_int("DIC_PAIR_STATIC_PCT", 70, 0, 100);
+    static const int v = env_int("DIC_PAIR_STATIC_PCT", 50, 0, 100);
     return v;
 }
 static int pair_grain() {
-    static const int v = env_int("DIC_PAIR_GRAIN", 2, 1, 1 << 20);
+    static const int v = env_int("DIC_PAIR_GRAIN", 4, 1, 1 << 20);
     return v;
 }
 static int pair_minb() {

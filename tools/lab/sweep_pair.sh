@@ -1,4 +1,4 @@
-for sp in 0 50 70 85 100; do for gr in 1 2 4; do
+# schedule sweep of the dense pair kernel on a real cfg4 chunk (tools/pair_kernel_probe.py)
+for sp in ${SPS:-30 50 70 100}; do for gr in ${GRS:-2 4}; do
   echo -n "sp=$sp gr=$gr: "; DIC_PAIR_STATIC_PCT=$sp DIC_PAIR_GRAIN=$gr python tools/pair_kernel_probe.py 7
 done; done
-echo -n "minb4 70/2: "; DIC_PAIR_MINB=4 python tools/pair_kernel_probe.py 7
