@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libdicb200.so"
+# DIC_LIB: an alternative build of the same library (A/B timing of kernel variants)
+_LIB_PATH = Path(os.environ.get("DIC_LIB") or Path(__file__).resolve().parent / "lib" / "libdicb200.so")
 
 DIC_OK, DIC_EINVAL, DIC_ECUDA, DIC_ENOMEM, DIC_EDATA, DIC_ESTATE = 0, -1, -2, -3, -4, -5
 

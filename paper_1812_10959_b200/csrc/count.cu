@@ -184,6 +184,14 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     }
 }
 
+// carry-save popcount of 4 words: 3 POPC + 2 LOP3 instead of 4 POPC (the
+// POPC pipe runs at a quarter of the LOP3 rate and binds for k = 2; cfg5
+// k = 2 bucket: 4.2 -> 3.8 ms in tools/lab/count_ab.py)
+__device__ __forceinline__ uint32_t popc4_csa(uint4 v) {
+    const uint32_t s = lop3_xor3(v.x, v.y, v.z), c = lop3_maj(v.x, v.y, v.z);
+    return __popc(s) + __popc(v.w) + 2u * __popc(c);
+}
+
 // Row-lane variant: SUB = TW/4 lanes share a candidate, lane `sub` reading
 // 16-byte chunk `sub` of each item row, so SUB adjacent lanes always read one
 // contiguous row (128 B at TW = 32, 64 B at TW = 16): conflict-free or nearly
@@ -261,7 +269,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
                 const uint32_t item = (j & 1) ? (it[r][j >> 1] >> 16) : (it[r][j >> 1] & 0xFFFFu);
                 v = and4(v, *reinterpret_cast<const uint4*>(bs + item * RB));
             }
-            cnt[r] += popc4(v);
+            cnt[r] += K <= 4 ? popc4_csa(v) : popc4(v);  // sizes 5+: shared memory binds, not POPC
         }
         __syncthreads();
         if (threadIdx.x == 0 && t + 2 < t1) {
