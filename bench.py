@@ -184,6 +184,26 @@ def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
+    # the streaming regime: first_pass's column popcounts (item_support) over
+    # the whole 3.2 GB bitmap, HBM-bound (SURVEY 8(d) evidence)
+    counts = torch.zeros(m, dtype=torch.int64, device="cuda")
+    D.item_support(tids, n, m, 0, n - 1, counts)
+    torch.cuda.synchronize()
+    hb = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        D.item_support(tids, n, m, 0, n - 1, counts)
+        e1.record()
+        torch.cuda.synchronize()
+        hb.append(e0.elapsed_time(e1))
+    hbm_gbs, hbm_src = measured_hbm()
+    t_hbm = min(hb)
+    moved = tids.numel() * tids.element_size()  # tiles incl. 4 pad words per item row
+    hbm = {"kernel": "item_support_kernel", "ms": t_hbm, "bytes_read": moved,
+           "algorithmic_bytes": n * words_for(m) * 8, "achieved_gbs": moved / (t_hbm * 1e-3) / 1e9,
+           "peak_gbs": hbm_gbs, "frac": moved / (t_hbm * 1e-3) / 1e9 / hbm_gbs, "peak_source": hbm_src}
+    del counts
     words = (n + 31) // 32
     ops = float(sum(int(b.shape[0]) * int(b.shape[1]) for b in buckets)) * words  # k lane-ops per cand-word
     sum_nnz64 = 0
@@ -200,6 +220,7 @@ def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
             "subset_tests_per_s": C * n / (best * 1e-3), "bound": "int-ALU (LOP3 lane-ops)",
             "achieved": achieved / 1e12, "peak": peaks["lop3"] / 1e12, "unit": "T lane-ops/s",
             "frac": achieved / peaks["lop3"], "support_checksum": checksum, "north_star": ns,
+            "hbm_streaming": hbm,
             "ops_rule": "k lane-ops per (candidate, 32-row word): (k-1) ANDs + >= 1 to accumulate the popcount"}
 
 
