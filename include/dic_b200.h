@@ -297,6 +297,14 @@ int dic_nccl_unique_id(uint8_t* out /* [128] */);
 int dic_nccl_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, void** comm);
 int dic_nccl_comm_destroy(void* comm);
 int dic_engine_set_comm(dic_engine* e, void* comm);
+/* How the engine reduces a stop's counts across ranks: 0 = not sharded,
+ * 1 = ncclAllReduce of the delta buffer and the dense pair triangle,
+ * 2 = fused: the count kernels write per-rank partials
+ *     into NCCL symmetric windows and one kernel per stop sums the partials of
+ *     every NVLink (LSA) peer straight from peer memory, sized on the device
+ *     by the live slots; chosen by dic_engine_set_comm when every rank is in
+ *     one LSA team and DIC_FUSED_REDUCE is not 0.                          */
+int dic_engine_collective_mode(dic_engine* e);
 
 /* Results: number of SOLID_BOX records, then copy them out to HOST arrays
  * masks[F][W] (uint64), sizes[F], supports[F] in the reference's canonical

@@ -79,6 +79,7 @@ SIGNATURES: dict[str, tuple] = {
     "dic_nccl_comm_init": (C.c_int, [vp, i32, i32, P(vp)]),
     "dic_nccl_comm_destroy": (C.c_int, [vp]),
     "dic_engine_set_comm": (C.c_int, [vp, vp]),
+    "dic_engine_collective_mode": (C.c_int, [vp]),
     "dic_containment": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
     "dic_containment_packed": (C.c_int, [vp, i64, i32, vp, vp, i64, vp, vp]),
     "dic_encode_status_init": (C.c_int, [vp, vp]),

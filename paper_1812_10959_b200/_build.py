@@ -25,6 +25,26 @@ NVCC_FLAGS = ARCH + [
 ]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function"]
 
+# NCCL >= 2.28 (headers + library) for the device API of the fused reduction:
+# the copy torch ships (and loads first at run time); the system one is 2.27
+def _nccl_home() -> Path | None:
+    try:
+        import nvidia.nccl as _n  # noqa: PLC0415
+
+        for base in _n.__path__:
+            if (Path(base) / "include" / "nccl_device.h").exists():
+                return Path(base)
+    except ImportError:
+        pass
+    return None
+
+
+NCCL_HOME = _nccl_home()
+if NCCL_HOME is None:
+    raise RuntimeError("libdicb200 needs NCCL >= 2.28 headers (nccl_device.h); pip package nvidia-nccl not found")
+NCCL_INC = ["-I", str(NCCL_HOME / "include")]
+NCCL_LINK = ["-L", str(NCCL_HOME / "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + str(NCCL_HOME / "lib")]
+
 CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "containment.cu", "probe.cu"]
 CPP_SOURCES = ["synth.cpp", "textio.cpp"]
 
@@ -53,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         objs.append(obj)
         if force or _stale(obj, src):
             extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-            jobs.append([NVCC, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)])
+            jobs.append([NVCC, *NVCC_FLAGS, *NCCL_INC, *extra, "-c", str(src), "-o", str(obj)])
     cxx = shutil.which("g++") or "g++"
     for name in CPP_SOURCES:
         src, obj = CSRC / name, OBJDIR / (name + ".o")
@@ -67,7 +87,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
                     print(" ".join(cmd), file=sys.stderr)
     if force or jobs or not LIB.exists():
         tmp = LIB.with_suffix(".so.tmp")
-        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", "-lnccl"])
+        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", *NCCL_LINK])
         os.replace(tmp, LIB)
     return LIB
 

@@ -39,7 +39,9 @@
 // engine omits it; the API-level prune on host catalogs keeps it.
 #include "common.cuh"
 
+#include <map>
 #include <nccl.h>
+#include <nccl_device.h>  // NCCL >= 2.28 device API: symmetric windows, LSA barriers
 
 #include <algorithm>
 #include <chrono>
@@ -49,6 +51,9 @@
 #include <vector>
 
 namespace dic {
+
+constexpr int kFusedCtas = 256;     // CTAs (and LSA barriers) of the fused per-stop reduction
+constexpr int kFusedMaxPeers = 72;  // LSA team size it supports (one NVLink domain)
 
 int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
                      uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
@@ -673,6 +678,7 @@ struct GraphKey {
     int64_t hcap;
     int64_t kuse;
     const unsigned long long* delta;
+    const unsigned long long* delta_p;  // fused reduction: the count graph's target
     const int32_t* keep;
     const int32_t* frontier;
     const unsigned long long* tmp_mask;
@@ -777,6 +783,18 @@ struct dic_engine {
     // and checkpoint halves
     ncclComm_t comm = nullptr;
     bool tri_live = true;                // host view: the pair triangle may still be dense
+    // fused reduction: the count kernels write this rank's
+    // partial counts into NCCL symmetric windows (delta_p, tri_p); one kernel
+    // per stop barriers with the peers over NVLink (LSA team), sums every
+    // peer's partial into delta / tri (what the checkpoint reads) and re-zeroes
+    // its partials, instead of two ncclAllReduce calls
+    bool fused = false;
+    ncclDevComm devc{};
+    unsigned long long* delta_p = nullptr;
+    unsigned long long* tri_p = nullptr;  // + 2 words: the pair kernel's grain counters
+    ncclWindow_t win_delta = nullptr, win_tri = nullptr;   // partials
+    ncclWindow_t win_dsum = nullptr, win_tsum = nullptr;   // sums (delta, tri) in fused mode
+    std::map<const unsigned long long*, int64_t> sym_counts;  // element count of each symmetric buffer held
 };
 
 namespace {
@@ -931,6 +949,94 @@ int sync_bucket_tables(dic_engine* e) {
     return flush();
 }
 
+// NCCL symmetric buffers of the fused reduction.  Allocation + window
+// registration is collective and host-synchronous (milliseconds), so buffers
+// are pooled per communicator and reused by later engines (a mining run per
+// bench step must not re-register); they are released by
+// dic_nccl_comm_destroy.  Every rank makes the same calls in the same order:
+// sizes and growth points come from the replicated statuses, and the pool's
+// best-fit choice depends only on that call sequence.
+struct SymBuf {
+    unsigned long long* ptr;
+    ncclWindow_t win;
+    int64_t count;
+};
+std::mutex g_sym_mu;
+std::map<ncclComm_t, std::vector<SymBuf>> g_sym_free;
+std::map<ncclComm_t, ncclDevComm> g_devcomm;
+
+int sym_free(dic_engine* e, unsigned long long** p, ncclWindow_t* w) {
+    if (!*p) return DIC_OK;
+    // kernels already enqueued may still read it; the next user zeroes it on
+    // its own (same) stream order only after a host sync, so drain here
+    DIC_CUDA(cudaStreamSynchronize(e->s));
+    std::lock_guard<std::mutex> lk(g_sym_mu);
+    g_sym_free[e->comm].push_back(SymBuf{*p, *w, e->sym_counts[*p]});
+    e->sym_counts.erase(*p);
+    *p = nullptr;
+    *w = nullptr;
+    return DIC_OK;
+}
+
+int sym_realloc(dic_engine* e, unsigned long long** p, ncclWindow_t* w, int64_t count) {
+    int rc;
+    if ((rc = sym_free(e, p, w))) return rc;
+    count = std::max<int64_t>(count, 1);
+    {
+        std::lock_guard<std::mutex> lk(g_sym_mu);
+        auto& fl = g_sym_free[e->comm];
+        int best = -1;
+        for (int i = 0; i < (int)fl.size(); ++i)
+            if (fl[i].count >= count && (best < 0 || fl[i].count < fl[best].count)) best = i;
+        if (best >= 0) {
+            *p = fl[best].ptr;
+            *w = fl[best].win;
+            e->sym_counts[*p] = fl[best].count;
+            fl.erase(fl.begin() + best);
+        }
+    }
+    if (!*p) {
+        const size_t bytes = (size_t)count * sizeof(unsigned long long);
+        void* q = nullptr;
+        ncclResult_t r = ncclMemAlloc(&q, bytes);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclMemAlloc");
+        r = ncclCommWindowRegister(e->comm, q, bytes, w, NCCL_WIN_COLL_SYMMETRIC);
+        if (r != ncclSuccess) {
+            ncclMemFree(q);
+            return nccl_fail(r, "ncclCommWindowRegister");
+        }
+        *p = static_cast<unsigned long long*>(q);
+        e->sym_counts[*p] = count;
+    }
+    DIC_CUDA(cudaMemsetAsync(*p, 0, (size_t)e->sym_counts[*p] * sizeof(unsigned long long), e->s));
+    return DIC_OK;
+}
+
+// release every pooled symmetric buffer (and the device communicator) of a
+// communicator, before it dies
+int sym_pool_release(ncclComm_t comm) {
+    std::vector<SymBuf> fl;
+    {
+        std::lock_guard<std::mutex> lk(g_sym_mu);
+        auto dc = g_devcomm.find(comm);
+        if (dc != g_devcomm.end()) {
+            ncclDevCommDestroy(comm, &dc->second);
+            g_devcomm.erase(dc);
+        }
+        auto it = g_sym_free.find(comm);
+        if (it == g_sym_free.end()) return DIC_OK;
+        fl.swap(it->second);
+        g_sym_free.erase(it);
+    }
+    for (SymBuf& b : fl) {
+        ncclResult_t r = ncclCommWindowDeregister(comm, b.win);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclCommWindowDeregister");
+        r = ncclMemFree(b.ptr);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclMemFree");
+    }
+    return DIC_OK;
+}
+
 // per-stop slot arrays (delta, keep, frontier) cover every bucket capacity
 int ensure_slot_arrays(dic_engine* e) {
     int64_t need = 0;
@@ -938,13 +1044,20 @@ int ensure_slot_arrays(dic_engine* e) {
     need = std::max<int64_t>(need, 1);
     if (need <= e->slot_cap) return DIC_OK;
     const int64_t nc = std::max<int64_t>(need, e->slot_cap + e->slot_cap / 2);
-    dfree(e->delta, e->s);
-    dfree(e->keep, e->s);
     int rc;
-    if ((rc = dalloc(&e->delta, nc, e->s)) || (rc = dalloc(&e->keep, nc, e->s))) return rc;
-    DIC_CUDA(cudaMemsetAsync(e->delta, 0, nc * sizeof(unsigned long long), e->s));  // apply re-zeroes
+    if (e->fused) {
+        // peers write the stop's sums straight into delta: a symmetric window
+        if ((rc = sym_realloc(e, &e->delta, &e->win_dsum, nc))) return rc;
+    } else {
+        dfree(e->delta, e->s);
+        if ((rc = dalloc(&e->delta, nc, e->s))) return rc;
+        DIC_CUDA(cudaMemsetAsync(e->delta, 0, nc * sizeof(unsigned long long), e->s));  // apply re-zeroes
+    }
+    dfree(e->keep, e->s);
+    if ((rc = dalloc(&e->keep, nc, e->s))) return rc;
     // the frontier of a stop awaiting a candidate replay must survive growth
     if ((rc = dgrow(&e->frontier, e->slot_cap, nc, e->s))) return rc;
+    if (e->fused && (rc = sym_realloc(e, &e->delta_p, &e->win_delta, nc))) return rc;
     e->slot_cap = nc;
     return DIC_OK;
 }
@@ -1046,6 +1159,77 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s) {
     return launch_status(e, s);
 }
 
+// Fused reduction of a stop's counts over NVLink peer memory (SURVEY 8(f)
+// row 1): one launch instead of two ncclAllReduce calls, sized on the device
+// by the live slots (doff[kuse]) instead of the slot capacity.  A reduce-
+// scatter + all-gather over the LSA team (every rank in one NVLink domain):
+// the slots are cut into G x P slices; CTA b of rank r owns slice (b, r).
+//   1. LSA barrier b: CTA b of every rank has started, so every rank's count
+//      kernels (earlier on its stream) have finished their partials;
+//   2. the owner sums slice (b, r) over the P partials (peer loads) and stores
+//      the sum into every rank's sum buffer (peer stores): (P-1)/P of the data
+//      in and out per rank, like a ring or NVLS allreduce;
+//   3. LSA barrier b again: every rank's CTA b has read slices (b, *) of this
+//      rank's partials and delivered its sums, so CTA b re-zeroes slices
+//      (b, *) of the local partials for the next stop's count.
+// The checkpoint graph then reads the local sums (delta / tri) exactly as on
+// one GPU.  Every rank runs both barriers whatever its data (abort and
+// density are replicated decisions), so the barrier epochs stay matched.
+__device__ __forceinline__ void fused_slices(ncclWindow_t wpart, ncclWindow_t wsum, int64_t n, int P, int me,
+                                             unsigned long long* const* part, unsigned long long* const* sum) {
+    const int64_t S = (int64_t)gridDim.x * P;
+    const int64_t q = (int64_t)blockIdx.x * P + me;
+    const int64_t lo = n * q / S, hi = n * (q + 1) / S;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        unsigned long long v = 0;
+        for (int p = 0; p < P; ++p) v += part[p][i];
+        for (int p = 0; p < P; ++p) sum[p][i] = v;
+    }
+}
+
+__device__ __forceinline__ void fused_zero(unsigned long long* mine, int64_t n, int P) {
+    const int64_t S = (int64_t)gridDim.x * P;
+    const int64_t lo = n * ((int64_t)blockIdx.x * P) / S, hi = n * ((int64_t)blockIdx.x * P + P) / S;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) mine[i] = 0;
+}
+
+__global__ void __launch_bounds__(256) fused_reduce_kernel(ncclDevComm dc, ncclWindow_t wdp, ncclWindow_t wds,
+                                                           ncclWindow_t wtp, ncclWindow_t wts,
+                                                           const int64_t* __restrict__ doff, int kuse,
+                                                           int64_t tri_len, const unsigned long long* bn2,
+                                                           const unsigned long long* abort_flag) {
+    __shared__ unsigned long long* ptr[4][kFusedMaxPeers];  // delta part / sum, tri part / sum per peer
+    const int P = dc.lsaSize, me = dc.lsaRank;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        ptr[0][p] = static_cast<unsigned long long*>(ncclGetLsaPointer(wdp, 0, p));
+        ptr[1][p] = static_cast<unsigned long long*>(ncclGetLsaPointer(wds, 0, p));
+        if (wtp) {
+            ptr[2][p] = static_cast<unsigned long long*>(ncclGetLsaPointer(wtp, 0, p));
+            ptr[3][p] = static_cast<unsigned long long*>(ncclGetLsaPointer(wts, 0, p));
+        }
+    }
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);  // also publishes ptr[][] to the CTA
+    const bool skip = *abort_flag != 0;
+    const int64_t nlive = skip ? 0 : doff[kuse];
+    const bool dense = !skip && wtp != nullptr && tri_len > 0 && 2 * (int64_t)*bn2 >= tri_len;
+    fused_slices(wdp, wds, nlive, P, me, ptr[0], ptr[1]);
+    if (dense) fused_slices(wtp, wts, tri_len, P, me, ptr[2], ptr[3]);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    fused_zero(ptr[0][me], nlive, P);
+    if (dense) fused_zero(ptr[2][me], tri_len, P);
+}
+
+int launch_fused_reduce(dic_engine* e, cudaStream_t s) {
+    const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
+    fused_reduce_kernel<<<kFusedCtas, 256, 0, s>>>(e->devc, e->win_delta, e->win_dsum, e->tri ? e->win_tri : nullptr,
+                                                   e->tri ? e->win_tsum : nullptr, e->d_doff, (int)e->kuse_issue,
+                                                   e->tri ? e->tri_len : 0, bn + 2, e->d_stat + S_ABORT);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("fused_reduce_kernel");
+    return DIC_OK;
+}
+
 // the count half: the pair triangle and every dashed bucket over the chunk
 // [lfirst, llast]; sched != nullptr: the chunk is read on the device from the
 // schedule slot S_SEQ % nsched ([lfirst, llast] then only sizes the grid)
@@ -1056,13 +1240,19 @@ int launch_count(dic_engine* e, int64_t lfirst, int64_t llast, const int64_t* sc
     const int ring = (int)e->nsched;
     int rc;
     if (e->tri) {
-        // the pair kernel's grain counters live past the triangle (tri[tri_len..+2))
-        if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, e->tri, bn + 2,
-                                         e->tri_len, abort_flag, s, sched, seq, ring, e->tri + e->tri_len)))
+        // the pair kernel's grain counters live past the triangle (tri[tri_len..+2));
+        // fused reduction: this rank's partial triangle in its symmetric window
+        unsigned long long* tri = e->fused ? e->tri_p : e->tri;
+        if ((rc = count_pairs_dev_launch(e->pair_tids, e->n_local, (int)e->nL1, lfirst, llast, tri, bn + 2,
+                                         e->tri_len, abort_flag, s, sched, seq, ring, tri + e->tri_len)))
             return rc;
     }
-    return count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse_issue, e->d_bitems, bn, e->d_doff,
-                            e->delta, abort_flag, e->tri ? e->tri_len : 0, s, sched, seq, ring);
+    if ((rc = count_dev_launch(e->tids, e->n_local, e->m, lfirst, llast, e->kuse_issue, e->d_bitems, bn, e->d_doff,
+                               e->fused ? e->delta_p : e->delta, abort_flag, e->tri ? e->tri_len : 0, s, sched,
+                               seq, ring)))
+        return rc;
+    // sharded, fused: the cross-rank sum of this stop's partials over NVLink
+    return e->fused ? launch_fused_reduce(e, s) : DIC_OK;
 }
 
 GraphKey graph_key(const dic_engine* e, bool with_sched) {
@@ -1073,6 +1263,7 @@ GraphKey graph_key(const dic_engine* e, bool with_sched) {
     k.hcap = e->hcap;
     k.kuse = e->kuse_issue;
     k.delta = e->delta;
+    k.delta_p = e->delta_p;
     k.keep = e->keep;
     k.frontier = e->frontier;
     k.tmp_mask = e->tmp_mask;
@@ -1204,10 +1395,18 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->ht, s);
     for (Bucket& b : e->buckets) { dfree(b.rec, s); dfree(b.items, s); }
     dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_doff, s); dfree(e->d_stat, s);
-    dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s); dfree(e->delta, s);
+    dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s);
+    if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
-    dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->tri, s); dfree(e->res_ids, s);
+    dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
+    if (!e->fused) dfree(e->tri, s);
+    if (e->fused) {
+        sym_free(e, &e->delta_p, &e->win_delta);
+        sym_free(e, &e->tri_p, &e->win_tri);
+        sym_free(e, &e->delta, &e->win_dsum);
+        sym_free(e, &e->tri, &e->win_tsum);
+    }
     e->hres.gx[0] = e->gx_count;  // pooled with the host resources
     e->hres.gx[1] = e->gx_ckpt;
     release_host_res(e->hres);  // the stream was synchronised above: no stop reads the ring any more
@@ -1253,6 +1452,8 @@ extern "C" int dic_nccl_comm_init(const uint8_t* id_bytes, int32_t nranks, int32
 
 extern "C" int dic_nccl_comm_destroy(void* comm) {
     if (!comm) return DIC_OK;
+    const int rc = sym_pool_release(static_cast<ncclComm_t>(comm));
+    if (rc) return rc;
     const ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
     return r == ncclSuccess ? DIC_OK : nccl_fail(r, "ncclCommDestroy");
 }
@@ -1264,7 +1465,37 @@ extern "C" int dic_engine_set_comm(dic_engine* e, void* comm) {
         return DIC_ESTATE;
     }
     e->comm = static_cast<ncclComm_t>(comm);
+    e->fused = false;
+    // the fused reduction needs every rank in one load/store-accessible (LSA)
+    // team, i.e. one NVLink domain; DIC_FUSED_REDUCE=0 keeps ncclAllReduce
+    const char* env = getenv("DIC_FUSED_REDUCE");
+    if (e->comm && !(env && atoi(env) == 0)) {
+        int nranks = 0;
+        ncclResult_t r = ncclCommCount(e->comm, &nranks);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclCommCount");
+        if (ncclTeamLsa(e->comm).nRanks == nranks && nranks <= kFusedMaxPeers) {
+            // one device communicator per NCCL communicator, kept with the pool
+            std::lock_guard<std::mutex> lk(g_sym_mu);
+            auto it = g_devcomm.find(e->comm);
+            if (it == g_devcomm.end()) {
+                ncclDevCommRequirements reqs;
+                memset(&reqs, 0, sizeof(reqs));
+                reqs.lsaBarrierCount = kFusedCtas;
+                ncclDevComm dc;
+                r = ncclDevCommCreate(e->comm, &reqs, &dc);
+                if (r != ncclSuccess) return nccl_fail(r, "ncclDevCommCreate");
+                it = g_devcomm.emplace(e->comm, dc).first;
+            }
+            e->devc = it->second;
+            e->fused = true;
+        }
+    }
     return DIC_OK;
+}
+
+extern "C" int dic_engine_collective_mode(dic_engine* e) {
+    DIC_REQUIRE(e, "dic_engine_collective_mode: null engine");
+    return e->comm ? (e->fused ? 2 : 1) : 0;
 }
 
 extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_level1, int64_t* n_pairs) {
@@ -1330,8 +1561,13 @@ extern "C" int dic_engine_seed(dic_engine* e, const int64_t* counts, int64_t* n_
         }
         e->tri_len = npairs;
         // + 2 words: the pair kernel's grain counters (it re-zeroes them itself)
-        if ((rc = dalloc(&e->tri, npairs + 2, e->s))) return rc;
-        DIC_CUDA(cudaMemsetAsync(e->tri, 0, (npairs + 2) * sizeof(unsigned long long), e->s));  // gather re-zeroes
+        if (e->fused) {
+            if ((rc = sym_realloc(e, &e->tri, &e->win_tsum, npairs + 2))) return rc;
+            if ((rc = sym_realloc(e, &e->tri_p, &e->win_tri, npairs + 2))) return rc;
+        } else {
+            if ((rc = dalloc(&e->tri, npairs + 2, e->s))) return rc;
+            DIC_CUDA(cudaMemsetAsync(e->tri, 0, (npairs + 2) * sizeof(unsigned long long), e->s));  // gather re-zeroes
+        }
     }
     if ((rc = ensure_headroom(e))) return rc;
     // per-stop counters zero, first stop's delta offsets
@@ -1438,8 +1674,10 @@ static int nccl_fail(ncclResult_t r, const char* what) {
 // The stop's cross-rank reduction (sharded engines): every rank enqueues the
 // same calls in the same order (the state machine and hence slot_cap /
 // tri_live are replicated), so the collectives always match.
+
 static int reduce_stop(dic_engine* e) {
     if (!e->comm) return DIC_OK;
+    if (e->fused) return DIC_OK;  // the count graph ends with fused_reduce_kernel
     ncclResult_t r = ncclAllReduce(e->delta, e->delta, (size_t)e->slot_cap, ncclUint64, ncclSum, e->comm, e->s);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(delta)");
     if (e->tri && e->tri_live) {

@@ -90,6 +90,10 @@ class DeviceEngine:
         allreduces the item counts and every stop's counts itself."""
         _abi.call("dic_engine_set_comm", self.h, comm)
 
+    def collective_mode(self) -> str:
+        """'none', 'nccl' (per-stop ncclAllReduce) or 'fused' (peer-memory reduction kernel)."""
+        return ("none", "nccl", "fused")[_abi.call("dic_engine_collective_mode", self.h)]
+
     def set_schedule(self, lfirst: np.ndarray, llast: np.ndarray) -> None:
         """The chunk cycle of the coming stops (matching counts run as graphs)."""
         lf = np.ascontiguousarray(lfirst, dtype=np.int64)
@@ -260,7 +264,8 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
             phase("loop")
             if trace is not None:
                 trace.native = {"stops": out.stops, "replays": out.replays, "issue_ms": out.issue_us / 1e3,
-                                "poll_ms": out.poll_us / 1e3, "graphs_captured": out.graphs_captured}
+                                "poll_ms": out.poll_us / 1e3, "graphs_captured": out.graphs_captured,
+                                "collective": eng.collective_mode() if hasattr(eng, "collective_mode") else "none"}
             stats.interval_counts += out.interval_counts
             stats.candidates_pruned += out.candidates_pruned
             stats.candidates_generated += out.candidates_generated

@@ -54,17 +54,26 @@ def test_collective_loop_matches_oracle(nccl_group, idx, n, interval):
     assert [(f.mask, f.support) for f in res2.frequent] == [(f.mask, f.support) for f in res.frequent]
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("idx,n,interval", [(4, 60_000, 6_000), (3, 30_000, 3_000), (2, 20_000, 2_000)])
-def test_native_nccl_loop_matches_oracle(nccl_group, idx, n, interval):
+def test_native_nccl_loop_matches_oracle(nccl_group, monkeypatch, idx, n, interval, fused):
     """The library's own NCCL communicator (dic_nccl_comm_init) on 1 rank:
-    item counts, per-stop deltas and the dense pair triangle allreduced inside
-    dic_engine_run, the loop fully native."""
+    item counts allreduced, and per stop the deltas and the dense pair
+    triangle reduced inside dic_engine_run, the loop fully native — either
+    by the fused peer-memory kernel over NCCL symmetric windows (fused=1,
+    the default) or by ncclAllReduce (DIC_FUSED_REDUCE=0)."""
+    from paper_1812_10959_b200.miner import StopTrace
+
+    monkeypatch.setenv("DIC_FUSED_REDUCE", fused)
     cfg = scaled(CONFIGS[idx], n, interval=interval)
     indptr, indices = generate_csr(cfg)
     db = dic.BitDatabase.from_csr(indptr, indices, cfg.m)
     params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
     plan = dic.ShardPlan.for_params(params, 1, 0)
-    res = run_engine(db.device_tids(), cfg.n, cfg.m, params, plan=plan, group=nccl_group, collective="native")
+    trace = StopTrace()
+    res = run_engine(db.device_tids(), cfg.n, cfg.m, params, plan=plan, group=nccl_group, collective="native",
+                     trace=trace)
+    assert trace.native["collective"] == ("fused" if fused == "1" else "nccl")
     want = O.mine(db.rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=8)
     assert [(f.mask, f.size, f.support) for f in res.frequent] == want.frequent
     s = res.stats
