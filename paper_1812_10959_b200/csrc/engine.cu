@@ -704,7 +704,7 @@ struct HostRes {
     cudaStream_t cap = nullptr;
     uint8_t* stage = nullptr;  // pinned staging for the result copies (grown on demand)
     size_t stage_bytes = 0;
-    cudaGraphExec_t gx[2] = {nullptr, nullptr};  // stop graphs, updated in place by the next engine
+    cudaGraphExec_t gx[3] = {nullptr, nullptr, nullptr};  // stop graphs, updated in place by the next engine
 };
 
 struct dic_engine {
@@ -771,6 +771,13 @@ struct dic_engine {
     cudaGraphExec_t gx_count = nullptr, gx_ckpt = nullptr;
     long long nk_count = 0, nk_ckpt = 0; // kernels per graph launch
     GraphKey key_count{}, key_ckpt{};
+    // dic_engine_run: a scheduled stop is ONE graph (count + checkpoint) when
+    // nothing runs between its halves on the host (single GPU, or the fused
+    // reduction, which is the count graph's last node)
+    bool in_run = false, merged_pending = false;
+    cudaGraphExec_t gx_stop = nullptr;
+    long long nk_stop = 0;
+    GraphKey key_stop{};
     int64_t graphs_captured = 0, graph_launches = 0;
     bool count_graphed = false;          // the pending count went through the graph
 
@@ -1375,7 +1382,8 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->cap_stream = e->hres.cap;
     e->gx_count = e->hres.gx[0];  // stale until the first capture updates them
     e->gx_ckpt = e->hres.gx[1];
-    e->hres.gx[0] = e->hres.gx[1] = nullptr;
+    e->gx_stop = e->hres.gx[2];
+    e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
@@ -1409,6 +1417,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     }
     e->hres.gx[0] = e->gx_count;  // pooled with the host resources
     e->hres.gx[1] = e->gx_ckpt;
+    e->hres.gx[2] = e->gx_stop;
     release_host_res(e->hres);  // the stream was synchronised above: no stop reads the ring any more
     delete e;
     return DIC_OK;
@@ -1604,7 +1613,13 @@ extern "C" int dic_engine_issue_count(dic_engine* e, int64_t lfirst, int64_t lla
     if (e->nsched && (empty ? e->h_sched[2 * sl + 1] < e->h_sched[2 * sl]
                             : e->h_sched[2 * sl] == lfirst && e->h_sched[2 * sl + 1] == llast)) {
         // the scheduled chunk: one graph launch (re-captured when its baked-in
-        // pointers / sizes changed)
+        // pointers / sizes changed) — or, inside dic_engine_run with no host
+        // step between the halves, deferred into the stop graph
+        if (e->in_run && (!e->comm || e->fused)) {
+            e->merged_pending = true;
+            e->counted = true;
+            return DIC_OK;
+        }
         const GraphKey k = graph_key(e, true);
         if (!e->gx_count || !(k == e->key_count)) {
             if ((rc = capture_graph(e, &e->gx_count, &e->nk_count, [&](cudaStream_t cs) {
@@ -1696,14 +1711,29 @@ extern "C" int dic_engine_issue_checkpoint(dic_engine* e, int64_t* seq) {
     }
     e->counted = false;
     int rc;
-    if ((rc = reduce_stop(e))) return rc;
-    const GraphKey k = graph_key(e, false);
-    if (!e->gx_ckpt || !(k == e->key_ckpt)) {
-        if ((rc = capture_graph(e, &e->gx_ckpt, &e->nk_ckpt, [&](cudaStream_t cs) { return launch_checkpoint(e, cs); })))
-            return rc;
-        e->key_ckpt = k;
+    if (e->merged_pending) {
+        // count + checkpoint of a scheduled stop as one graph launch
+        e->merged_pending = false;
+        const GraphKey k = graph_key(e, true);
+        if (!e->gx_stop || !(k == e->key_stop)) {
+            if ((rc = capture_graph(e, &e->gx_stop, &e->nk_stop, [&](cudaStream_t cs) {
+                     int r = launch_count(e, k.sched_first, k.sched_last, e->d_sched, cs);
+                     return r ? r : launch_checkpoint(e, cs);
+                 })))
+                return rc;
+            e->key_stop = k;
+        }
+        if ((rc = launch_graph(e, e->gx_stop, e->nk_stop))) return rc;
+    } else {
+        if ((rc = reduce_stop(e))) return rc;
+        const GraphKey k = graph_key(e, false);
+        if (!e->gx_ckpt || !(k == e->key_ckpt)) {
+            if ((rc = capture_graph(e, &e->gx_ckpt, &e->nk_ckpt, [&](cudaStream_t cs) { return launch_checkpoint(e, cs); })))
+                return rc;
+            e->key_ckpt = k;
+        }
+        if ((rc = launch_graph(e, e->gx_ckpt, e->nk_ckpt))) return rc;
     }
-    if ((rc = launch_graph(e, e->gx_ckpt, e->nk_ckpt))) return rc;
     const int slot = (int)(e->issued % kRing);
     e->kuse_at[slot] = e->kuse;
     DIC_CUDA(cudaEventRecord(e->ev[slot], e->s));
@@ -1763,6 +1793,7 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         // the skipped stops are re-issued by the caller
         e->issued = seq + 1;
         e->counted = false;
+        e->merged_pending = false;
         *replayed = 1;
     }
     e->polled = seq + 1;
@@ -1824,6 +1855,12 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     std::deque<Flight> inflight;
     cudaEvent_t t0[kRing], t1[kRing];
     const bool timed = count_ms != nullptr;
+    // one graph per scheduled stop unless the count half is timed on its own
+    // (DIC_STOP_GRAPH=0: two graphs per stop)
+    {
+        const char* env = getenv("DIC_STOP_GRAPH");
+        e->in_run = !timed && !(env && atoi(env) == 0);
+    }
     if (timed)
         for (int i = 0; i < kRing; ++i) {
             DIC_CUDA(cudaEventCreate(&t0[i]));
@@ -1877,6 +1914,7 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
         if (st.dashed_at_end == 0) done = true;
     }
     out->graphs_captured = e->graphs_captured - captured0;
+    e->in_run = false;
     if (timed)
         for (int i = 0; i < kRing; ++i) {
             cudaEventDestroy(t0[i]);
