@@ -184,6 +184,21 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     }
 }
 
+#ifdef DIC_LAB_TIMING
+// per-CTA phase stamps for tools/lab (globaltimer ns): start, ids loaded,
+// first tile landed, tiles done, end
+__device__ unsigned long long g_lab_stamp[4096][6];
+__device__ __forceinline__ void lab_stamp(int i) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_lab_stamp[(blockIdx.y * gridDim.x + blockIdx.x) & 4095][i] = t;
+    }
+}
+#else
+__device__ __forceinline__ void lab_stamp(int) {}
+#endif
+
 // carry-save popcount of 4 words: 3 POPC + 2 LOP3 instead of 4 POPC (the
 // POPC pipe runs at a quarter of the LOP3 rate and binds for k = 2; cfg5
 // k = 2 bucket: 4.2 -> 3.8 ms in tools/lab/count_ab.py)
@@ -201,6 +216,8 @@ __device__ __forceinline__ uint32_t popc4_csa(uint4 v) {
 // rl_slots x R candidates; each lane's partial count is reduced over its SUB
 // lanes once per unit.
 __host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 24 : (K <= 6 ? 16 : 12)); }
+static_assert(rl_regs(1) % 4 == 0 && rl_regs(3) % 4 == 0 && rl_regs(5) % 4 == 0 && rl_regs(7) % 4 == 0,
+              "row-lane id spans are loaded 8 bytes at a time");
 __host__ __device__ constexpr int rl_slots(int TW) { return kStreamThreads / (TW / 4); }  // candidate slots per CTA row
 
 template <int K, int TW>
@@ -215,6 +232,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     // a thread owns R CONSECUTIVE candidates: in a sorted bucket they mostly
     // share their first item, whose chunk is then loaded once per tile
     const int64_t cbase = blk * (int64_t)rl_slots(TW) * R + (int64_t)slot * R;
+    lab_stamp(0);
     if (threadIdx.x == 0) {
         fence_proxy_async();
         issue_tile(smem, tids, tb, t0, 0);
@@ -223,21 +241,47 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     uint32_t it[R][KP];
     uint32_t cnt[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int64_t c = cbase + r;
-        const int64_t cc = c < C ? c : C - 1;
-        cnt[r] = 0;
+    for (int r = 0; r < R; ++r) cnt[r] = 0;
+    if (cbase + R <= C && ((reinterpret_cast<uintptr_t>(items + cbase * K) & 7u) == 0)) {
+        // the thread's R x K ids are one contiguous, 8-byte aligned span
+        // (R is a multiple of 4): R*K/4 8-byte loads instead of R*K 2-byte
+        // ones, which dominated the unit's prologue (~2.7 us at R*K = 72)
+        uint32_t w[R * K / 2];
+        const uint2* src = reinterpret_cast<const uint2*>(items + cbase * K);
 #pragma unroll
-        for (int j = 0; j < KP; ++j) {
-            uint32_t lo = __ldg(items + cc * K + 2 * j);
-            uint32_t hi = (2 * j + 1 < K) ? (uint32_t)__ldg(items + cc * K + 2 * j + 1) : 0u;
-            it[r][j] = lo | (hi << 16);
+        for (int q = 0; q < R * K / 4; ++q) {
+            const uint2 v = __ldg(src + q);
+            w[2 * q] = v.x;
+            w[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+                const int p = r * K + 2 * j;  // item p and p + 1 of the span
+                const uint32_t lo = (w[p >> 1] >> ((p & 1) * 16)) & 0xFFFFu;
+                const uint32_t hi = (2 * j + 1 < K) ? (w[(p + 1) >> 1] >> (((p + 1) & 1) * 16)) & 0xFFFFu : 0u;
+                it[r][j] = lo | (hi << 16);
+            }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t c = cbase + r;
+            const int64_t cc = c < C ? c : C - 1;
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+                uint32_t lo = __ldg(items + cc * K + 2 * j);
+                uint32_t hi = (2 * j + 1 < K) ? (uint32_t)__ldg(items + cc * K + 2 * j + 1) : 0u;
+                it[r][j] = lo | (hi << 16);
+            }
         }
     }
+    lab_stamp(1);
     for (int64_t t = t0; t < t1; ++t) {
         const int s = (int)((t - t0) & 1);
         mbar_wait(&bar[s], uses[s] & 1u);
         ++uses[s];
+        if (t == t0) lab_stamp(2);
         uint8_t* base = bufs + (size_t)s * tb;
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
@@ -277,6 +321,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
             issue_tile(smem, tids, tb, t + 2, s);
         }
     }
+    lab_stamp(3);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         uint32_t x = cnt[r];
@@ -285,6 +330,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         const int64_t c = cbase + r;
         if (sub == 0 && c < C && x) atomicAdd(out + c, (unsigned long long)x);
     }
+    lab_stamp(4);
 }
 
 template <int TW>
@@ -822,6 +868,14 @@ extern "C" int dic_item_support(const uint32_t* tids, int64_t n, int32_t m, int6
     return item_support_launch(tids, n, m, first, last, reinterpret_cast<unsigned long long*>(counts),
                                as_stream(stream));
 }
+
+#ifdef DIC_LAB_TIMING
+extern "C" int dic_lab_stamps(unsigned long long* host, int32_t n) {
+    cudaDeviceSynchronize();
+    DIC_CUDA(cudaMemcpyFromSymbol(host, g_lab_stamp, (size_t)n * 6 * sizeof(unsigned long long)));
+    return DIC_OK;
+}
+#endif
 
 extern "C" int dic_count_support(const uint32_t* tids, int64_t n, int32_t m, int64_t first, int64_t last,
                                  const uint16_t* items, int32_t k, int64_t C, uint64_t* support_inc,
