@@ -231,7 +231,16 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     const int sub = threadIdx.x & (SUB - 1), slot = threadIdx.x / SUB;
     // a thread owns R CONSECUTIVE candidates: in a sorted bucket they mostly
     // share their first item, whose chunk is then loaded once per tile
-    const int64_t cbase = blk * (int64_t)rl_slots(TW) * R + (int64_t)slot * R;
+    // the bucket's blocks hold equal shares (not full blocks plus a short
+    // tail): every CTA of a row split then finishes at the same time
+    const int64_t cap = (int64_t)rl_slots(TW) * R;
+    const int64_t nblk = (C + cap - 1) / cap;
+    // shares rounded to 4 candidates keep every thread's id span 8-byte aligned
+    const int64_t per = ((C + nblk - 1) / nblk + 3) & ~int64_t(3);
+    const int64_t bend = min(C, (blk + 1) * per);  // this block's candidates: [blk * per, bend)
+    const int64_t cbase = blk * per + (int64_t)slot * R;
+    // slots past the share re-count the block's last candidate (all lanes of
+    // such a warp read the same rows: broadcasts) and add nothing
     lab_stamp(0);
     if (threadIdx.x == 0) {
         fence_proxy_async();
@@ -242,7 +251,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     uint32_t cnt[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) cnt[r] = 0;
-    if (cbase + R <= C && ((reinterpret_cast<uintptr_t>(items + cbase * K) & 7u) == 0)) {
+    if (cbase + R <= bend && ((reinterpret_cast<uintptr_t>(items + cbase * K) & 7u) == 0)) {
         // the thread's R x K ids are one contiguous, 8-byte aligned span
         // (R is a multiple of 4): R*K/4 8-byte loads instead of R*K 2-byte
         // ones, which dominated the unit's prologue (~2.7 us at R*K = 72)
@@ -267,7 +276,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int64_t c = cbase + r;
-            const int64_t cc = c < C ? c : C - 1;
+            const int64_t cc = c < bend ? c : bend - 1;
 #pragma unroll
             for (int j = 0; j < KP; ++j) {
                 uint32_t lo = __ldg(items + cc * K + 2 * j);
@@ -328,7 +337,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
 #pragma unroll
         for (int o = 1; o < SUB; o <<= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
         const int64_t c = cbase + r;
-        if (sub == 0 && c < C && x) atomicAdd(out + c, (unsigned long long)x);
+        if (sub == 0 && c < bend && x) atomicAdd(out + c, (unsigned long long)x);
     }
     lab_stamp(4);
 }
