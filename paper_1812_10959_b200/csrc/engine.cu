@@ -687,6 +687,7 @@ struct GraphKey {
     const int64_t* sched;
     int64_t nsched;
     int64_t sched_first, sched_last;  // chunk sizing the pair kernel's grid
+    int64_t pair_live;                // the pair kernel is still in the count graph
     bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -1246,7 +1247,9 @@ int launch_count(dic_engine* e, int64_t lfirst, int64_t llast, const int64_t* sc
     const unsigned long long* seq = e->d_stat + S_SEQ;
     const int ring = (int)e->nsched;
     int rc;
-    if (e->tri) {
+    // once the host has seen the pair bucket leave dense mode (it never
+    // returns) the pair kernel, a no-op from then on, leaves the graph
+    if (e->tri && e->tri_live) {
         // the pair kernel's grain counters live past the triangle (tri[tri_len..+2));
         // fused reduction: this rank's partial triangle in its symmetric window
         unsigned long long* tri = e->fused ? e->tri_p : e->tri;
@@ -1271,6 +1274,7 @@ GraphKey graph_key(const dic_engine* e, bool with_sched) {
     k.kuse = e->kuse_issue;
     k.delta = e->delta;
     k.delta_p = e->delta_p;
+    k.pair_live = e->tri && e->tri_live;
     k.keep = e->keep;
     k.frontier = e->frontier;
     k.tmp_mask = e->tmp_mask;

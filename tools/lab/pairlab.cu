@@ -909,12 +909,11 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, 0));
     printf("m %d rows %lld tiles %lld pairs %lld; roofline ops %.3e\n", m, (long long)rows, (long long)nt,
            (long long)c.tri_len, c.ops);
-    run_static<TW, 3, 0, false, 2, false>("v0 ref (2st sync)", c);
-    run_v2<TW, 3, 1, 3, 2, 1, 70>("w2 v2 imad tps1 st3", c);
-    run_v2<TW, 3, 1, 3, 1, 1, 0, 1>("q1 persm gr1 imad st3", c);
-    run_v2<TW, 3, 1, 3, 2, 1, 0, 1>("q2 persm gr2 imad st3", c);
-    run_v2<TW, 3, 0, 3, 1, 1, 0, 1>("q3 persm gr1 iadd st3", c);
-    run_v2<TW, 3, 1, 4, 1, 1, 0, 1>("q4 persm gr1 imad st4", c);
-    run_v2<TW, 3, 1, 2, 1, 1, 0, 1>("q5 persm gr1 imad st2", c);
+    run_dyn<TW, 3, 1, true, 3, 2, 4, 4, 50>("t44 256thr minb3", c);
+    run_dyn<TW, 4, 1, true, 3, 2, 4, 8, 50>("t48 128thr minb4", c);
+    run_dyn<TW, 2, 1, true, 3, 2, 2, 4, 50>("t24 512thr minb2", c);
+    run_dyn<TW, 2, 1, true, 3, 2, 4, 2, 50>("t42 512thr minb2", c);
+    run_dyn<TW, 1, 1, true, 3, 2, 2, 2, 50>("t22 1024thr minb1", c);
+    run_dyn<TW, 2, 1, true, 3, 2, 8, 4, 50>("t84 128thr minb2", c);
     return 0;
 }
