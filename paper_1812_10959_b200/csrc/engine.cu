@@ -445,14 +445,17 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                     x &= x - 1;
                 }
             }
-            if (ht_find_items(ht, hmask, R, W, hc, its, k, l, -1, k + 1) >= 0) continue;  // already known
+            // the subset test rejects almost every join (its first subset
+            // is rarely a box yet), so it runs before the "already known"
+            // lookup; the admitted set is the same in either order
             for (int q = 0; q < k && ok; ++q) {
                 const int d = its[q];
                 const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, k, l, d, k);
                 ok = e >= 0 && is_box(R.shape[e]);
             }
+            if (!ok) continue;
+            if (ht_find_items(ht, hmask, R, W, hc, its, k, l, -1, k + 1) >= 0) continue;  // already known
         } else {
-        if (ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
         for (int w = 0; w < W && ok; ++w) {
             unsigned long long x = cand.word(w);
             while (x) {
@@ -467,6 +470,7 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                 }
             }
         }
+        if (ok && ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
         }
         if (!ok) continue;
         const unsigned long long pos = atomicAdd(&stat[S_NADM], 1ull);

@@ -197,10 +197,13 @@ def test_audit_mode_is_legal_and_equal():
         assert {(o, nw) for _, o, nw in audit.transitions} <= dic.LEGAL_TRANSITIONS
 
 
-@pytest.mark.parametrize("seed", range(8))
-def test_random_wide_engine_matches_oracle(seed):
+@pytest.mark.parametrize("seed,m_fixed", [(s, None) for s in range(8)] + [(100, 1100), (101, 1600)])
+def test_random_wide_engine_matches_oracle(seed, m_fixed):
+    """m_fixed > 1024: masks of more than 16 words take the generic (mask
+    view) candidate evaluation; at 1600 items a double-buffered tile no
+    longer fits shared memory and the counts take the unstaged path."""
     rng = np.random.default_rng(seed)
-    m = int(rng.choice([65, 130, 257, 700, 1000, 1200]))
+    m = m_fixed or int(rng.choice([65, 130, 257, 700, 1000, 1200]))
     n = int(rng.integers(200, 6000))
     hot = rng.choice(m, size=8, replace=False)
     W = (m + 63) // 64
