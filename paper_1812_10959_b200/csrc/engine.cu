@@ -256,6 +256,7 @@ struct PairArgs {  // the dense pair triangle (tri == nullptr: none)
     const int32_t* rank;
     uint16_t* const* items_tab;
     int64_t L, tri_len;
+    int64_t rec0;  // record id of seeded pair 0: pair p = record rec0 + p = triangle slot p
 };
 
 __device__ __forceinline__ int64_t tri_pos(int64_t a, int64_t b, int64_t L) {
@@ -285,8 +286,14 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
             int64_t dg = (int64_t)delta[g];
             delta[g] = 0;  // the buffer is zero again for the next stop's count
             if (bk == 2 && dense) {
-                const uint16_t* it = pa.items_tab[2] + 2 * c;
-                const int64_t p = tri_pos(pa.rank[it[0]], pa.rank[it[1]], pa.L);
+                // until the bucket is first compacted, slot c still holds the
+                // seeded pair c (record rec0 + c, triangle slot c): no item /
+                // rank lookups on the dependent-load chain
+                int64_t p = c;
+                if ((int64_t)r != pa.rec0 + c) {
+                    const uint16_t* it = pa.items_tab[2] + 2 * c;
+                    p = tri_pos(pa.rank[it[0]], pa.rank[it[1]], pa.L);
+                }
                 dg = (int64_t)pa.tri[p];
                 pa.tri[p] = 0;  // each pair has one slot: zero again for the next stop
             }
@@ -1156,7 +1163,7 @@ int launch_status(dic_engine* e, cudaStream_t s) {
 // compaction of the flagged buckets, make_candidates (device-sized,
 // all-or-nothing), status
 int launch_checkpoint(dic_engine* e, cudaStream_t s) {
-    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0};
+    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0, e->m};
     apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, s>>>(
         e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
         e->keep, e->d_stat, pa, e->KS);
