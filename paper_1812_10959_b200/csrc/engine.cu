@@ -1507,11 +1507,14 @@ extern "C" int dic_engine_set_comm(dic_engine* e, void* comm) {
                 reqs.lsaBarrierCount = kFusedCtas;
                 ncclDevComm dc;
                 r = ncclDevCommCreate(e->comm, &reqs, &dc);
-                if (r != ncclSuccess) return nccl_fail(r, "ncclDevCommCreate");
-                it = g_devcomm.emplace(e->comm, dc).first;
+                // no device API on this communicator (e.g. no symmetric
+                // memory support): keep the ncclAllReduce path
+                if (r == ncclSuccess) it = g_devcomm.emplace(e->comm, dc).first;
             }
-            e->devc = it->second;
-            e->fused = true;
+            if (it != g_devcomm.end()) {
+                e->devc = it->second;
+                e->fused = true;
+            }
         }
     }
     return DIC_OK;
