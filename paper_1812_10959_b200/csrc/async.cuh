@@ -95,14 +95,11 @@ __device__ __forceinline__ uint32_t and_popc8_acc(uint4 a0, uint4 a1, uint4 b0, 
     const uint32_t s2 = lop3_xor3(x3, x4, x5), c2 = lop3_maj(x3, x4, x5);
     const uint32_t s3 = lop3_xor3(s1, s2, x6), c3 = lop3_maj(s1, s2, x6);
     const uint32_t t = lop3_xor3(c1, c2, c3), f = lop3_maj(c1, c2, c3);
-#ifdef DIC_PAIR_IADD
-    return acc + __popc(s3) + __popc(x7) + 2u * __popc(t) + 4u * __popc(f);
-#else
+    // (an IADD3 combine measured 1-3 % slower on a cfg4 chunk: tools/lab/pair_ab.sh)
     acc = imad_u32(__popc(s3), one, acc);
     acc = imad_u32(__popc(x7), one, acc);
     acc = imad_u32(__popc(t), 2u, acc);
     return imad_u32(__popc(f), 4u, acc);
-#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
