@@ -50,6 +50,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-bench", action="store_true")
+    ap.add_argument("--no-config-sweep", action="store_true", help="skip the cfg1-3 GPU vs CPU-oracle sweep")
     ap.add_argument("--clock-ms", type=int, default=500, help="nvidia-smi sampling period in the timed region")
     ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
     ap.add_argument("--step-trace", action="store_true", help="per-step host phase / loop diagnostics in the JSON")
@@ -507,6 +508,9 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, db, params)
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_config_sweep:
+        sweep = config_sweep()
     kernel = None
     if rank == 0 and world == 1 and not args.no_kernel_bench:
         del db, tids
@@ -531,11 +535,59 @@ def main() -> None:
             "host_phases_ms": {k: round(v, 3) for k, v in trace.phases.items()},
             **({"step_diag": step_diag} if step_diag else {}),
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
-            "cpu_baseline": cpu, "kernel_microbench": kernel,
+            "cpu_baseline": cpu, "kernel_microbench": kernel, "config_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def config_sweep(reps: int = 5) -> dict:
+    """BASELINE.json cfg1-3 (the parity configs) at full size: the GPU DIC
+    (HBM-resident bitmap -> sorted results, min of `reps` after a warm-up)
+    against the oracle port mining the same rows on all host cores, with the
+    frequent sets checked equal (bit-exact itemsets and supports)."""
+    import torch
+
+    import paper_1812_10959_b200 as dic
+    from oracle import oracle as O
+    from paper_1812_10959_b200.miner import StopTrace, run_engine
+    from paper_1812_10959_b200.workloads import CONFIGS, generate_csr
+
+    cores = os.cpu_count() or 1
+    out = {}
+    for idx in (1, 2, 3):
+        cfg = CONFIGS[idx]
+        ip, ix = generate_csr(cfg)
+        db = dic.BitDatabase.from_csr(ip, ix, cfg.m)
+        tids = db.device_tids()
+        params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+        trace = StopTrace()
+        res = run_engine(tids, cfg.n, cfg.m, params, trace=trace)
+        tests = subset_tests(cfg.n, cfg.m, params, trace)
+        best = 1e30
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = run_engine(tids, cfg.n, cfg.m, params)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        rows = db.rows
+        t = time.perf_counter()
+        want = O.mine(rows, cfg.m, cfg.minsup, interval=cfg.interval, threads=cores)
+        cpu_s = time.perf_counter() - t
+        same = [(f.mask, f.size, f.support) for f in res.frequent] == want.frequent
+        out[cfg.name] = {"n": cfg.n, "m": cfg.m, "minsup": cfg.minsup, "interval": cfg.interval,
+                         "stops": len(trace.stops), "frequent_itemsets": len(res.frequent),
+                         "subset_tests": tests, "gpu_ms": best, "gpu_subset_tests_per_s": tests / (best * 1e-3),
+                         "cpu_oracle_s": cpu_s, "cpu_cores": cores,
+                         "cpu_subset_tests_per_s": tests / cpu_s, "speedup": cpu_s * 1e3 / best,
+                         "bit_exact_vs_oracle": same}
+        del db, tids, rows
+        torch.cuda.empty_cache()
+    return out
 
 
 def cpu_baseline(cfg, db, params) -> dict:
