@@ -7,6 +7,7 @@ import os
 import shutil
 import subprocess
 import sys
+import sysconfig
 from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
@@ -44,6 +45,9 @@ if NCCL_HOME is None:
     raise RuntimeError("libdicb200 needs NCCL >= 2.28 headers (nccl_device.h); pip package nvidia-nccl not found")
 NCCL_INC = ["-I", str(NCCL_HOME / "include")]
 NCCL_LINK = ["-L", str(NCCL_HOME / "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + str(NCCL_HOME / "lib")]
+
+# the CPython result builder (csrc/pyresults.c), next to the library
+PY_EXT = LIBDIR / ("_dicpy" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 
 CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "containment.cu", "probe.cu"]
 CPP_SOURCES = ["synth.cpp", "textio.cpp"]
@@ -85,6 +89,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
             for cmd, _ in zip(jobs, ex.map(_run, jobs)):
                 if verbose:
                     print(" ".join(cmd), file=sys.stderr)
+    pysrc = CSRC / "pyresults.c"
+    if force or not PY_EXT.exists() or PY_EXT.stat().st_mtime < pysrc.stat().st_mtime:
+        cc = shutil.which("gcc") or "gcc"
+        tmp = PY_EXT.with_name(PY_EXT.name + ".tmp")
+        _run([cc, "-O3", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"], str(pysrc), "-o",
+              str(tmp)])
+        os.replace(tmp, PY_EXT)
     if force or jobs or not LIB.exists():
         tmp = LIB.with_suffix(".so.tmp")
         _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", *NCCL_LINK])
