@@ -1114,7 +1114,7 @@ int ensure_tmp(dic_engine* e, int64_t want) {
 }
 
 // Headroom for the stops in flight: >= 64k join slots and record / hash room,
-// every bucket of size >= 3 in use with room to grow by half (>= 4096), the
+// every bucket of size >= 3 in use (and the next three) with room to grow by half (>= 4096), the
 // next size up allocated, slot arrays covering the capacities.
 int ensure_headroom(dic_engine* e) {
     int rc;
@@ -1126,7 +1126,10 @@ int ensure_headroom(dic_engine* e) {
     int top = 2;
     for (int k = 2; k < e->KS; ++k)
         if (e->buckets[k].n > 0) top = k;
-    for (int k = 3; k <= std::min(top + 1, e->KS - 1); ++k) {  // pairs are only ever seeded
+    // sizes up to three above the largest live one: with stops in flight a
+    // new level can spawn the next before the host sees it (each miss is an
+    // abort + replay round trip)
+    for (int k = 3; k <= std::min(top + 3, e->KS - 1); ++k) {  // pairs are only ever seeded
         const Bucket& b = e->buckets[k];
         const int64_t want = b.n + std::max<int64_t>(4096, b.n / 2);
         if (want > b.cap && (rc = grow_bucket(e, k, want, &changed))) return rc;
