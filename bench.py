@@ -375,8 +375,10 @@ def main() -> None:
 
     # pinned host CSR (the e2e input) and the HBM-resident bit-sliced copy
     # pinned host CSR (the e2e input): item ids as uint16 (the universe is
-    # < 65536), the form BitDatabase.from_csr streams to the encoder
-    h_indptr = torch.from_numpy(indptr).pin_memory()
+    # < 65536) and int32 offsets (nnz < 2^31), the compact form
+    # BitDatabase.from_csr streams to the encoder
+    off_dtype = np.int32 if int(indptr[-1]) < 2**31 else np.int64
+    h_indptr = torch.from_numpy(indptr.astype(off_dtype)).pin_memory()
     h_indices = torch.from_numpy(indices.astype(np.uint16)).pin_memory()
     db = dic.BitDatabase.from_csr(h_indptr, h_indices, cfg.m)
     tids = db.device_tids()

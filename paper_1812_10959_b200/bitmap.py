@@ -84,7 +84,8 @@ class BitDatabase:
         """Encode CSR item lists (host or device arrays) on the GPU, straight
         into the bit-sliced tiles the count kernels stream.
 
-        ``indptr`` int64 [n+1]; ``indices`` uint16 (any universe up to
+        ``indptr`` int64 or int32 [n+1] (int32 halves its PCIe bytes; it is
+        widened on the device); ``indices`` uint16 (any universe up to
         MAX_ITEMS fits) or int32 ids.  Host inputs are copied in ``slabs``
         tile-aligned row slabs on a side stream, each slab encoded as soon as
         it lands (pinned host tensors make the copies asynchronous).
@@ -101,7 +102,7 @@ class BitDatabase:
             raise ValueError(f"item universe size must be in [1, {MAX_ITEMS}], got {m}")
         ip = indptr if isinstance(indptr, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(indptr))
         ix = indices if isinstance(indices, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(indices))
-        if ip.dtype != torch.int64:
+        if ip.dtype not in (torch.int64, torch.int32):
             ip = ip.to(torch.int64)
         if ix.dtype not in (torch.uint16, torch.int32):
             ix = ix.to(torch.int32)
@@ -112,14 +113,14 @@ class BitDatabase:
         status = torch.empty(4, dtype=torch.int64, device="cuda")
         D.encode_status_init(status)
         if ix.is_cuda:
-            dip = ip.cuda(non_blocking=True)
+            dip = ip.cuda(non_blocking=True).to(torch.int64)
             D.encode_csr_tids(dip, ix, n, m, 0, n, tids, status)
             dix = ix
         else:
             # slab pipeline: H2D of slab i+1 on a copy stream overlaps the
             # encode of slab i on the current stream
             host_ip = ip.numpy() if not ip.is_cuda else ip.cpu().numpy()
-            dip = ip.cuda(non_blocking=True)
+            dip = ip.cuda(non_blocking=True).to(torch.int64)  # int32 offsets widen on the device
             dix = torch.empty(max(int(ix.numel()), 1), dtype=ix.dtype, device="cuda")
             rpt = D.tile_groups(m) * 32
             per = -(-n // max(slabs, 1))  # ceil(n / slabs) rows, rounded up to whole tiles

@@ -145,6 +145,12 @@ def test_from_csr_host_slabs_equal_device_path():
     dev = dic.BitDatabase.from_csr(to_dev(indptr), to_dev(ids.astype(np.int32)), m)
     assert torch.equal(host.device_tids(), dev.device_tids())
     assert np.array_equal(host.rows, dev.rows)
+    # int32 offsets (half the PCIe bytes; widened on the device), host and device
+    h32 = dic.BitDatabase.from_csr(torch.from_numpy(indptr.astype(np.int32)).pin_memory(),
+                                   torch.from_numpy(ids).pin_memory(), m, slabs=5)
+    d32 = dic.BitDatabase.from_csr(to_dev(indptr.astype(np.int32)), to_dev(ids), m)
+    assert torch.equal(h32.device_tids(), host.device_tids())
+    assert torch.equal(d32.device_tids(), host.device_tids())
     with pytest.raises(dic.ItemOutOfRange) as ei:
         bad = ids.copy()
         bad[int(indptr[4321]) + 1] = 1000
