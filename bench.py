@@ -236,15 +236,16 @@ def pair_kernel_roofline(tids, n: int, m: int, interval: int, peaks: dict, reps:
     first, last = 0, min(interval, n) - 1
     D.count_pairs(tids, n, m, first, last, tri)
     torch.cuda.synchronize()
-    ms = []
+    # `reps` launches back to back between two events on the launching
+    # stream: the average launch duration, without the host's per-call
+    # launch latency (the engine launches it from CUDA graphs)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
         D.count_pairs(tids, n, m, first, last, tri)
-        e1.record()
-        torch.cuda.synchronize()
-        ms.append(e0.elapsed_time(e1))
-    t = sum(ms) / len(ms)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps
     words = (last - first + 1 + 31) // 32
     ops = 2.0 * tri.numel() * words  # k = 2
     rows = last - first + 1
