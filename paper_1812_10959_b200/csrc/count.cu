@@ -215,7 +215,7 @@ __device__ __forceinline__ uint32_t popc4_csa(uint4 v) {
 // two per register (the row offset is one IMAD away) so a CTA still holds
 // rl_slots x R candidates; each lane's partial count is reduced over its SUB
 // lanes once per unit.
-__host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 24 : (K <= 6 ? 16 : 12)); }
+__host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 28 : (K <= 6 ? 20 : 12)); }
 static_assert(rl_regs(1) % 4 == 0 && rl_regs(3) % 4 == 0 && rl_regs(5) % 4 == 0 && rl_regs(7) % 4 == 0,
               "row-lane id spans are loaded 8 bytes at a time");
 __host__ __device__ constexpr int rl_slots(int TW) { return kStreamThreads / (TW / 4); }  // candidate slots per CTA row
