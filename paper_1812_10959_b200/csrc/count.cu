@@ -215,8 +215,15 @@ __device__ __forceinline__ uint32_t popc4_csa(uint4 v) {
 // two per register (the row offset is one IMAD away) so a CTA still holds
 // rl_slots x R candidates; each lane's partial count is reduced over its SUB
 // lanes once per unit.
-__host__ __device__ constexpr int rl_regs(int K) { return K <= 2 ? 32 : (K <= 4 ? 28 : (K <= 6 ? 20 : 12)); }
-static_assert(rl_regs(1) % 4 == 0 && rl_regs(3) % 4 == 0 && rl_regs(5) % 4 == 0 && rl_regs(7) % 4 == 0,
+__host__ __device__ constexpr int rl_regs(int K, int TW) {
+    return TW == 32 ? (K <= 4 ? 32 : (K == 5 ? 20 : (K == 6 ? 24 : 12)))   // cfg5-shaped (m <= 768)
+                    : (K <= 2 ? 32 : (K <= 4 ? 28 : (K <= 6 ? 20 : 12)));  // cfg4's m = 1000 stops
+}
+// (tuned per size on cfg5 with tools/lab/count_ab.sh; register allocation
+// across the per-size instantiations does not make this monotone)
+static_assert(rl_regs(1, 32) % 4 == 0 && rl_regs(5, 32) % 4 == 0 && rl_regs(6, 32) % 4 == 0 &&
+                  rl_regs(7, 32) % 4 == 0 && rl_regs(3, 16) % 4 == 0 && rl_regs(5, 16) % 4 == 0 &&
+                  rl_regs(7, 16) % 4 == 0,
               "row-lane id spans are loaded 8 bytes at a time");
 __host__ __device__ constexpr int rl_slots(int TW) { return kStreamThreads / (TW / 4); }  // candidate slots per CTA row
 
@@ -225,7 +232,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
                                                const ChunkGeom& geom, const uint16_t* __restrict__ items, int64_t C,
                                                unsigned long long* __restrict__ out, int64_t blk, int64_t t0,
                                                int64_t t1, uint8_t* smem, uint32_t (&uses)[2]) {
-    constexpr int RB = (TW + 4) * 4, R = rl_regs(K), KP = (K + 1) / 2, SUB = TW / 4;
+    constexpr int RB = (TW + 4) * 4, R = rl_regs(K, TW), KP = (K + 1) / 2, SUB = TW / 4;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
     const int sub = threadIdx.x & (SUB - 1), slot = threadIdx.x / SUB;
@@ -361,7 +368,7 @@ __device__ __forceinline__ void dispatch_unit_rl(int k, const uint32_t* tids, in
 
 // candidates per block of the unit kind used for (TW, k)
 __host__ __device__ inline int64_t cands_per_block(int TW, int k, bool rowlanes) {
-    if (rowlanes && k <= 8) return (int64_t)rl_slots(TW) * rl_regs(k);
+    if (rowlanes && k <= 8) return (int64_t)rl_slots(TW) * rl_regs(k, TW);
     return (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
 }
 
