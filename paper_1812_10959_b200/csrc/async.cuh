@@ -42,12 +42,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// carry-save adder: a + b + c == s + 2*c_out, bitwise (two LOP3s)
-__device__ __forceinline__ void csa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cout) {
-    s = a ^ b ^ c;
-    cout = (a & b) | (b & c) | (a & c);
-}
-
 __device__ __forceinline__ uint32_t lop3_xor3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -64,23 +58,11 @@ __device__ __forceinline__ uint32_t lop3_and(uint32_t a, uint32_t b) {
     return d;
 }
 
-// sum_w popc(a_w & b_w) over 8 words with a carry-save tree: 16 LOP3 + 4 POPC
-// (7 terms -> ones/twos/fours, plus one leftover word)
-__device__ __forceinline__ uint32_t and_popc8(uint4 a0, uint4 a1, uint4 b0, uint4 b1) {
-    const uint32_t x0 = lop3_and(a0.x, b0.x), x1 = lop3_and(a0.y, b0.y), x2 = lop3_and(a0.z, b0.z);
-    const uint32_t x3 = lop3_and(a0.w, b0.w), x4 = lop3_and(a1.x, b1.x), x5 = lop3_and(a1.y, b1.y);
-    const uint32_t x6 = lop3_and(a1.z, b1.z), x7 = lop3_and(a1.w, b1.w);
-    const uint32_t s1 = lop3_xor3(x0, x1, x2), c1 = lop3_maj(x0, x1, x2);
-    const uint32_t s2 = lop3_xor3(x3, x4, x5), c2 = lop3_maj(x3, x4, x5);
-    const uint32_t s3 = lop3_xor3(s1, s2, x6), c3 = lop3_maj(s1, s2, x6);
-    const uint32_t t = lop3_xor3(c1, c2, c3), f = lop3_maj(c1, c2, c3);
-    return __popc(s3) + __popc(x7) + 2u * __popc(t) + 4u * __popc(f);
-}
-
-// acc + sum_w popc(a_w & b_w) with the same tree; the four weighted adds go
-// through IMAD with a runtime 1 (`one`), i.e. onto the FMA pipe, which the
-// pair kernel otherwise leaves idle, instead of IADD3 on the ALU pipe the
-// LOP3s saturate
+// acc + sum_w popc(a_w & b_w) over 8 words with a carry-save tree: 16 LOP3 +
+// 4 POPC (7 terms -> ones/twos/fours, plus one leftover word).  The four
+// weighted adds go through IMAD with a runtime 1 (`one`), i.e. onto the FMA
+// pipe, which the pair kernel otherwise leaves idle, instead of IADD3 on the
+// ALU pipe the LOP3s saturate
 __device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
