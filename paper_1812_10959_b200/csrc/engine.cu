@@ -2034,15 +2034,36 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
         }
     }
     std::vector<int64_t> idx(F);
-    std::iota(idx.begin(), idx.end(), 0);
-    const uint64_t* kp = keys.data();
-    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
-        const uint64_t* x = kp + (size_t)a * KW;
-        const uint64_t* y = kp + (size_t)b * KW;
-        for (int q = 0; q < KW; ++q)
-            if (x[q] != y[q]) return x[q] < y[q];
-        return false;
-    });
+    if (KW <= 3) {
+        // itemsets of up to 8 items (every config): keys sorted in place as
+        // 32-byte records (key words + index), not through an index array
+        struct Rec {
+            uint64_t k[3];
+            int64_t i;
+        };
+        std::vector<Rec> recs((size_t)F);
+        for (int64_t i = 0; i < F; ++i) {
+            Rec& r = recs[(size_t)i];
+            for (int q = 0; q < 3; ++q) r.k[q] = q < KW ? keys[(size_t)i * KW + q] : 0;
+            r.i = i;
+        }
+        std::sort(recs.begin(), recs.end(), [](const Rec& a, const Rec& b) {
+            if (a.k[0] != b.k[0]) return a.k[0] < b.k[0];
+            if (a.k[1] != b.k[1]) return a.k[1] < b.k[1];
+            return a.k[2] < b.k[2];
+        });
+        for (int64_t i = 0; i < F; ++i) idx[(size_t)i] = recs[(size_t)i].i;
+    } else {
+        std::iota(idx.begin(), idx.end(), 0);
+        const uint64_t* kp = keys.data();
+        std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+            const uint64_t* x = kp + (size_t)a * KW;
+            const uint64_t* y = kp + (size_t)b * KW;
+            for (int q = 0; q < KW; ++q)
+                if (x[q] != y[q]) return x[q] < y[q];
+            return false;
+        });
+    }
     for (int64_t i = 0; i < F; ++i) {
         const int64_t j = idx[i];
         memcpy(masks_host + (size_t)i * W, m1 + (size_t)j * W, W * sizeof(uint64_t));
