@@ -407,6 +407,18 @@ def main() -> None:
     trace = StopTrace()
     ref = one_run(trace=trace)
     tests = subset_tests(cfg.n, cfg.m, params, trace)
+    cross_check = None
+    if world > 1 and (trace.native or {}).get("collective") == "fused":
+        # the fused peer-memory reduction must agree with ncclAllReduce, bit
+        # for bit, before anything is timed (every rank runs both)
+        os.environ["DIC_FUSED_REDUCE"] = "0"
+        try:
+            alt = one_run()
+        finally:
+            os.environ.pop("DIC_FUSED_REDUCE", None)
+        same = [(f.mask, f.support) for f in alt.frequent] == [(f.mask, f.support) for f in ref.frequent]
+        assert same, "fused reduction disagrees with ncclAllReduce"
+        cross_check = "fused reduction == ncclAllReduce (frequent sets and supports)"
 
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -538,6 +550,7 @@ def main() -> None:
             "host_phases_ms": {k: round(v, 3) for k, v in trace.phases.items()},
             **({"step_diag": step_diag} if step_diag else {}),
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
+            "collective": (trace.native or {}).get("collective"), "collective_cross_check": cross_check,
             "cpu_baseline": cpu, "kernel_microbench": kernel, "config_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
