@@ -283,9 +283,12 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
             const int32_t r = rec_tab[bk][c];
             uint8_t sh = R.shape[r];
             bool kept = false;
-            int64_t dg = (int64_t)delta[g];
-            delta[g] = 0;  // the buffer is zero again for the next stop's count
-            if (bk == 2 && dense) {
+            int64_t dg = 0;
+            if (!(bk == 2 && dense)) {
+                // (dense pairs are counted into the triangle: their delta slots stay zero)
+                dg = (int64_t)delta[g];
+                delta[g] = 0;  // the buffer is zero again for the next stop's count
+            } else {
                 // until the bucket is first compacted, slot c still holds the
                 // seeded pair c (record rec0 + c, triangle slot c): no item /
                 // rank lookups on the dependent-load chain
