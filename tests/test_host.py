@@ -164,3 +164,29 @@ def test_config_shapes():
     ip, ix = generate_csr(scaled(CONFIGS[3], 20000))
     dens = np.diff(ip).mean() / 128
     assert 0.3 < dens < 0.45  # Beta(2,5) mean 0.286 plus planted groups
+
+
+def test_result_builder_matches_python_construction():
+    """csrc/pyresults.c builds MiningResult.frequent: the same FrequentItemset
+    tuples (Python ints of any width, LSW-first words) as the reference's
+    NamedTuple constructor would, for 1-word and wide masks, in input order."""
+    from paper_1812_10959_b200.miner import sorted_frequent
+    from paper_1812_10959_b200.phases import FrequentItemset
+
+    rng = np.random.default_rng(3)
+    for W in (1, 2, 16, 25):
+        F = 500
+        masks = rng.integers(0, 2**63, size=(F, W), dtype=np.uint64)
+        masks[::7] = 0
+        masks[::7, -1] = np.uint64(1) << np.uint64(63)  # the top bit of the top word
+        sizes = rng.integers(1, 9, size=F).astype(np.int32)
+        sups = rng.integers(0, 2**40, size=F).astype(np.int64)
+        got = sorted_frequent(masks, sizes, sups, presorted=True)
+        want = tuple(FrequentItemset(int(sum(int(masks[i, w]) << (64 * w) for w in range(W))), int(sizes[i]),
+                                     int(sups[i])) for i in range(F))
+        assert got == want
+        assert all(type(f) is FrequentItemset for f in got) and got[0]._fields == ("mask", "size", "support")
+    one = sorted_frequent(np.array([5, 3], dtype=np.uint64), np.array([2, 2], dtype=np.int32),
+                          np.array([7, 8], dtype=np.int64), presorted=True)
+    assert one == (FrequentItemset(5, 2, 7), FrequentItemset(3, 2, 8))
+    assert sorted_frequent(np.zeros((0, 4), dtype=np.uint64), np.zeros(0, np.int32), np.zeros(0, np.int64)) == ()
