@@ -316,6 +316,19 @@ int dic_engine_frequent(dic_engine* e, uint64_t* masks_host,
                         int64_t F);
 /* Words per mask of this engine (W = ceil(m/64)).                        */
 int dic_engine_words(dic_engine* e);
+/* Replicated layout.  The record ids and bucket positions a stop gives its
+ * new candidates are canonical: candidates of the stop are ordered by
+ * (size, item ids ascending) and numbered in that order, so they depend only
+ * on the set of candidates (never on thread timing), and compaction keeps
+ * order.  Every rank of a sharded run therefore holds the same slot layout
+ * and the slot-indexed delta / triangle reductions add counts of the same
+ * itemsets (the reference reduces per record, engine.py:268-270).
+ * Diagnostics: bucket k (itemsets of k items) as the device holds it now —
+ * *n filled slots (live and dead); with rec_host non-null, their record ids
+ * and item lists (items_host[n][k], ascending) are copied out (cap >= *n).
+ * Synchronises the engine's stream.                                        */
+int dic_engine_bucket(dic_engine* e, int32_t k, int32_t* rec_host,
+                      uint16_t* items_host, int64_t cap, int64_t* n);
 
 /* Synthetic generators (host, multithreaded, counter-based RNG) ---------
  * Seeded restatements of BASELINE.json's config generators (DESIGN.md

@@ -95,6 +95,7 @@ SIGNATURES: dict[str, tuple] = {
     "dic_engine_num_frequent": (C.c_int, [vp, P(i64)]),
     "dic_engine_frequent": (C.c_int, [vp, vp, vp, vp, i64]),
     "dic_engine_words": (C.c_int, [vp]),
+    "dic_engine_bucket": (C.c_int, [vp, i32, vp, vp, i64, P(i64)]),
     "dic_synth_zipf": (C.c_int, [vp, vp, C.c_int, i32, dbl, dbl, u64, C.c_int, P(vp)]),
     "dic_synth_quest": (C.c_int, [vp, vp, C.c_int, i32, i32, dbl, dbl, u64, C.c_int, P(vp)]),
     "dic_synth_dense": (C.c_int, [vp, vp, C.c_int, i32, i32, i32, dbl, u64, C.c_int, P(vp)]),

@@ -532,19 +532,32 @@ __device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap
     }
 }
 
-// Dedup + commit the admissible joins in one pass: the thread whose CAS
-// claims a hash slot for a mask creates the record, appends it to its size
-// bucket and publishes the record id in the slot; a thread meeting an
-// occupied slot compares masks (temporary entries: kTempFlag | tmp index)
-// and drops its join as a duplicate.  Records published in this kernel are
-// read through L2 (__ldcg): L1 is not coherent within a launch.
-__global__ void insert_commit_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
-                                     const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
-                                     Records R, hent_t* ht, uint64_t hmask, unsigned long long* stat, int KS,
-                                     int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
+// Candidate commit, in two kernels, with a CANONICAL result: the record ids
+// and bucket positions of a stop's new candidates depend only on the SET of
+// candidates, never on thread timing.  Sharded engines reduce their counts
+// slot by slot, so every rank must lay its buckets out identically
+// (the reference reduces per record, engine.py:268-270); with atomics
+// deciding the order, ranks would add up counts of different itemsets.
+//
+// 1. dedup: the thread whose CAS claims a hash slot for a mask owns that
+//    candidate (a temporary entry kTempFlag | join index until commit); a
+//    thread meeting an occupied slot compares masks and drops its join as a
+//    duplicate (all duplicates carry the same mask, so which join wins does
+//    not matter).  Owners are listed in win[] (in arbitrary order) and
+//    counted per size in ins_k[].  No record is published in this kernel, so
+//    a non-temporary entry always names a record of an earlier stop.
+// 2. order_commit: the owners are sorted by (size, item ids ascending) — the
+//    order of make_candidates' lexicographic joins, which also makes
+//    candidates sharing a prefix contiguous for the count kernel — and the
+//    i-th gets record id nrec + i and position bn[size] + (its rank within its
+//    size).  Then the records, bucket entries and hash entries are written.
+__global__ void dedup_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
+                             const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
+                             const Records R, hent_t* ht, uint64_t hmask, unsigned long long* stat,
+                             int64_t* __restrict__ tmp_slot, int32_t* __restrict__ win,
+                             unsigned long long* __restrict__ ins_k) {
     if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t na = (int64_t)stat[S_NADM];
-    unsigned long long* bn = stat + S_HEAD + 2 * KS;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t h = tmp_hash[t];
         const unsigned long long* mk = tmp_mask + t * W;
@@ -552,28 +565,9 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
         while (true) {
             const hent_t pe = atomicCAS(ht + slot, kEmptyEnt, hent(h, kTempFlag | (int32_t)t));
             if (pe == kEmptyEnt) {
-                const int64_t r = (int64_t)atomicAdd(&stat[S_NREC], 1ull);
-                atomicAdd(&stat[S_NINS], 1ull);
-                const int sz = tmp_size[t];
-                for (int w = 0; w < W; ++w) R.mask[r * W + w] = mk[w];
-                R.hash[r] = h;
-                R.size[r] = sz;
-                R.support[r] = 0;
-                R.intervals[r] = 0;
-                R.shape[r] = DASHED_CIRCLE;
-                const unsigned long long pos = atomicAdd(bn + sz, 1ull);
-                b_rec_tab[sz][pos] = (int32_t)r;
-                uint16_t* it = b_items_tab[sz] + (int64_t)pos * sz;
-                int j = 0;
-                for (int w = 0; w < W; ++w) {
-                    unsigned long long x = mk[w];
-                    while (x) {
-                        it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
-                        x &= x - 1;
-                    }
-                }
-                __threadfence();
-                atomicExch(ht + slot, hent(h, (int32_t)r));
+                tmp_slot[t] = (int64_t)slot;
+                win[atomicAdd(&stat[S_NINS], 1ull)] = (int32_t)t;
+                atomicAdd(&ins_k[tmp_size[t]], 1ull);
                 break;
             }
             const int32_t prev = hent_id(pe);
@@ -583,12 +577,237 @@ __global__ void insert_commit_kernel(int W, const unsigned long long* __restrict
                 same = tmp_hash[o] == h;
                 for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
             } else if (same) {
-                for (int w = 0; same && w < W; ++w) same = __ldcg(R.mask + (int64_t)prev * W + w) == mk[w];
+                for (int w = 0; same && w < W; ++w) same = R.mask[(int64_t)prev * W + w] == mk[w];
             }
-            if (same) break;  // duplicate of a join admitted by another thread
+            if (same) break;  // duplicate of a join owned by another thread
             slot = (slot + 1) & hmask;
         }
     }
+}
+
+// Sort key of a candidate: (size, first seven item ids), 16 bits per id, in
+// two words compared high word first; equal keys (size >= 8 sharing seven
+// ids) fall back to the masks, where the lexicographically smaller item list
+// is the one holding the lowest bit in which the two masks differ.
+struct CandKey {
+    unsigned long long hi, lo;
+    int32_t t;  // join index (tmp slot); -1 = padding, sorts last
+};
+
+__device__ __forceinline__ CandKey cand_key(const unsigned long long* __restrict__ tmp_mask,
+                                            const int32_t* __restrict__ tmp_size, int W, int32_t t) {
+    CandKey k;
+    k.t = t;
+    unsigned long long hi = (unsigned long long)(uint32_t)tmp_size[t] << 48, lo = 0;
+    const unsigned long long* mk = tmp_mask + (int64_t)t * W;
+    int j = 0;
+    for (int w = 0; w < W && j < 7; ++w) {
+        unsigned long long x = mk[w];
+        while (x && j < 7) {
+            const unsigned long long it = (unsigned long long)(w * 64 + __ffsll((long long)x) - 1);
+            x &= x - 1;
+            if (j < 3) hi |= it << (32 - 16 * j);
+            else lo |= it << (48 - 16 * (j - 3));
+            ++j;
+        }
+    }
+    k.hi = hi;
+    k.lo = lo;
+    return k;
+}
+
+__device__ __forceinline__ bool cand_less(const CandKey& a, const CandKey& b,
+                                          const unsigned long long* __restrict__ tmp_mask, int W) {
+    if (a.hi != b.hi) return a.hi < b.hi;
+    if (a.lo != b.lo) return a.lo < b.lo;
+    if (a.t == b.t) return false;
+    if (a.t < 0 || b.t < 0) return b.t < 0;  // padding last
+    const unsigned long long* x = tmp_mask + (int64_t)a.t * W;
+    const unsigned long long* y = tmp_mask + (int64_t)b.t * W;
+    for (int w = 0; w < W; ++w) {
+        const unsigned long long d = x[w] ^ y[w];
+        if (d) return (x[w] & (d & (~d + 1))) != 0;
+    }
+    return false;  // equal masks: impossible after dedup
+}
+
+constexpr int kOrderThreads = 512;
+constexpr int kOrderRun = 4096;  // candidates one CTA sorts in shared memory
+constexpr size_t kOrderSmem = (size_t)kOrderRun * sizeof(CandKey);
+
+// Bitonic sort of keys[0, npad) (npad a power of two) in shared memory.
+__device__ void bitonic_sort(CandKey* keys, int npad, const unsigned long long* __restrict__ tmp_mask, int W) {
+    for (int k = 2; k <= npad; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const bool up = (i & k) == 0;
+                    if (cand_less(keys[p], keys[i], tmp_mask, W) == up) {
+                        const CandKey x = keys[i];
+                        keys[i] = keys[p];
+                        keys[p] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Commit the candidate of rank `rank` (0-based over the stop's new candidates
+// in canonical order): record nrec0 + rank at bucket slot bn0[sz] + rank -
+// start[sz], then publish its record id in the hash slot it claimed.
+__device__ __forceinline__ void commit_rank(int W, int64_t rank, int32_t t,
+                                            const unsigned long long* __restrict__ tmp_mask,
+                                            const uint64_t* __restrict__ tmp_hash,
+                                            const int32_t* __restrict__ tmp_size,
+                                            const int64_t* __restrict__ tmp_slot, Records R, hent_t* ht,
+                                            int64_t nrec0, const int64_t* start, const int64_t* bn0,
+                                            int32_t* const* __restrict__ b_rec_tab,
+                                            uint16_t* const* __restrict__ b_items_tab) {
+    const int64_t r = nrec0 + rank;
+    const int sz = tmp_size[t];
+    const uint64_t h = tmp_hash[t];
+    const unsigned long long* mk = tmp_mask + (int64_t)t * W;
+    for (int w = 0; w < W; ++w) R.mask[r * W + w] = mk[w];
+    R.hash[r] = h;
+    R.size[r] = sz;
+    R.support[r] = 0;
+    R.intervals[r] = 0;
+    R.shape[r] = DASHED_CIRCLE;
+    const int64_t pos = bn0[sz] + (rank - start[sz]);
+    b_rec_tab[sz][pos] = (int32_t)r;
+    uint16_t* it = b_items_tab[sz] + pos * sz;
+    int j = 0;
+    for (int w = 0; w < W; ++w) {
+        unsigned long long x = mk[w];
+        while (x) {
+            it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
+            x &= x - 1;
+        }
+    }
+    ht[tmp_slot[t]] = hent(h, (int32_t)r);
+}
+
+// keys written by other CTAs of the launch: read through L2
+__device__ __forceinline__ CandKey ld_key(const CandKey* p) {
+    CandKey k;
+    k.hi = __ldcg(&p->hi);
+    k.lo = __ldcg(&p->lo);
+    k.t = __ldcg(&p->t);
+    return k;
+}
+
+// Number of keys of the sorted run [run, run + len) less than `key`.
+__device__ __forceinline__ int64_t run_lower_bound(const CandKey* __restrict__ run, int64_t len, const CandKey& key,
+                                                   const unsigned long long* __restrict__ tmp_mask, int W) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cand_less(ld_key(run + mid), key, tmp_mask, W)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// ins_k[0, kDoffMax): new candidates by size (dedup); ins_k[kDoffMax + 0/1]:
+// grid-barrier / last-CTA counters of the multi-run path.
+__global__ void __launch_bounds__(kOrderThreads) order_commit_kernel(
+    int W, const unsigned long long* __restrict__ tmp_mask, const uint64_t* __restrict__ tmp_hash,
+    const int32_t* __restrict__ tmp_size, const int64_t* __restrict__ tmp_slot, const int32_t* __restrict__ win,
+    CandKey* __restrict__ runs, Records R, hent_t* ht, unsigned long long* stat, int KS,
+    unsigned long long* ins_k, int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
+    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
+    const int64_t N = (int64_t)stat[S_NINS];
+    if (N == 0) return;
+    const bool single = N <= kOrderRun;
+    if (single && blockIdx.x != 0) return;
+    extern __shared__ __align__(16) uint8_t osm[];
+    CandKey* keys = reinterpret_cast<CandKey*>(osm);
+    __shared__ int64_t start[kDoffMax], bn0[kDoffMax];
+    __shared__ int64_t nrec0;
+    unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    const int top = KS < kDoffMax ? KS : kDoffMax;
+    // every CTA reads the pre-commit sizes before any CTA can update them
+    // (the update is made by the last CTA out)
+    if (threadIdx.x == 0) {
+        nrec0 = (int64_t)stat[S_NREC];
+        int64_t acc = 0;
+        for (int k = 0; k < top; ++k) {
+            start[k] = acc;
+            acc += (int64_t)ins_k[k];
+            bn0[k] = (int64_t)bn[k];
+        }
+    }
+    __syncthreads();
+    if (single) {
+        int npad = 1;
+        while (npad < N) npad <<= 1;
+        for (int i = threadIdx.x; i < npad; i += blockDim.x)
+            keys[i] = i < N ? cand_key(tmp_mask, tmp_size, W, win[i]) : CandKey{~0ull, ~0ull, -1};
+        __syncthreads();
+        bitonic_sort(keys, npad, tmp_mask, W);
+        for (int i = threadIdx.x; i < N; i += blockDim.x)
+            commit_rank(W, i, keys[i].t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0, b_rec_tab,
+                        b_items_tab);
+    } else {
+        // sorted runs of kOrderRun, then each candidate's rank = its place in
+        // its run + the number of smaller keys in every other run
+        const int64_t nruns = (N + kOrderRun - 1) / kOrderRun;
+        for (int64_t rn = blockIdx.x; rn < nruns; rn += gridDim.x) {
+            const int64_t b = rn * kOrderRun;
+            const int len = (int)min((int64_t)kOrderRun, N - b);
+            int npad = 1;
+            while (npad < len) npad <<= 1;
+            for (int i = threadIdx.x; i < npad; i += blockDim.x)
+                keys[i] = i < len ? cand_key(tmp_mask, tmp_size, W, win[b + i]) : CandKey{~0ull, ~0ull, -1};
+            __syncthreads();
+            bitonic_sort(keys, npad, tmp_mask, W);
+            for (int i = threadIdx.x; i < len; i += blockDim.x) runs[b + i] = keys[i];
+            __syncthreads();
+        }
+        // grid barrier (every CTA of this launch is resident: gridDim <= SMs)
+        unsigned long long* bar = ins_k + kDoffMax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&bar[0], 1ull);
+            while (*(volatile unsigned long long*)&bar[0] < gridDim.x) __nanosleep(64);
+            __threadfence();
+        }
+        __syncthreads();
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t rn = i / kOrderRun;
+            const CandKey key = ld_key(runs + i);
+            int64_t rank = i - rn * kOrderRun;
+            for (int64_t q = 0; q < nruns; ++q) {
+                if (q == rn) continue;
+                const int64_t b = q * kOrderRun;
+                rank += run_lower_bound(runs + b, min((int64_t)kOrderRun, N - b), key, tmp_mask, W);
+            }
+            commit_rank(W, rank, key.t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0, b_rec_tab,
+                        b_items_tab);
+        }
+        __shared__ int last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(&bar[1], 1ull) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!last) return;
+        if (threadIdx.x == 0) {
+            bar[0] = 0;
+            bar[1] = 0;
+        }
+    }
+    // sizes after the commit (one CTA: the single one, or the last one out)
+    __syncthreads();
+    for (int k = threadIdx.x; k < top; k += blockDim.x) {
+        if (ins_k[k]) bn[k] = (unsigned long long)(bn0[k] + (int64_t)ins_k[k]);
+        ins_k[k] = 0;
+    }
+    if (threadIdx.x == 0) stat[S_NREC] = (unsigned long long)(nrec0 + N);
 }
 
 // The stop's status into its (host-mapped, pinned) ring slot S_SEQ % kRing:
@@ -753,8 +972,11 @@ struct dic_engine {
     unsigned long long* tmp_mask = nullptr;
     uint64_t* tmp_hash = nullptr;
     int32_t* tmp_size = nullptr;
-    int64_t* tmp_slot = nullptr;
+    int64_t* tmp_slot = nullptr;          // hash slot claimed by each owning join (dedup)
+    int32_t* tmp_win = nullptr;           // owning joins, in claim order (dedup)
+    CandKey* tmp_runs = nullptr;          // sorted key runs (order_commit, > kOrderRun new candidates)
     int64_t tmp_cap = 0;
+    unsigned long long* ins_k = nullptr;  // [kDoffMax + 2] new candidates by size + order_commit counters
 
     // the pair bucket as a dense triangle over the frequent items (pairs.cu)
     const uint32_t* pair_tids = nullptr;  // tids restricted to level1 (or tids itself)
@@ -1108,9 +1330,12 @@ int ensure_tmp(dic_engine* e, int64_t want) {
     dfree(e->tmp_hash, e->s);
     dfree(e->tmp_size, e->s);
     dfree(e->tmp_slot, e->s);
+    dfree(e->tmp_win, e->s);
+    dfree(e->tmp_runs, e->s);
     int rc;
     if ((rc = dalloc(&e->tmp_mask, nc * e->W, e->s)) || (rc = dalloc(&e->tmp_hash, nc, e->s)) ||
-        (rc = dalloc(&e->tmp_size, nc, e->s)) || (rc = dalloc(&e->tmp_slot, nc, e->s)))
+        (rc = dalloc(&e->tmp_size, nc, e->s)) || (rc = dalloc(&e->tmp_slot, nc, e->s)) ||
+        (rc = dalloc(&e->tmp_win, nc, e->s)) || (rc = dalloc(&e->tmp_runs, nc, e->s)))
         return rc;
     e->tmp_cap = nc;
     return DIC_OK;
@@ -1142,15 +1367,34 @@ int ensure_headroom(dic_engine* e) {
     return DIC_OK;
 }
 
+// CTAs per SM of the join evaluation and dedup kernels (DIC_CAND_GRID; the
+// layout-determinism tests vary it: the committed layout must not change)
+static int cand_grid_per_sm() {
+    const char* env = getenv("DIC_CAND_GRID");
+    const int v = env && *env ? atoi(env) : 4;
+    return std::min(64, std::max(1, v));
+}
+
 int candidate_step(dic_engine* e, cudaStream_t s) {
-    const int G = sm_count() * 4;
+    const int G = sm_count() * cand_grid_per_sm();
     unsigned long long* st = e->d_stat;
     eval_candidates_kernel<<<G, 256, 0, s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
                                                  (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
                                                  e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap);
     ::dic::note_launch();
-    insert_commit_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht,
-                                               (uint64_t)e->hcap - 1, st, e->KS, e->d_brec, e->d_bitems);
+    dedup_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht, (uint64_t)e->hcap - 1, st,
+                                   e->tmp_slot, e->tmp_win, e->ins_k);
+    ::dic::note_launch();
+    static bool attr = false;
+    if (!attr) {
+        DIC_CUDA(cudaFuncSetAttribute(order_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kOrderSmem));
+        attr = true;
+    }
+    // one CTA per SM (all resident: the multi-run path has a grid barrier)
+    order_commit_kernel<<<sm_count(), kOrderThreads, kOrderSmem, s>>>(
+        e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->tmp_win, e->tmp_runs, e->R, e->ht, st, e->KS,
+        e->ins_k, e->d_brec, e->d_bitems);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("candidate_step");
     return DIC_OK;
@@ -1389,7 +1633,8 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     int rc = 0;
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
-        (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s))) {
+        (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s)) ||
+        (rc = dalloc(&e->ins_k, kDoffMax + 2, e->s))) {
         delete e;
         return rc;
     }
@@ -1407,6 +1652,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->ins_k, 0, (kDoffMax + 2) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
     cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
     cudaMemsetAsync(e->d_bcap, 0, KS * sizeof(int64_t), e->s);
@@ -1428,6 +1674,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
+    dfree(e->tmp_win, s); dfree(e->tmp_runs, s); dfree(e->ins_k, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
     if (!e->fused) dfree(e->tri, s);
     if (e->fused) {
@@ -1702,6 +1949,27 @@ extern "C" int dic_engine_pair_counts(dic_engine* e, void** ptr, int64_t* len) {
     DIC_REQUIRE(e && ptr && len, "dic_engine_pair_counts: null argument");
     *ptr = e->tri;
     *len = e->tri ? e->tri_len : 0;
+    return DIC_OK;
+}
+
+// Diagnostics: bucket k (record ids and item lists, live and dead slots) as
+// the device holds it now.  Synchronises the engine's stream.
+extern "C" int dic_engine_bucket(dic_engine* e, int32_t k, int32_t* rec_host, uint16_t* items_host, int64_t cap,
+                                 int64_t* n) {
+    DIC_REQUIRE(e && n && k >= 1 && k < e->KS, "dic_engine_bucket: bad arguments");
+    unsigned long long* pin = e->hres.ring + kRing * e->hres.words;
+    DIC_CUDA(cudaMemcpyAsync(pin, e->d_stat + S_HEAD + 2 * e->KS + k, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));
+    const int64_t fill = (int64_t)pin[0];
+    *n = fill;
+    if (fill == 0 || !rec_host) return DIC_OK;
+    DIC_REQUIRE(items_host && cap >= fill, "dic_engine_bucket: cap %lld < %lld slots", (long long)cap,
+                (long long)fill);
+    const Bucket& b = e->buckets[k];
+    DIC_CUDA(cudaMemcpyAsync(rec_host, b.rec, (size_t)fill * sizeof(int32_t), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaMemcpyAsync(items_host, b.items, (size_t)fill * k * sizeof(uint16_t), cudaMemcpyDeviceToHost, e->s));
+    DIC_CUDA(cudaStreamSynchronize(e->s));
     return DIC_OK;
 }
 

@@ -128,6 +128,17 @@ class DeviceEngine:
         """The per-stop dense pair-triangle counts (empty if none)."""
         return self._device_view("dic_engine_pair_counts")
 
+    def bucket(self, k: int) -> tuple[np.ndarray, np.ndarray]:
+        """Bucket k as the device holds it now: record ids [n] and item lists [n][k]
+        (live and dead slots; diagnostics, synchronising)."""
+        n = C.c_int64()
+        _abi.call("dic_engine_bucket", self.h, k, None, None, 0, C.byref(n))
+        rec = np.zeros(max(n.value, 1), dtype=np.int32)
+        items = np.zeros((max(n.value, 1), k), dtype=np.uint16)
+        if n.value:
+            _abi.call("dic_engine_bucket", self.h, k, rec.ctypes.data, items.ctypes.data, n.value, C.byref(n))
+        return rec[: n.value], items[: n.value]
+
     def issue_checkpoint(self) -> int:
         seq = C.c_int64()
         _abi.call("dic_engine_issue_checkpoint", self.h, C.byref(seq))
