@@ -137,11 +137,20 @@ int dic_count_support(const uint32_t* tids, int64_t n, int32_t m,
 /* All pairs at once: the 2-itemset bucket as a dense triangle ----------
  * For every pair of items a < b < m of a tids layout:
  *   tri[a*m - a*(a+1)/2 + (b-a-1)] += #{ j in [first, last] : row j holds a and b }
- * (a-major, the order first_pass seeds pairs in, engine.py:165-168).  A
- * register-blocked AND/POPC kernel over 64 x 64 blocks of the triangle; tri
- * holds m*(m-1)/2 uint64 counts and is accumulated into.                  */
+ * (a-major, the order first_pass seeds pairs in, engine.py:165-168).  The
+ * count is the Gram matrix X^T X of the chunk's 0/1 matrix: for m >= 128
+ * items it runs on the tensor cores (tcgen05.mma kind::i8, u8 operands
+ * expanded from the bits in shared memory, s32 accumulators in TMEM, exact);
+ * below that, or when selected, as a register-blocked AND/POPC kernel over
+ * 64 x 64 blocks.  tri holds m*(m-1)/2 uint64 counts, accumulated into.     */
 int dic_count_pairs(const uint32_t* tids, int64_t n, int32_t m,
                     int64_t first, int64_t last, uint64_t* tri, void* stream);
+/* Which kernel dic_count_pairs (and the engine's pair stops) use, process-
+ * wide: -1 = from the environment (DIC_PAIR_TC, default on), 0 = automatic
+ * (tensor cores for m >= 128), 1 = AND/POPC, 2 = tensor cores; *previous
+ * (optional) receives the mode it replaces.  Engines apply it when they next
+ * capture a stop graph.                                                    */
+int dic_pair_kernel_select(int32_t mode, int32_t* previous);
 /* The tids layout restricted to items[0..L) (in that order, L <= m); out
  * holds dic_tids_words(n, L) words.  Lets dic_count_pairs run over the
  * frequent items only.                                                    */

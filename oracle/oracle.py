@@ -34,7 +34,7 @@ class OrcStats(C.Structure):
 
 
 def build() -> Path:
-    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    subprocess.run(["make", "-s", "-C", str(HERE), "all"], check=True)
     return LIB
 
 
@@ -59,6 +59,12 @@ def load() -> C.CDLL:
         lib.orc_result_get.argtypes = [vp, vp, vp, vp]
         lib.orc_result_free.restype = None
         lib.orc_result_free.argtypes = [vp]
+        lib.orc_bernoulli_rows.restype = None
+        lib.orc_bernoulli_rows.argtypes = [i64, i64, C.c_int, C.c_double, C.c_uint64, vp]
+        lib.orc_bernoulli_cols.restype = C.c_int
+        lib.orc_bernoulli_cols.argtypes = [i64, C.c_int, C.c_double, C.c_uint64, vp, C.c_int]
+        lib.orc_count_cols.restype = C.c_int
+        lib.orc_count_cols.argtypes = [vp, i64, vp, vp, i64, C.c_int, vp, C.c_int]
         _lib = lib
     return _lib
 
@@ -156,3 +162,32 @@ def mine(rows: np.ndarray, m: int, minsup: float, interval: int | None = None, p
     freq = [(mask_from_words(masks[i]), int(sizes[i]), int(sups[i])) for i in range(F)]
     return OracleRun(freq, st.scanned / n, st.peak_dashed, st.candidates_generated, st.candidates_pruned,
                      st.interval_counts, st.stops)
+
+
+# ---------------------------------------------------------------- cfg5 (cfg5.c)
+def bernoulli_rows(r0: int, nrows: int, m: int, p: float, seed: int) -> np.ndarray:
+    """Rows [r0, r0 + nrows) of the cfg5 bitmap, uint64 [nrows][W] (the device
+    generator's hash restated on the host)."""
+    W = (m + 63) // 64
+    out = np.zeros((nrows, W), dtype=np.uint64)
+    load().orc_bernoulli_rows(r0, nrows, m, p, seed, out.ctypes.data)
+    return out
+
+
+def bernoulli_cols(n: int, m: int, p: float, seed: int, threads: int = 1) -> np.ndarray:
+    """The whole cfg5 bitmap column-wise: uint64 [m][ceil(n/64)], item i's bits of rows 64w..64w+63 in word w."""
+    cols = np.empty((m, (n + 63) // 64), dtype=np.uint64)
+    if load().orc_bernoulli_cols(n, m, p, seed, cols.ctypes.data, threads) != 0:
+        raise ValueError("orc_bernoulli_cols: bad arguments")
+    return cols
+
+
+def count_cols(cols: np.ndarray, items: np.ndarray, ks: np.ndarray, threads: int = 1) -> np.ndarray:
+    """Support of every candidate (items[c][:ks[c]]) over a column bitmap."""
+    cols = np.ascontiguousarray(cols, dtype=np.uint64)
+    items = np.ascontiguousarray(items, dtype=np.uint16)
+    ks = np.ascontiguousarray(ks, dtype=np.int32)
+    out = np.zeros(len(ks), dtype=np.int64)
+    load().orc_count_cols(cols.ctypes.data, cols.shape[1], items.ctypes.data, ks.ctypes.data, len(ks),
+                          items.shape[1], out.ctypes.data, threads)
+    return out

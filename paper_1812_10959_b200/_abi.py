@@ -64,6 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "dic_item_support": (C.c_int, [vp, i64, i32, i64, i64, vp, vp]),
     "dic_count_support": (C.c_int, [vp, i64, i32, i64, i64, vp, i32, i64, vp, vp]),
     "dic_count_pairs": (C.c_int, [vp, i64, i32, i64, i64, vp, vp]),
+    "dic_pair_kernel_select": (C.c_int, [i32, P(i32)]),
     "dic_tids_select": (C.c_int, [vp, i64, i32, vp, i32, vp, vp]),
     "dic_count_support_rows": (C.c_int, [vp, i32, i64, i64, vp, i64, vp, vp]),
     "dic_candidate_admission": (C.c_int, [vp, i64, vp, i64, i32, vp, i64, vp, i64, vp, vp]),

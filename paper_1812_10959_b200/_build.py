@@ -49,7 +49,7 @@ NCCL_LINK = ["-L", str(NCCL_HOME / "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpat
 # the CPython result builder (csrc/pyresults.c), next to the library
 PY_EXT = LIBDIR / ("_dicpy" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 
-CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "engine.cu", "containment.cu", "probe.cu"]
+CU_SOURCES = ["abi.cu", "encode.cu", "count.cu", "pairs.cu", "pairs_mma.cu", "engine.cu", "containment.cu", "probe.cu"]
 CPP_SOURCES = ["synth.cpp", "textio.cpp"]
 
 

@@ -14,6 +14,7 @@
 // operand block arrives by one bulk async copy (TMA engine), double-buffered.
 #include "async.cuh"
 
+#include <atomic>
 #include <map>
 #include <mutex>
 
@@ -360,6 +361,23 @@ int pair_launch(const uint32_t* tids, int m, ChunkGeom geom, int64_t t_first, in
     return DIC_OK;
 }
 
+int pair_tc_launch(const uint32_t* tids, int L, ChunkGeom geom, unsigned long long* tri, const unsigned long long* bn2,
+                   int64_t tri_len, const unsigned long long* abort_flag, const int64_t* chunk_ring,
+                   const unsigned long long* seq, int ring, cudaStream_t s);
+
+// The tensor-core triangle (pairs_mma.cu) for universes of at least
+// DIC_PAIR_TC_MIN items (default 128); DIC_PAIR_TC=0 keeps the LOP3/POPC
+// kernel.  dic_pair_kernel_select() overrides both (tests, A/B probes).
+static std::atomic<int> g_pair_mode{-1};  // -1: from the environment, 0: auto, 1: LOP3, 2: tensor cores
+static bool pair_use_tc(int m) {
+    static const int on = env_int("DIC_PAIR_TC", 1, 0, 1);
+    static const int lo = env_int("DIC_PAIR_TC_MIN", 128, 2, 1 << 16);
+    const int mode = g_pair_mode.load();
+    if (mode == 1) return false;
+    if (mode == 2) return true;
+    return (mode == 0 || on) && m >= lo;
+}
+
 int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                        unsigned long long* tri, cudaStream_t s, const unsigned long long* bn2 = nullptr,
                        int64_t tri_len = 0, const unsigned long long* abort_flag = nullptr,
@@ -367,6 +385,8 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
                        int ring = 0, unsigned long long* sched = nullptr) {
     // with a chunk ring, [first, last] only sizes the grid (the largest chunk)
     if (last < first || m < 2) return DIC_OK;
+    if (pair_use_tc(m))
+        return pair_tc_launch(tids, m, chunk_geom(first, last), tri, bn2, tri_len, abort_flag, chunk_ring, seq, ring, s);
     if (!sched && !(sched = stream_sched(s))) {
         set_error("dic_count_pairs: no device memory for the grain counters");
         return DIC_ENOMEM;
@@ -428,4 +448,11 @@ extern "C" int dic_tids_select(const uint32_t* tids, int64_t n, int32_t m, const
                                uint32_t* out, void* stream) {
     DIC_REQUIRE(n >= 1 && m >= 1 && L >= 1 && L <= m && tids && items && out, "dic_tids_select: bad arguments");
     return tids_select_launch(tids, n, m, items, L, out, as_stream(stream));
+}
+
+extern "C" int dic_pair_kernel_select(int32_t mode, int32_t* previous) {
+    DIC_REQUIRE(mode >= -1 && mode <= 2, "dic_pair_kernel_select: mode %d (-1 env, 0 auto, 1 LOP3, 2 tensor)", mode);
+    const int prev = g_pair_mode.exchange(mode);
+    if (previous) *previous = prev;
+    return DIC_OK;
 }

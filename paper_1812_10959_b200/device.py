@@ -136,6 +136,13 @@ def count_support(tids: torch.Tensor, n: int, m: int, first: int, last: int, ite
     return out
 
 
+def pair_kernel_select(mode: int) -> int:
+    """Process-wide pair-triangle kernel: -1 env, 0 auto, 1 AND/POPC, 2 tensor cores; returns the previous mode."""
+    prev = C.c_int32()
+    _abi.call("dic_pair_kernel_select", mode, C.byref(prev))
+    return prev.value
+
+
 def count_pairs(tids: torch.Tensor, n: int, m: int, first: int, last: int,
                 tri: torch.Tensor | None = None) -> torch.Tensor:
     """Counts of all pairs a < b < m over rows [first, last], a-major triangle (int64)."""
