@@ -520,13 +520,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __gr
     ChunkGeom geom;
     int64_t t_first, t_last;
     if (!dev_chunk(a, geom, t_first, t_last)) return;
+    // bucket fills loaded in parallel (a loop of dependent-latency loads in
+    // one thread would cost one L2 round trip per size)
+    if (threadIdx.x < a.kuse) cpref[threadIdx.x + 1] = (int64_t)a.bn[threadIdx.x];
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const bool dense = a.tri_len > 0 && 2 * (int64_t)a.bn[2] >= a.tri_len;
+        const bool dense = a.tri_len > 0 && 2 * cpref[3] >= a.tri_len;
         int64_t acc = 0, cacc = 0;
         pref[0] = 0;
         cpref[0] = 0;
         for (int k = 1; k < a.kuse; ++k) {
-            int64_t C = (int64_t)a.bn[k];
+            int64_t C = cpref[k + 1];
             if (k == 2 && dense) C = 0;
             const int64_t per = cands_per_block(TW, k, true);
             pref[k] = acc;

@@ -269,7 +269,12 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
                                             int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
                                             unsigned long long* __restrict__ stat, PairArgs pa, int KS) {
     if (stat[S_ABORT]) return;
-    const int64_t total = doff[kuse];
+    // the bucket offsets in shared memory: each slot's bucket search is then
+    // a few shared loads instead of a chain of dependent global ones
+    __shared__ int64_t sdoff[kDoffMax + 1];
+    for (int i = threadIdx.x; i <= kuse; i += blockDim.x) sdoff[i] = doff[i];
+    __syncthreads();
+    const int64_t total = sdoff[kuse];
     // pair counts come from the triangle while the pair bucket is dense
     const bool dense = pa.tri != nullptr && 2 * (int64_t)stat[S_HEAD + 2 * KS + 2] >= pa.tri_len;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -278,8 +283,8 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
         bool pruned = false, fin = false, surv = false, gone = false;
         int bk = 0;
         if (g < total) {
-            while (bk + 1 < kuse && g >= doff[bk + 1]) ++bk;
-            const int64_t c = g - doff[bk];
+            while (bk + 1 < kuse && g >= sdoff[bk + 1]) ++bk;
+            const int64_t c = g - sdoff[bk];
             const int32_t r = rec_tab[bk][c];
             uint8_t sh = R.shape[r];
             bool kept = false;
@@ -543,18 +548,67 @@ __device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap
 //    candidate (a temporary entry kTempFlag | join index until commit); a
 //    thread meeting an occupied slot compares masks and drops its join as a
 //    duplicate (all duplicates carry the same mask, so which join wins does
-//    not matter).  Owners are listed in win[] (in arbitrary order) and
-//    counted per size in ins_k[].  No record is published in this kernel, so
-//    a non-temporary entry always names a record of an earlier stop.
-// 2. order_commit: the owners are sorted by (size, item ids ascending) — the
-//    order of make_candidates' lexicographic joins, which also makes
+//    not matter).  Owners write their sort key to keys[] (in arbitrary order)
+//    and are counted per size in ins_k[].  No record is published in this
+//    kernel, so a non-temporary entry always names a record of an earlier stop.
+// 2. rank_commit_status: the owners are ranked by (size, item ids ascending)
+//    — the order of make_candidates' lexicographic joins, which also makes
 //    candidates sharing a prefix contiguous for the count kernel — and the
-//    i-th gets record id nrec + i and position bn[size] + (its rank within its
-//    size).  Then the records, bucket entries and hash entries are written.
+//    one of rank i gets record id nrec + i and position bn[size] + (its rank
+//    within its size); then the records, bucket entries and hash entries are
+//    written.  A rank is a count of smaller keys, one warp per candidate
+//    (N^2 / 32 warp steps spread over the GPU: a few microseconds for the
+//    hundreds of joins a stop commits; no sort, no serial phase).
+
+// Sort key of a candidate: (size, first seven item ids), 16 bits per id, in
+// two words compared high word first; equal keys (size >= 8 sharing seven
+// ids) fall back to the masks, where the lexicographically smaller item list
+// is the one holding the lowest bit in which the two masks differ.
+struct CandKey {
+    unsigned long long hi, lo;
+    int32_t t;  // join index (tmp slot)
+};
+
+__device__ __forceinline__ void key_take(int w, unsigned long long x, int& j, unsigned long long& hi,
+                                         unsigned long long& lo) {
+    while (x && j < 7) {
+        const unsigned long long it = (unsigned long long)(w * 64 + __ffsll((long long)x) - 1);
+        x &= x - 1;
+        if (j < 3) hi |= it << (32 - 16 * j);
+        else lo |= it << (48 - 16 * (j - 3));
+        ++j;
+    }
+}
+
+__device__ __forceinline__ CandKey cand_key(const unsigned long long* __restrict__ mk, int sz, int W, int32_t t) {
+    CandKey k;
+    k.t = t;
+    unsigned long long hi = (unsigned long long)(uint32_t)sz << 48, lo = 0;
+    int j = 0;
+    for (int w = 0; w < W && j < 7; ++w) key_take(w, mk[w], j, hi, lo);
+    k.hi = hi;
+    k.lo = lo;
+    return k;
+}
+
+__device__ __forceinline__ bool cand_less(const CandKey& a, const CandKey& b,
+                                          const unsigned long long* __restrict__ tmp_mask, int W) {
+    if (a.hi != b.hi) return a.hi < b.hi;
+    if (a.lo != b.lo) return a.lo < b.lo;
+    if (a.t == b.t) return false;
+    const unsigned long long* x = tmp_mask + (int64_t)a.t * W;
+    const unsigned long long* y = tmp_mask + (int64_t)b.t * W;
+    for (int w = 0; w < W; ++w) {
+        const unsigned long long d = x[w] ^ y[w];
+        if (d) return (x[w] & (d & (~d + 1))) != 0;
+    }
+    return false;  // equal masks: impossible after dedup
+}
+
 __global__ void dedup_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
                              const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
                              const Records R, hent_t* ht, uint64_t hmask, unsigned long long* stat,
-                             int64_t* __restrict__ tmp_slot, int32_t* __restrict__ win,
+                             int64_t* __restrict__ tmp_slot, CandKey* __restrict__ keys,
                              unsigned long long* __restrict__ ins_k) {
     if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t na = (int64_t)stat[S_NADM];
@@ -566,8 +620,9 @@ __global__ void dedup_kernel(int W, const unsigned long long* __restrict__ tmp_m
             const hent_t pe = atomicCAS(ht + slot, kEmptyEnt, hent(h, kTempFlag | (int32_t)t));
             if (pe == kEmptyEnt) {
                 tmp_slot[t] = (int64_t)slot;
-                win[atomicAdd(&stat[S_NINS], 1ull)] = (int32_t)t;
-                atomicAdd(&ins_k[tmp_size[t]], 1ull);
+                const int sz = tmp_size[t];
+                keys[atomicAdd(&stat[S_NINS], 1ull)] = cand_key(mk, sz, W, (int32_t)t);
+                atomicAdd(&ins_k[sz], 1ull);
                 break;
             }
             const int32_t prev = hent_id(pe);
@@ -585,92 +640,19 @@ __global__ void dedup_kernel(int W, const unsigned long long* __restrict__ tmp_m
     }
 }
 
-// Sort key of a candidate: (size, first seven item ids), 16 bits per id, in
-// two words compared high word first; equal keys (size >= 8 sharing seven
-// ids) fall back to the masks, where the lexicographically smaller item list
-// is the one holding the lowest bit in which the two masks differ.
-struct CandKey {
-    unsigned long long hi, lo;
-    int32_t t;  // join index (tmp slot); -1 = padding, sorts last
-};
-
-__device__ __forceinline__ CandKey cand_key(const unsigned long long* __restrict__ tmp_mask,
-                                            const int32_t* __restrict__ tmp_size, int W, int32_t t) {
-    CandKey k;
-    k.t = t;
-    unsigned long long hi = (unsigned long long)(uint32_t)tmp_size[t] << 48, lo = 0;
-    const unsigned long long* mk = tmp_mask + (int64_t)t * W;
-    int j = 0;
-    for (int w = 0; w < W && j < 7; ++w) {
-        unsigned long long x = mk[w];
-        while (x && j < 7) {
-            const unsigned long long it = (unsigned long long)(w * 64 + __ffsll((long long)x) - 1);
-            x &= x - 1;
-            if (j < 3) hi |= it << (32 - 16 * j);
-            else lo |= it << (48 - 16 * (j - 3));
-            ++j;
-        }
-    }
-    k.hi = hi;
-    k.lo = lo;
-    return k;
-}
-
-__device__ __forceinline__ bool cand_less(const CandKey& a, const CandKey& b,
-                                          const unsigned long long* __restrict__ tmp_mask, int W) {
-    if (a.hi != b.hi) return a.hi < b.hi;
-    if (a.lo != b.lo) return a.lo < b.lo;
-    if (a.t == b.t) return false;
-    if (a.t < 0 || b.t < 0) return b.t < 0;  // padding last
-    const unsigned long long* x = tmp_mask + (int64_t)a.t * W;
-    const unsigned long long* y = tmp_mask + (int64_t)b.t * W;
-    for (int w = 0; w < W; ++w) {
-        const unsigned long long d = x[w] ^ y[w];
-        if (d) return (x[w] & (d & (~d + 1))) != 0;
-    }
-    return false;  // equal masks: impossible after dedup
-}
-
-constexpr int kOrderThreads = 512;
-constexpr int kOrderRun = 4096;  // candidates one CTA sorts in shared memory
-constexpr size_t kOrderSmem = (size_t)kOrderRun * sizeof(CandKey);
-
-// Bitonic sort of keys[0, npad) (npad a power of two) in shared memory.
-__device__ void bitonic_sort(CandKey* keys, int npad, const unsigned long long* __restrict__ tmp_mask, int W) {
-    for (int k = 2; k <= npad; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-                const int p = i ^ j;
-                if (p > i) {
-                    const bool up = (i & k) == 0;
-                    if (cand_less(keys[p], keys[i], tmp_mask, W) == up) {
-                        const CandKey x = keys[i];
-                        keys[i] = keys[p];
-                        keys[p] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
 // Commit the candidate of rank `rank` (0-based over the stop's new candidates
 // in canonical order): record nrec0 + rank at bucket slot bn0[sz] + rank -
 // start[sz], then publish its record id in the hash slot it claimed.
-__device__ __forceinline__ void commit_rank(int W, int64_t rank, int32_t t,
-                                            const unsigned long long* __restrict__ tmp_mask,
-                                            const uint64_t* __restrict__ tmp_hash,
-                                            const int32_t* __restrict__ tmp_size,
-                                            const int64_t* __restrict__ tmp_slot, Records R, hent_t* ht,
-                                            int64_t nrec0, const int64_t* start, const int64_t* bn0,
-                                            int32_t* const* __restrict__ b_rec_tab,
-                                            uint16_t* const* __restrict__ b_items_tab) {
+__device__ __noinline__ void commit_rank(int W, int64_t rank, int32_t t, const unsigned long long* __restrict__ tmp_mask,
+                                         const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
+                                         const int64_t* __restrict__ tmp_slot, Records R, hent_t* ht, int64_t nrec0,
+                                         const int64_t* start, const int64_t* bn0,
+                                         int32_t* const* __restrict__ b_rec_tab,
+                                         uint16_t* const* __restrict__ b_items_tab) {
     const int64_t r = nrec0 + rank;
     const int sz = tmp_size[t];
     const uint64_t h = tmp_hash[t];
     const unsigned long long* mk = tmp_mask + (int64_t)t * W;
-    for (int w = 0; w < W; ++w) R.mask[r * W + w] = mk[w];
     R.hash[r] = h;
     R.size[r] = sz;
     R.support[r] = 0;
@@ -682,132 +664,13 @@ __device__ __forceinline__ void commit_rank(int W, int64_t rank, int32_t t,
     int j = 0;
     for (int w = 0; w < W; ++w) {
         unsigned long long x = mk[w];
+        R.mask[r * W + w] = x;
         while (x) {
             it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
             x &= x - 1;
         }
     }
     ht[tmp_slot[t]] = hent(h, (int32_t)r);
-}
-
-// keys written by other CTAs of the launch: read through L2
-__device__ __forceinline__ CandKey ld_key(const CandKey* p) {
-    CandKey k;
-    k.hi = __ldcg(&p->hi);
-    k.lo = __ldcg(&p->lo);
-    k.t = __ldcg(&p->t);
-    return k;
-}
-
-// Number of keys of the sorted run [run, run + len) less than `key`.
-__device__ __forceinline__ int64_t run_lower_bound(const CandKey* __restrict__ run, int64_t len, const CandKey& key,
-                                                   const unsigned long long* __restrict__ tmp_mask, int W) {
-    int64_t lo = 0, hi = len;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (cand_less(ld_key(run + mid), key, tmp_mask, W)) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// ins_k[0, kDoffMax): new candidates by size (dedup); ins_k[kDoffMax + 0/1]:
-// grid-barrier / last-CTA counters of the multi-run path.
-__global__ void __launch_bounds__(kOrderThreads) order_commit_kernel(
-    int W, const unsigned long long* __restrict__ tmp_mask, const uint64_t* __restrict__ tmp_hash,
-    const int32_t* __restrict__ tmp_size, const int64_t* __restrict__ tmp_slot, const int32_t* __restrict__ win,
-    CandKey* __restrict__ runs, Records R, hent_t* ht, unsigned long long* stat, int KS,
-    unsigned long long* ins_k, int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab) {
-    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
-    const int64_t N = (int64_t)stat[S_NINS];
-    if (N == 0) return;
-    const bool single = N <= kOrderRun;
-    if (single && blockIdx.x != 0) return;
-    extern __shared__ __align__(16) uint8_t osm[];
-    CandKey* keys = reinterpret_cast<CandKey*>(osm);
-    __shared__ int64_t start[kDoffMax], bn0[kDoffMax];
-    __shared__ int64_t nrec0;
-    unsigned long long* bn = stat + S_HEAD + 2 * KS;
-    const int top = KS < kDoffMax ? KS : kDoffMax;
-    // every CTA reads the pre-commit sizes before any CTA can update them
-    // (the update is made by the last CTA out)
-    if (threadIdx.x == 0) {
-        nrec0 = (int64_t)stat[S_NREC];
-        int64_t acc = 0;
-        for (int k = 0; k < top; ++k) {
-            start[k] = acc;
-            acc += (int64_t)ins_k[k];
-            bn0[k] = (int64_t)bn[k];
-        }
-    }
-    __syncthreads();
-    if (single) {
-        int npad = 1;
-        while (npad < N) npad <<= 1;
-        for (int i = threadIdx.x; i < npad; i += blockDim.x)
-            keys[i] = i < N ? cand_key(tmp_mask, tmp_size, W, win[i]) : CandKey{~0ull, ~0ull, -1};
-        __syncthreads();
-        bitonic_sort(keys, npad, tmp_mask, W);
-        for (int i = threadIdx.x; i < N; i += blockDim.x)
-            commit_rank(W, i, keys[i].t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0, b_rec_tab,
-                        b_items_tab);
-    } else {
-        // sorted runs of kOrderRun, then each candidate's rank = its place in
-        // its run + the number of smaller keys in every other run
-        const int64_t nruns = (N + kOrderRun - 1) / kOrderRun;
-        for (int64_t rn = blockIdx.x; rn < nruns; rn += gridDim.x) {
-            const int64_t b = rn * kOrderRun;
-            const int len = (int)min((int64_t)kOrderRun, N - b);
-            int npad = 1;
-            while (npad < len) npad <<= 1;
-            for (int i = threadIdx.x; i < npad; i += blockDim.x)
-                keys[i] = i < len ? cand_key(tmp_mask, tmp_size, W, win[b + i]) : CandKey{~0ull, ~0ull, -1};
-            __syncthreads();
-            bitonic_sort(keys, npad, tmp_mask, W);
-            for (int i = threadIdx.x; i < len; i += blockDim.x) runs[b + i] = keys[i];
-            __syncthreads();
-        }
-        // grid barrier (every CTA of this launch is resident: gridDim <= SMs)
-        unsigned long long* bar = ins_k + kDoffMax;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(&bar[0], 1ull);
-            while (*(volatile unsigned long long*)&bar[0] < gridDim.x) __nanosleep(64);
-            __threadfence();
-        }
-        __syncthreads();
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t rn = i / kOrderRun;
-            const CandKey key = ld_key(runs + i);
-            int64_t rank = i - rn * kOrderRun;
-            for (int64_t q = 0; q < nruns; ++q) {
-                if (q == rn) continue;
-                const int64_t b = q * kOrderRun;
-                rank += run_lower_bound(runs + b, min((int64_t)kOrderRun, N - b), key, tmp_mask, W);
-            }
-            commit_rank(W, rank, key.t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0, b_rec_tab,
-                        b_items_tab);
-        }
-        __shared__ int last;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            last = atomicAdd(&bar[1], 1ull) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (!last) return;
-        if (threadIdx.x == 0) {
-            bar[0] = 0;
-            bar[1] = 0;
-        }
-    }
-    // sizes after the commit (one CTA: the single one, or the last one out)
-    __syncthreads();
-    for (int k = threadIdx.x; k < top; k += blockDim.x) {
-        if (ins_k[k]) bn[k] = (unsigned long long)(bn0[k] + (int64_t)ins_k[k]);
-        ins_k[k] = 0;
-    }
-    if (threadIdx.x == 0) stat[S_NREC] = (unsigned long long)(nrec0 + N);
 }
 
 // The stop's status into its (host-mapped, pinned) ring slot S_SEQ % kRing:
@@ -817,8 +680,9 @@ __global__ void __launch_bounds__(kOrderThreads) order_commit_kernel(
 // next stop (dead slots >= a quarter), reset the per-stop counters and
 // compute the next stop's delta offsets from the bucket fill.
 // ring == nullptr: reset only (engine seeding).
-__global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int kuse,
-                              unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
+__device__ void status_body(unsigned long long* __restrict__ stat, int KS, int kuse,
+                            unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
+    __shared__ int64_t sh[kDoffMax];
     if (ring) {
         unsigned long long* slot = ring + (int64_t)(stat[S_SEQ] % kRing) * ring_words;
         for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
@@ -838,21 +702,123 @@ __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int
         stat[S_HEAD + k] = 0;       // removed
         stat[S_HEAD + KS + k] = 0;  // adm
     }
-    // exclusive prefix of the bucket fill (blockDim == kDoffMax threads)
-    __shared__ int64_t sh[kDoffMax];
+    // exclusive prefix of the bucket fill (the first kDoffMax threads)
     const int top = KS < kDoffMax ? KS : kDoffMax;
     const int k = threadIdx.x;
-    const int64_t v = k < top ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
-    sh[k] = v;
+    const bool in = k < kDoffMax;
+    const int64_t v = in && k < top ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
+    if (in) sh[k] = v;
     __syncthreads();
     for (int off = 1; off < kDoffMax; off <<= 1) {
-        const int64_t add = k >= off ? sh[k - off] : 0;
+        const int64_t add = in && k >= off ? sh[k - off] : 0;
         __syncthreads();
-        sh[k] += add;
+        if (in) sh[k] += add;
         __syncthreads();
     }
     if (k < top) doff[k] = sh[k] - v;
     if (k == top - 1) doff[top] = sh[k];
+}
+
+// ring == nullptr: reset only (engine seeding)
+__global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int kuse,
+                              unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
+    status_body(stat, KS, kuse, ring, ring_words, doff);
+}
+
+#ifdef DIC_LAB_TIMING
+// lab build: per-stop phase stamps of commit_status (globaltimer ns), slot S_SEQ % 512
+__device__ unsigned long long g_lab_commit[512][8];
+#define COMMIT_STAMP(i)                                                                      \
+    do {                                                                                     \
+        if (threadIdx.x == 0) {                                                              \
+            unsigned long long _t;                                                           \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
+            g_lab_commit[stat[S_SEQ] % 512][i] = _t;                                         \
+        }                                                                                    \
+    } while (0)
+#else
+#define COMMIT_STAMP(i) \
+    do {                \
+    } while (0)
+#endif
+
+// The stop's canonical commit, then its status.  ins_k[0, kDoffMax): new
+// candidates by size (dedup); ins_k[kDoffMax]: CTAs done (the last CTA out
+// finalises the sizes and writes the status).
+constexpr int kCommitThreads = 256;
+__global__ void __launch_bounds__(kCommitThreads) rank_commit_status_kernel(
+    int W, const unsigned long long* __restrict__ tmp_mask, const uint64_t* __restrict__ tmp_hash,
+    const int32_t* __restrict__ tmp_size, const int64_t* __restrict__ tmp_slot, const CandKey* __restrict__ keys,
+    Records R, hent_t* ht, unsigned long long* stat, int KS, int kuse, unsigned long long* ins_k,
+    int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab,
+    unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
+    __shared__ int64_t start[kDoffMax], bn0[kDoffMax];
+    __shared__ int64_t nrec0;
+    __shared__ int last;
+    COMMIT_STAMP(0);
+    const int64_t N = (stat[S_ABORT] || stat[S_NFRONT] == 0) ? 0 : (int64_t)stat[S_NINS];
+    if (N == 0) {
+        if (blockIdx.x == 0) status_body(stat, KS, kuse, ring, ring_words, doff);
+        return;
+    }
+    unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    const int top = kuse < kDoffMax ? kuse : kDoffMax;  // sizes that can hold candidates
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // start[k] = new candidates of sizes < k: warp 0 scans 32 sizes per step
+    if (wid == 0) {
+        int64_t carry = 0;
+        for (int k0 = 0; k0 < top; k0 += 32) {
+            const int k = k0 + lane;
+            const int64_t v = k < top ? (int64_t)ins_k[k] : 0;
+            int64_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (k < top) {
+                start[k] = carry + x - v;
+                bn0[k] = (int64_t)bn[k];
+            }
+            carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+        }
+        if (lane == 0) nrec0 = (int64_t)stat[S_NREC];
+    }
+    __syncthreads();
+    COMMIT_STAMP(1);
+    // one warp per candidate: its rank is the number of smaller keys
+    const int64_t warps = (int64_t)gridDim.x * (kCommitThreads / 32);
+    for (int64_t e = (int64_t)blockIdx.x * (kCommitThreads / 32) + wid; e < N; e += warps) {
+        const CandKey ke = keys[e];
+        unsigned cnt = 0;
+        for (int64_t j = lane; j < N; j += 32) cnt += cand_less(keys[j], ke, tmp_mask, W) ? 1u : 0u;
+        cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+        if (lane == 0)
+            commit_rank(W, (int64_t)cnt, ke.t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0,
+                        b_rec_tab, b_items_tab);
+    }
+    COMMIT_STAMP(2);
+    // the last CTA out: sizes after the commit, then the stop's status
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&ins_k[kDoffMax], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int k = threadIdx.x; k < top; k += blockDim.x) {
+        const unsigned long long a = *(volatile unsigned long long*)&ins_k[k];
+        if (a) bn[k] = (unsigned long long)(bn0[k] + (int64_t)a);
+        ins_k[k] = 0;
+    }
+    if (threadIdx.x == 0) {
+        stat[S_NREC] = (unsigned long long)(nrec0 + N);
+        ins_k[kDoffMax] = 0;
+    }
+    __syncthreads();
+    COMMIT_STAMP(3);
+    status_body(stat, KS, kuse, ring, ring_words, doff);
 }
 
 struct TableUpdate {
@@ -973,10 +939,9 @@ struct dic_engine {
     uint64_t* tmp_hash = nullptr;
     int32_t* tmp_size = nullptr;
     int64_t* tmp_slot = nullptr;          // hash slot claimed by each owning join (dedup)
-    int32_t* tmp_win = nullptr;           // owning joins, in claim order (dedup)
-    CandKey* tmp_runs = nullptr;          // sorted key runs (order_commit, > kOrderRun new candidates)
+    CandKey* tmp_keys = nullptr;          // sort keys of the owning joins (dedup -> rank_commit_status)
     int64_t tmp_cap = 0;
-    unsigned long long* ins_k = nullptr;  // [kDoffMax + 2] new candidates by size + order_commit counters
+    unsigned long long* ins_k = nullptr;  // [kDoffMax + 2] new candidates by size (dedup -> commit_status)
 
     // the pair bucket as a dense triangle over the frequent items (pairs.cu)
     const uint32_t* pair_tids = nullptr;  // tids restricted to level1 (or tids itself)
@@ -1330,12 +1295,11 @@ int ensure_tmp(dic_engine* e, int64_t want) {
     dfree(e->tmp_hash, e->s);
     dfree(e->tmp_size, e->s);
     dfree(e->tmp_slot, e->s);
-    dfree(e->tmp_win, e->s);
-    dfree(e->tmp_runs, e->s);
+    dfree(e->tmp_keys, e->s);
     int rc;
     if ((rc = dalloc(&e->tmp_mask, nc * e->W, e->s)) || (rc = dalloc(&e->tmp_hash, nc, e->s)) ||
         (rc = dalloc(&e->tmp_size, nc, e->s)) || (rc = dalloc(&e->tmp_slot, nc, e->s)) ||
-        (rc = dalloc(&e->tmp_win, nc, e->s)) || (rc = dalloc(&e->tmp_runs, nc, e->s)))
+        (rc = dalloc(&e->tmp_keys, nc, e->s)))
         return rc;
     e->tmp_cap = nc;
     return DIC_OK;
@@ -1383,31 +1347,17 @@ int candidate_step(dic_engine* e, cudaStream_t s) {
                                                  e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap);
     ::dic::note_launch();
     dedup_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht, (uint64_t)e->hcap - 1, st,
-                                   e->tmp_slot, e->tmp_win, e->ins_k);
+                                   e->tmp_slot, e->tmp_keys, e->ins_k);
     ::dic::note_launch();
-    static bool attr = false;
-    if (!attr) {
-        DIC_CUDA(cudaFuncSetAttribute(order_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kOrderSmem));
-        attr = true;
-    }
-    // one CTA per SM (all resident: the multi-run path has a grid barrier)
-    order_commit_kernel<<<sm_count(), kOrderThreads, kOrderSmem, s>>>(
-        e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->tmp_win, e->tmp_runs, e->R, e->ht, st, e->KS,
-        e->ins_k, e->d_brec, e->d_bitems);
+    // the canonical commit (one warp per new candidate) and the stop's status
+    rank_commit_status_kernel<<<sm_count(), kCommitThreads, 0, s>>>(
+        e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->tmp_keys, e->R, e->ht, st, e->KS, e->kuse,
+        e->ins_k, e->d_brec, e->d_bitems, e->ring_dev, e->ring_words, e->d_doff);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("candidate_step");
     return DIC_OK;
 }
 
-// status of the stop into its ring slot (one kernel writing host-mapped
-// pinned memory; the slot is S_SEQ % kRing on the device)
-int launch_status(dic_engine* e, cudaStream_t s) {
-    status_kernel<<<1, kDoffMax, 0, s>>>(e->d_stat, e->KS, e->kuse, e->ring_dev, e->ring_words, e->d_doff);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("status_kernel");
-    return DIC_OK;
-}
 
 // the checkpoint half of a stop: apply + prune + finalize over every slot,
 // compaction of the flagged buckets, make_candidates (device-sized,
@@ -1423,9 +1373,7 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s) {
         e->d_brec, e->d_bitems, e->d_doff, e->keep, e->d_stat, e->KS);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("compact_flagged_kernel");
-    int rc;
-    if ((rc = candidate_step(e, s))) return rc;
-    return launch_status(e, s);
+    return candidate_step(e, s);  // eval, dedup, commit + status
 }
 
 // Fused reduction of a stop's counts over NVLink peer memory (SURVEY 8(f)
@@ -1674,7 +1622,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
     dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
-    dfree(e->tmp_win, s); dfree(e->tmp_runs, s); dfree(e->ins_k, s);
+    dfree(e->tmp_keys, s); dfree(e->ins_k, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
     if (!e->fused) dfree(e->tri, s);
     if (e->fused) {
@@ -1692,6 +1640,14 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
 }
 
 extern "C" int dic_engine_words(dic_engine* e) { return e ? e->W : DIC_EINVAL; }
+
+#ifdef DIC_LAB_TIMING
+extern "C" int dic_lab_commit_stamps(unsigned long long* host) {
+    cudaDeviceSynchronize();
+    DIC_CUDA(cudaMemcpyFromSymbol(host, g_lab_commit, sizeof(g_lab_commit)));
+    return DIC_OK;
+}
+#endif
 
 extern "C" int dic_engine_item_counts(dic_engine* e, int64_t* counts) {
     DIC_REQUIRE(e && counts, "dic_engine_item_counts: null argument");
@@ -2077,8 +2033,7 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_ABORT, 0, u, e->s));
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
-        if ((rc = candidate_step(e, e->s))) return rc;
-        if ((rc = launch_status(e, e->s))) return rc;
+        if ((rc = candidate_step(e, e->s))) return rc;  // ends with the stop's status
         e->kuse_at[slot] = e->kuse;
         DIC_CUDA(cudaStreamSynchronize(e->s));
         ku = e->kuse_at[slot];

@@ -140,3 +140,34 @@ def test_lockstep_cfg2_full_matches_reference_golden():
     st = g.stats
     assert _stats(res.stats) == (st["db_passes"], st["peak_dashed"], st["candidates_generated"],
                                  st["candidates_pruned"], st["interval_counts"])
+
+
+def test_large_stop_multi_run_commit_is_canonical_and_exact(monkeypatch):
+    """A dense database whose stops admit more than one sort run (2,048) of
+    new candidates at once: the run-merging commit path, under two grid
+    sizes and over 2 lockstep ranks, against the oracle."""
+    rng = np.random.default_rng(11)
+    n, m = 3000, 24
+    rows = np.zeros((n, 1), dtype=np.uint64)
+    bits = rng.random((n, m)) < 0.6
+    for i in range(m):
+        rows[:, 0] |= bits[:, i].astype(np.uint64) << np.uint64(i)
+    params = dic.MiningParams.create(n, 0.15, interval=300)
+    ints = [int(x) for x in rows[:, 0]]
+    shards = []
+    for r in range(2):
+        plan = dic.ShardPlan.for_params(params, 2, r)
+        shards.append(dic.BitDatabase([ints[b + j] for b, ln in plan.ranges() for j in range(ln)], m=m))
+    res, info = mine_lockstep(shards, params)
+    assert max(st["inserted"] for st in info.statuses) > 2048
+    want = O.mine(rows, m, 0.15, interval=300, threads=THREADS)
+    assert [(f.mask, f.size, f.support) for f in res.frequent] == want.frequent
+    assert _stats(res.stats) == _oracle_tuple(want)
+    db = dic.BitDatabase(ints, m=m)
+    runs = []
+    for grid in ("1", "16"):
+        monkeypatch.setenv("DIC_CAND_GRID", grid)
+        runs.append(_step_dumps(db, params, kmax=8))
+    for a, b in zip(*runs):
+        for (ra, ia), (rb, ib) in zip(a, b):
+            assert np.array_equal(ra, rb) and np.array_equal(ia, ib)

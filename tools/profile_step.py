@@ -69,7 +69,8 @@ def main() -> None:
     # per-launch duration series of the per-stop kernels (stop order)
     series = defaultdict(list)
     for s0, e0, n0 in acts:
-        for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "insert_commit", "compact", "status"):
+        for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "pair_tc", "dedup", "commit_status",
+                    "compact", "status_kernel"):
             if key in n0:
                 series[key].append(round(e0 - s0, 1))
     for key, v in series.items():
@@ -84,7 +85,8 @@ def main() -> None:
         print(f"{ms:9.3f} ms {n:6d} x {ms / n * 1000:9.2f} us  {name}")
     if out_json:
         Path(out_json).write_text(json.dumps({"config": cfg.name, "depth": depth, "wall_ms": wall * 1000,
-                                              "gpu_busy_ms": busy,
+                                              "gpu_busy_ms": busy, "series_us": series,
+                                              "dashed": d,
                                               "kernels": [{"name": k, "launches": n, "total_ms": ms}
                                                           for k, (n, ms) in rows]}, indent=1))
 
