@@ -160,3 +160,100 @@ def test_cfg5_bit_sliced_count_equals_row_count_and_is_linear(cfg5_bitmap, k):
     assert np.array_equal(got, full[:300])
     if k <= 3:  # i.i.d. Bernoulli(0.05): E[support] = n * 0.05^k (tight for small k)
         assert abs(full.mean() / (n * 0.05 ** k) - 1) < 0.05
+
+
+# ------------------------------------------------ full-size oracle goldens
+# tests/golden/cfg4.npz: the C oracle mined all 10M rows (make_golden_cfg4.py,
+# 51 min on 7 host threads); tests/golden/cfg5.npz: the support of all 100k
+# cfg5 candidates over all 50M rows (make_golden_cfg5.py).  The oracle itself
+# is pinned to the reference in tests/test_oracle_golden.py.
+from tests.golden_util import csr_digest, load_config_golden  # noqa: E402
+
+
+def _golden_stats(g) -> tuple:
+    st = g.stats
+    return (st["db_passes"], st["peak_dashed"], st["candidates_generated"], st["candidates_pruned"],
+            st["interval_counts"])
+
+
+def _stats(s) -> tuple:
+    return (s.db_passes, s.peak_dashed, s.candidates_generated, s.candidates_pruned, s.interval_counts)
+
+
+def test_cfg4_full_equals_oracle_golden(cfg4_run):
+    """Bench workload, one GPU: every frequent itemset, its support and every
+    MiningStats counter equal the oracle's full-size run."""
+    cfg, db, params, res = cfg4_run
+    g = load_config_golden(4)
+    indptr, indices = generate_csr(cfg)
+    assert csr_digest(indptr, indices) == g.meta["csr_sha256"], "generator drift"
+    assert [(f.mask, f.support) for f in res.frequent] == g.pairs
+    assert [f.size for f in res.frequent] == g.sizes.tolist()
+    assert _stats(res.stats) == _golden_stats(g)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_cfg4_full_sharded_lockstep_equals_oracle_golden(world):
+    """The sharded trajectory at full size: `world` engines over the
+    chunk-sliced shards of all 10M rows, counts summed slot by slot per stop
+    (lockstep.py), against the same golden — frequent set, supports, stats."""
+    from paper_1812_10959_b200.lockstep import mine_lockstep
+
+    cfg = CONFIGS[4]
+    g = load_config_golden(4)
+    params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
+    shards = []
+    for r in range(world):
+        plan = dic.ShardPlan.for_params(params, world, r)
+        ip, ix = generate_csr(cfg, ranges=plan.ranges())
+        shards.append(dic.BitDatabase.from_csr(ip, ix, cfg.m))
+    res, info = mine_lockstep(shards, params, check_layout=world == 2, max_size=6)
+    assert [(f.mask, f.support) for f in res.frequent] == g.pairs
+    assert _stats(res.stats) == _golden_stats(g)
+    assert info.stops == g.meta["stops"]
+    del shards
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_device_generator_matches_host_restatement(cfg5_bitmap):
+    from oracle import oracle as O
+
+    cfg, rows, tids, ks, items = cfg5_bitmap
+    for r0 in (0, 31_415_926, cfg.n - 2000):
+        host = O.bernoulli_rows(r0, 2000, cfg.m, cfg.params["p"], cfg.seed)
+        dev = rows[r0:r0 + 2000].cpu().numpy().view(np.uint64)
+        assert np.array_equal(host, dev)
+
+
+def test_cfg5_all_candidates_equal_oracle_golden(cfg5_bitmap):
+    """All 100,000 cfg5 candidates over all 50M rows through the product
+    count kernel (dic_count_support, one launch per size bucket) against the
+    oracle's column count; plus first_pass's column popcounts."""
+    import hashlib
+
+    from paper_1812_10959_b200 import device as D
+
+    z = np.load(GOLD5)
+    import json
+
+    meta = json.loads(str(z["meta"]))
+    cfg, rows, tids, ks, items = cfg5_bitmap
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(ks, dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(items, dtype=np.uint16).tobytes())
+    assert h.hexdigest() == meta["cand_sha256"]
+    n, m = cfg.n, cfg.m
+    counts = torch.zeros(m, dtype=torch.int64, device="cuda")
+    D.item_support(tids, n, m, 0, n - 1, counts)
+    assert np.array_equal(counts.cpu().numpy(), z["item_counts"].astype(np.int64))
+    got = np.zeros(len(ks), dtype=np.int64)
+    for k in range(cfg.params["kmin"], cfg.params["kmax"] + 1):
+        idx = np.nonzero(ks == k)[0]
+        it = torch.from_numpy(np.ascontiguousarray(items[idx, :k]).view(np.int16)).cuda()
+        got[idx] = D.count_support(tids, n, m, 0, n - 1, it).cpu().numpy()
+    want = z["supports"].astype(np.int64)
+    assert np.array_equal(got, want)
+    assert int(got.sum()) == meta["support_checksum"]
+
+
+GOLD5 = __import__("pathlib").Path(__file__).resolve().parent / "golden" / "cfg5.npz"
