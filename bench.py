@@ -215,19 +215,53 @@ def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
     ns = north_star_roofline(n, words_for(m), sum_nnz64, best, peaks)
     achieved = ops / (best * 1e-3)
     checksum = int(sum(int(o.sum().item()) for o in outs))
+    golden = None
+    gp = ROOT / "tests" / "golden" / "cfg5.npz"
+    if gp.exists():
+        z = np.load(gp)
+        gmeta = json.loads(str(z["meta"]))
+        # per-candidate equality in the bench's own (per-size, sorted) order
+        ks_all, items_all = ks, items
+        want = z["supports"].astype(np.int64)
+        ok = True
+        for b, o, k in zip(buckets, outs, range(cfg.params["kmin"], cfg.params["kmax"] + 1)):
+            idx = np.nonzero(ks_all == k)[0]
+            sel = items_all[idx][:, :k]
+            order = np.lexsort(sel.T[::-1])
+            ok &= bool(np.array_equal(o.cpu().numpy(), want[idx][order]))
+        golden = {"support_checksum": gmeta["support_checksum"], "match": bool(ok and checksum ==
+                                                                             gmeta["support_checksum"]),
+                  "golden": "tests/golden/cfg5.npz (all 100k candidates x 50M rows, oracle/cfg5.c)"}
     del tids
     torch.cuda.empty_cache()
     return {"workload": cfg.name, "n": n, "m": m, "candidates": C, "ms": best,
             "subset_tests_per_s": C * n / (best * 1e-3), "bound": "alu", "bound_detail": "integer ALU pipe (LOP3 lane-ops); neither HBM nor tensor cores bind this path",
             "achieved": achieved / 1e12, "peak": peaks["lop3"] / 1e12, "unit": "T lane-ops/s",
-            "frac": achieved / peaks["lop3"], "support_checksum": checksum, "north_star": ns,
+            "frac": achieved / peaks["lop3"], "support_checksum": checksum, "golden_check": golden,
+            "north_star": ns,
             "hbm_streaming": hbm,
             "ops_rule": "k lane-ops per (candidate, 32-row word): (k-1) ANDs + >= 1 to accumulate the popcount"}
 
 
+def measured_tensor_peak() -> tuple[float, str]:
+    """Dense peak of the pair kernel's MMA kind in FLOP/s: the measured bf16
+    GEMM burst (MEASURED_PEAKS.json) scaled by NVIDIA's nominal dense ratio of
+    the kind to bf16 (FP4 9 / 2.25 = 4, INT8 4.5 / 2.25 = 2): B200_PROFILING.md
+    gives no measured FP4 / INT8 figure."""
+    kind = os.environ.get("DIC_PAIR_TC_KIND", "4")
+    ratio, name = (2.0, "i8") if kind == "8" else (4.0, "mxf4")
+    try:
+        bf16 = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+        src = "MEASURED_PEAKS.json bf16 burst"
+    except Exception:
+        bf16, src = 1590.0, "fallback bf16 1.59 PF (B200_PROFILING.md)"
+    return bf16 * ratio * 1e12, f"{src} {bf16:.0f} TF/s x {ratio:g} (nominal {name}:bf16 dense ratio)"
+
+
 def pair_kernel_roofline(tids, n: int, m: int, interval: int, peaks: dict, reps: int = 10) -> dict:
-    """The dominant kernel of the cfg4 run, measured alone on the run's own
-    data: dic_count_pairs over one M-row chunk (a dense-pair stop)."""
+    """The pair-wave kernel of the cfg4 run, measured alone on the run's own
+    data: dic_count_pairs over one M-row chunk (a dense-pair stop), which runs
+    the tensor-core triangle (pairs_mma.cu) for m >= 128."""
     import torch
 
     from paper_1812_10959_b200 import device as D
@@ -247,17 +281,24 @@ def pair_kernel_roofline(tids, n: int, m: int, interval: int, peaks: dict, reps:
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / reps
     words = (last - first + 1 + 31) // 32
-    ops = 2.0 * tri.numel() * words  # k = 2
     rows = last - first + 1
+    pairs = tri.numel()
+    # algorithmic work: one multiply-add (2 FLOP) per (pair, row); the MMAs
+    # also cover the lower half of the diagonal tiles and the padding to
+    # 128 x 256 tiles (issued FLOPs)
+    flops = 2.0 * pairs * rows
+    na, nb = -(-m // 128), -(-m // 256)
+    tiles = sum(nb - ia // 2 for ia in range(na))
+    issued = 2.0 * 128 * 256 * tiles * (-(-rows // 256) * 256)
     # north-star roofline: 2 lane-ops per 64-bit word-test of a
     # candidate's non-zero words, per ROW; a pair has 1 such word if both
     # items share a 64-bit word, else 2
     full, rem = divmod(m, 64)
     same = full * (64 * 63 // 2) + rem * (rem - 1) // 2
-    nnz64 = same + 2 * (tri.numel() - same)
+    nnz64 = same + 2 * (pairs - same)
     ns = north_star_roofline(rows, words_for(m), nnz64, t, peaks)
-    return {"t_ms": t, "ops": ops, "tests_per_s": tri.numel() * rows / (t * 1e-3),
-            "achieved": ops / (t * 1e-3), "north_star": ns}
+    return {"t_ms": t, "flops": flops, "issued_flops": issued, "tests_per_s": pairs * rows / (t * 1e-3),
+            "achieved": flops / (t * 1e-3), "lop3_equiv_ops": 2.0 * pairs * words, "north_star": ns}
 
 
 def words_for(m: int) -> int:
@@ -304,12 +345,14 @@ def run_reference(args, cfg, rank: int, world: int) -> None:
     if rank != 0:
         return
     from oracle import oracle as O
+    from oracle import synth as S
     from paper_1812_10959_b200.config import MiningParams
-    from paper_1812_10959_b200.workloads import generate_csr
     from tests.golden_util import rows_from_csr
 
     cores = os.cpu_count() or 1
-    indptr, indices = generate_csr(cfg, threads=cores)
+    # the input from the generator's own build (oracle/_build/libsynth.so):
+    # this process maps no product library, only the oracle's
+    indptr, indices = S.generate_csr(cfg, threads=cores)
     rows = rows_from_csr(indptr, indices, cfg.m)
     params = MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
     times, tests = [], 0
@@ -334,7 +377,65 @@ def run_reference(args, cfg, rank: int, world: int) -> None:
             "cpu_baseline": {"value": value, "unit": "subset-tests/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "subset-tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["native_libs"] = mapped_libs()
     print(json.dumps(line), flush=True)
+
+
+def mapped_libs() -> list:
+    """Shared objects of this repo mapped into the process (evidence of which
+    native code a leg ran)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return []
+    out = sorted({ln.split()[-1] for ln in maps if ln.endswith(".so") and str(ROOT) in ln})
+    return [str(Path(x).relative_to(ROOT)) for x in out]
+
+
+def golden_check(idx: int, res) -> dict | None:
+    """The run's frequent itemsets, supports and MiningStats against the
+    committed full-size oracle golden (tests/golden/cfg<idx>.npz)."""
+    from tests.golden_util import has_config_golden, load_config_golden
+
+    if not has_config_golden(idx):
+        return None
+    g = load_config_golden(idx)
+    s = res.stats
+    st = g.stats
+    same_sets = [(f.mask, f.support) for f in res.frequent] == g.pairs
+    same_stats = (s.db_passes, s.peak_dashed, s.candidates_generated, s.candidates_pruned, s.interval_counts) == (
+        st["db_passes"], st["peak_dashed"], st["candidates_generated"], st["candidates_pruned"], st["interval_counts"])
+    return {"match": bool(same_sets and same_stats), "frequent_itemsets_equal": bool(same_sets),
+            "stats_equal": bool(same_stats), "golden": f"tests/golden/cfg{idx}.npz",
+            "source": g.meta.get("source", "reference")}
+
+
+def same_sample_rate(cfg, tids, n_local: int, params, reps: int = 5) -> dict:
+    """The B200 engine on exactly the CPU arm's sample: first pass over all
+    rows + the first checkpoint (the step-by-step API, CUDA events around
+    engine creation .. the first stop's status), median of `reps`."""
+    import torch
+
+    from paper_1812_10959_b200.miner import DeviceEngine
+
+    first, last = params.chunk_bounds(1)
+    times, tests = [], 0
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng = DeviceEngine(tids, n_local, cfg.m, params, True)
+        eng.seed(eng.item_counts())
+        eng.issue_count(first, last)
+        st, _ = eng.poll(eng.issue_checkpoint())
+        e1.record()
+        torch.cuda.synchronize()
+        eng.close()
+        times.append(e0.elapsed_time(e1))
+        tests = cfg.n * cfg.m + st.dashed_at_start * (last - first + 1)
+    ms = statistics.median(times[1:])
+    return {"value": tests / (ms * 1e-3), "unit": "subset-tests/s", "ms": ms,
+            "sample": "first pass + checkpoint 1 (the --impl reference sample)", "subset_tests": tests}
 
 
 # ---------------------------------------------------------------- B200 arm
@@ -407,6 +508,8 @@ def main() -> None:
     trace = StopTrace()
     ref = one_run(trace=trace)
     tests = subset_tests(cfg.n, cfg.m, params, trace)
+    golden = golden_check(args.config, ref)  # correctness gate before timing (benchmark.py:91-95)
+    assert golden is None or golden["match"], f"result differs from the oracle golden: {golden}"
     cross_check = None
     if world > 1 and (trace.native or {}).get("collective") == "fused":
         # the fused peer-memory reduction must agree with ncclAllReduce, bit
@@ -476,18 +579,26 @@ def main() -> None:
     dense_stops = min(len(count_ms), params.intervals_per_pass)
     roofline = None
     if pk is not None:
-        roofline = {"bound": "alu", "bound_detail": "integer ALU pipe (LOP3 lane-ops); neither HBM nor tensor cores bind this path", "achieved": pk["achieved"] / 1e12,
-                    "peak": peaks["lop3"] / 1e12, "unit": "T lane-ops/s", "frac": pk["achieved"] / peaks["lop3"],
-                    "traffic": ncu_traffic("pair_tri_kernel"), "kernel": "pair_tri_kernel",
-                    "avg_launch_ms": pk["t_ms"], "ops_per_launch": pk["ops"],
+        tpk, tsrc = measured_tensor_peak()
+        roofline = {"bound": "tensor",
+                    "bound_detail": "tensor cores (tcgen05 kind::mxf4, bits expanded to E2M1 operands in shared "
+                                    "memory): the dense pair triangle X^T X of each chunk",
+                    "achieved": pk["achieved"] / 1e12, "peak": tpk / 1e12, "unit": "TFLOP/s",
+                    "frac": pk["achieved"] / tpk, "traffic": ncu_traffic("pair_tc_kernel"),
+                    "kernel": "pair_tc_kernel", "avg_launch_ms": pk["t_ms"], "flops_per_launch": pk["flops"],
+                    "issued_flops_per_launch": pk["issued_flops"],
+                    "issued_frac": pk["issued_flops"] / (pk["t_ms"] * 1e-3) / tpk,
                     "tests_per_s": pk["tests_per_s"],
-                    "ops_rule": "2 lane-ops per (pair, 32-row word): 1 AND + >= 1 to accumulate the popcount",
-                    "share_of_step": pk["t_ms"] * dense_stops / ms if ms else None,
-                    "peak_source": f"live probe: LOP3 {peaks['lop3'] / 1e12:.2f} T lane-ops/s, "
-                                   f"POPC {peaks['popc'] / 1e12:.2f} T lane-ops/s (MEASURED_PEAKS.json has no "
-                                   "integer pipes)",
+                    "flops_rule": "2 FLOP (one multiply-add) per (pair, row) of the chunk; issued = 128x256 MMA "
+                                  "tiles incl. the lower half of diagonal tiles and padding",
+                    "share_of_step": pk["t_ms"] * dense_stops / ms if ms else None, "peak_source": tsrc,
+                    "vs_lop3": {"ops": pk["lop3_equiv_ops"], "frac_of_lop3_peak":
+                                pk["lop3_equiv_ops"] / (pk["t_ms"] * 1e-3) / peaks["lop3"],
+                                "lop3_peak": peaks["lop3"], "note": "the round-1 AND/POPC kernel's metric "
+                                "(2 lane-ops per pair and 32-row word) against the live LOP3 probe; > 1 means "
+                                "faster than any integer-pipe kernel can be"},
                     "north_star": pk["north_star"],
-                    "count_launches_in_step": len(count_ms), "count_ms_in_step": tot_ms,
+                    "count_launches_in_step": len(count_ms),
                     "hbm_peak_gbs": hbm_gbs, "hbm_peak_source": hbm_src}
 
     # end to end through the public API from pinned host CSR
@@ -520,6 +631,7 @@ def main() -> None:
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "host_wall_ms_per_step":
                    1000 * (time.perf_counter() - t) / args.steps}
 
+    same_sample = same_sample_rate(cfg, tids, n_local, params) if world == 1 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, db, params)
@@ -552,6 +664,7 @@ def main() -> None:
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
             "collective": (trace.native or {}).get("collective"), "collective_cross_check": cross_check,
             "cpu_baseline": cpu, "kernel_microbench": kernel, "config_sweep": sweep,
+            "golden_check": golden, "same_sample": same_sample, "native_libs": mapped_libs(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -26,17 +26,19 @@
  *   rows   : uint64 [n][W], W = ceil(m/64); item p of row j is bit (p & 63)
  *            of word (p >> 6) — the reference's single-word layout
  *            (bitops.py:36) extended LSW-first to W words.
- *   tids   : the tiled, pre-swizzled bit-sliced ("vertical") copy, uint32
- *            words.  Rows are grouped 32 per word (group g = rows 32g..32g+31,
- *            bit b <-> row 32g+b).  A tile holds TW groups of all m items,
- *            TW = dic_tids_tile_groups(m) = 32 (m <= 768) or 16; item i's TW
- *            words of tile t form one row whose 16-byte chunks are XOR-
- *            swizzled by sw(i) = i & 7 (TW 32) or (i >> 1) & 3 (TW 16):
- *              word(i, g) = tids[t*m*TW + i*TW + ((q ^ sw(i))*4 + e)],
- *              t = g / TW, q = (g % TW) / 4, e = g % 4.
- *            A tile's global image equals its shared-memory image, so one
- *            bulk copy (TMA engine) stages it.  Rows past n read as zero;
- *            the buffer holds dic_tids_words(n, m) words.
+ *   tids   : the tiled, padded bit-sliced ("vertical") copy, uint32 words.
+ *            Rows are grouped 32 per word (group g = rows 32g..32g+31, bit
+ *            b <-> row 32g+b).  A tile holds TW groups of all m items,
+ *            TW = dic_tids_tile_groups(m) = 32 (m <= 768) or 16.  Item i's TW
+ *            words of tile t form one row padded by 4 zero words, so the row
+ *            stride is RW = TW + 4 words (an odd number of 16-byte chunks: the
+ *            shared-memory copy of a tile reads conflict-free) and there is
+ *            no swizzle:
+ *              word(i, g) = tids[t*m*RW + i*RW + (g - t*TW)],  t = g / TW,
+ *            i.e. dic_tids_index(m, i, g).  A tile's global image equals its
+ *            shared-memory image, so one bulk copy (TMA engine) stages it.
+ *            Rows past n and the pad words read as zero; the buffer holds
+ *            dic_tids_words(n, m) = ceil(ceil(n/32)/TW) * m * RW words.
  *   items  : uint16 [C][k], the k ascending item ids of each candidate of a
  *            size-k bucket (candidates of one launch share k).
  */
@@ -111,6 +113,9 @@ int dic_tids_to_rows(const uint32_t* tids, int64_t n, int32_t m, uint64_t* rows,
 /* Layout helpers (host functions).                                         */
 int64_t dic_tids_words(int64_t n, int32_t m);
 int dic_tids_tile_groups(int32_t m);
+/* Index (in uint32 words) of item i's word of row group g in the tids
+ * layout of an m-item universe (the formula above; host callable).        */
+int64_t dic_tids_index(int32_t m, int32_t item, int64_t group);
 
 /* First pass: per-item supports -----------------------------------------
  * Replaces first_pass's singleton counting (engine.py:132-154): for every

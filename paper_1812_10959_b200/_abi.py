@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "dic_rows_to_tids": (C.c_int, [vp, i64, i32, vp, vp]),
     "dic_tids_words": (i64, [i64, i32]),
     "dic_tids_tile_groups": (C.c_int, [i32]),
+    "dic_tids_index": (i64, [i32, i32, i64]),
     "dic_item_support": (C.c_int, [vp, i64, i32, i64, i64, vp, vp]),
     "dic_count_support": (C.c_int, [vp, i64, i32, i64, i64, vp, i32, i64, vp, vp]),
     "dic_count_pairs": (C.c_int, [vp, i64, i32, i64, i64, vp, vp]),

@@ -880,6 +880,11 @@ extern "C" int64_t dic_tids_words(int64_t n, int32_t m) {
 
 extern "C" int dic_tids_tile_groups(int32_t m) { return m >= 1 ? tile_groups(m) : DIC_EINVAL; }
 
+extern "C" int64_t dic_tids_index(int32_t m, int32_t item, int64_t group) {
+    if (m < 1 || item < 0 || item >= m || group < 0) return DIC_EINVAL;
+    return tids_index(m, tile_groups(m), (uint32_t)item, group);
+}
+
 extern "C" int dic_item_support(const uint32_t* tids, int64_t n, int32_t m, int64_t first, int64_t last,
                                 int64_t* counts, void* stream) {
     DIC_REQUIRE(m >= 1 && tids && counts, "dic_item_support: bad arguments");

@@ -246,3 +246,29 @@ def test_tids_select_then_pairs():
     bitsm = np.stack([(blk[:, i >> 6] >> np.uint64(i & 63)) & np.uint64(1) for i in items], axis=1).astype(np.float64)
     gram = bitsm.T @ bitsm
     assert np.array_equal(tri, gram[np.triu_indices(300, k=1)].astype(np.int64))
+
+
+@pytest.mark.parametrize("m,n", [(64, 5_000), (700, 3_000), (1000, 2_345), (769, 40)])
+def test_encoded_tids_decode_with_header_formula_only(m, n):
+    """An external consumer indexing the tids buffer with nothing but the
+    header's formula (tests/test_host.py header_tids_index) reads back the
+    rows; pad words and rows past n are zero."""
+    from tests.test_host import header_tids_index
+
+    rng = np.random.default_rng(m + n)
+    rows = random_rows(rng, n, m, 0.2)
+    tids = D.rows_to_tids(to_dev(rows), n, m).cpu().numpy().view(np.uint32)
+    TW = 32 if m <= 768 else 16
+    G = -(-(-(-n // 32)) // TW) * TW  # groups of the whole tiles
+    idx = np.array([[header_tids_index(m, i, g) for i in range(m)] for g in range(G)], dtype=np.int64)
+    words = tids[idx]  # [G][m]
+    bits_gm = np.unpackbits(words.astype("<u4").view(np.uint8).reshape(G, m, 4), axis=2, bitorder="little")
+    rowbits = bits_gm.transpose(0, 2, 1).reshape(G * 32, m)  # row 32g + b, item i
+    assert not rowbits[n:].any(), "bits set past the last row"
+    back = np.zeros_like(rows)
+    for i in range(m):
+        back[:, i >> 6] |= rowbits[:n, i].astype(np.uint64) << np.uint64(i & 63)
+    assert np.array_equal(back, rows)
+    used = np.zeros(tids.size, dtype=bool)
+    used[idx.ravel()] = True
+    assert not tids[~used].any(), "pad words must be zero"

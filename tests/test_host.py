@@ -190,3 +190,27 @@ def test_result_builder_matches_python_construction():
                           np.array([7, 8], dtype=np.int64), presorted=True)
     assert one == (FrequentItemset(5, 2, 7), FrequentItemset(3, 2, 8))
     assert sorted_frequent(np.zeros((0, 4), dtype=np.uint64), np.zeros(0, np.int32), np.zeros(0, np.int64)) == ()
+
+
+def header_tids_index(m: int, item: int, g: int) -> int:
+    """The tids layout exactly as include/dic_b200.h documents it."""
+    TW = 32 if m <= 768 else 16
+    RW = TW + 4
+    t = g // TW
+    return t * m * RW + item * RW + (g - t * TW)
+
+
+@pytest.mark.parametrize("m", [1, 64, 128, 700, 768, 769, 1000, 4096])
+def test_tids_layout_matches_header_formula(m):
+    """dic_tids_index / dic_tids_words agree with the header's formula (the
+    layout an external consumer indexes by)."""
+    lib = _abi.load()
+    TW = lib.dic_tids_tile_groups(m)
+    assert TW == (32 if m <= 768 else 16)
+    rng = np.random.default_rng(m)
+    for _ in range(200):
+        item, g = int(rng.integers(0, m)), int(rng.integers(0, 1 << 22))
+        assert _abi.call("dic_tids_index", m, item, g) == header_tids_index(m, item, g)
+    for n in (1, 31, 32, 33, TW * 32, TW * 32 + 1, 10_000_000):
+        groups = -(-n // 32)
+        assert lib.dic_tids_words(n, m) == -(-groups // TW) * m * (TW + 4)
