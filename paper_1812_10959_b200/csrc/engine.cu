@@ -585,7 +585,17 @@ __device__ __forceinline__ CandKey cand_key(const unsigned long long* __restrict
     k.t = t;
     unsigned long long hi = (unsigned long long)(uint32_t)sz << 48, lo = 0;
     int j = 0;
-    for (int w = 0; w < W && j < 7; ++w) key_take(w, mk[w], j, hi, lo);
+    if (W <= 16) {
+        // every word loaded before the first use (a loop with an early exit
+        // would chain W dependent L2 latencies)
+        unsigned long long v[16];
+#pragma unroll
+        for (int w = 0; w < 16; ++w) v[w] = w < W ? mk[w] : 0ull;
+#pragma unroll
+        for (int w = 0; w < 16; ++w) key_take(w, v[w], j, hi, lo);
+    } else {
+        for (int w = 0; w < W && j < 7; ++w) key_take(w, mk[w], j, hi, lo);
+    }
     k.hi = hi;
     k.lo = lo;
     return k;
@@ -696,27 +706,40 @@ __device__ void status_body(unsigned long long* __restrict__ stat, int KS, int k
     if (stat[S_ABORT]) return;
     if (ring && threadIdx.x == 0) stat[S_SEQ] += 1;
     for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
-    for (int k = threadIdx.x; k < KS && k < kDoffMax; k += blockDim.x) {
+    // per-size words: only sizes <= kuse can be non-zero (a stop's joins are
+    // one item larger than its largest live itemset, which is < kuse)
+    const int lim = min(min(KS, kDoffMax), kuse + 1);
+    for (int k = threadIdx.x; k < lim; k += blockDim.x) {
         const unsigned long long rem = stat[S_HEAD + k], fill = stat[S_HEAD + 2 * KS + k];
         stat[S_HEAD + 3 * KS + k] = (rem > 0 && (rem * 4 >= fill || rem == fill)) ? 1ull : 0ull;  // cflag
         stat[S_HEAD + k] = 0;       // removed
         stat[S_HEAD + KS + k] = 0;  // adm
     }
-    // exclusive prefix of the bucket fill (the first kDoffMax threads)
+    // delta offsets: exclusive prefix of the bucket fills; sizes >= kuse are
+    // empty, so every later offset is the total (a later stop may use a
+    // larger kuse).  Warp 0 scans 32 sizes per step.
     const int top = KS < kDoffMax ? KS : kDoffMax;
-    const int k = threadIdx.x;
-    const bool in = k < kDoffMax;
-    const int64_t v = in && k < top ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
-    if (in) sh[k] = v;
-    __syncthreads();
-    for (int off = 1; off < kDoffMax; off <<= 1) {
-        const int64_t add = in && k >= off ? sh[k - off] : 0;
-        __syncthreads();
-        if (in) sh[k] += add;
-        __syncthreads();
+    const int use = min(top, kuse);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int64_t carry = 0;
+        for (int k0 = 0; k0 < use; k0 += 32) {
+            const int k = k0 + lane;
+            const int64_t v = k < use ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
+            int64_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (k < use) doff[k] = carry + x - v;
+            carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+        }
+        if (lane == 0) sh[0] = carry;
     }
-    if (k < top) doff[k] = sh[k] - v;
-    if (k == top - 1) doff[top] = sh[k];
+    __syncthreads();
+    const int64_t total = sh[0];
+    for (int k = use + threadIdx.x; k <= top; k += blockDim.x) doff[k] = total;
 }
 
 // ring == nullptr: reset only (engine seeding)
