@@ -361,9 +361,9 @@ int pair_launch(const uint32_t* tids, int m, ChunkGeom geom, int64_t t_first, in
     return DIC_OK;
 }
 
-int pair_tc_launch(const uint32_t* tids, int L, ChunkGeom geom, unsigned long long* tri, const unsigned long long* bn2,
-                   int64_t tri_len, const unsigned long long* abort_flag, const int64_t* chunk_ring,
-                   const unsigned long long* seq, int ring, cudaStream_t s);
+int pair_tc_launch(const uint32_t* tids, int64_t n, int L, ChunkGeom geom, unsigned long long* tri,
+                   const unsigned long long* bn2, int64_t tri_len, const unsigned long long* abort_flag,
+                   const int64_t* chunk_ring, const unsigned long long* seq, int ring, cudaStream_t s);
 
 // The tensor-core triangle (pairs_mma.cu) for universes of at least
 // DIC_PAIR_TC_MIN items (default 128); DIC_PAIR_TC=0 keeps the LOP3/POPC
@@ -386,7 +386,8 @@ int count_pairs_launch(const uint32_t* tids, int64_t n, int m, int64_t first, in
     // with a chunk ring, [first, last] only sizes the grid (the largest chunk)
     if (last < first || m < 2) return DIC_OK;
     if (pair_use_tc(m))
-        return pair_tc_launch(tids, m, chunk_geom(first, last), tri, bn2, tri_len, abort_flag, chunk_ring, seq, ring, s);
+        return pair_tc_launch(tids, n, m, chunk_geom(first, last), tri, bn2, tri_len, abort_flag, chunk_ring, seq, ring,
+                              s);
     if (!sched && !(sched = stream_sched(s))) {
         set_error("dic_count_pairs: no device memory for the grain counters");
         return DIC_ENOMEM;
