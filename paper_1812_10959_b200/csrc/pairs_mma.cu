@@ -12,7 +12,8 @@
 //     of the upper triangle, 8-word stage of the chunk) space;
 //   * warp 13 streams the bits of the coming stages into a shared-memory ring
 //     with TMA (cp.async.bulk.tensor over a 3-D view of the tids tiles: word,
-//     item, tile — items past L come back zero-filled);
+//     item, tile — items past L come back zero-filled; 32-byte swizzle, so
+//     the expanders' reads are conflict-free);
 //   * 12 expander warps turn each item's 8 words into 8 x 16 bytes of E2M1
 //     nibbles — nibble k of u32 q holds row 4k + (1, 0, 2, 3)[q] of the word,
 //     one permutation of the K axis applied to A and B alike, so the dot
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
         const uint32_t step = isA ? kTcAStep : kTcBStep;
         const uint32_t off0 = (isA ? 0u : kTcMmas * kTcAStep) + (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
         const uint32_t boff = (isA ? 0u : kTcBitsA) + (uint32_t)row * (kTcKW * 4);
+        const uint32_t bsw = ((uint32_t)row >> 2 & 1u) * 16u;  // SWIZZLE_32B: chunk bit 4 ^= address bit 7
         uint32_t* xp = xpose + (warp - 1) * 32 * 33;
         int s = 0, r = 0;
         uint32_t ph = 0, rph = 0, ue = 0;
@@ -312,9 +314,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
             const int edge1 = (int)(walk.nst - 1 - sg.st0);
             for (int j = 0; j < n; ++j) {
                 mbar_wait(&bfull[r], rph);
+                // the TMA box is 32-byte swizzled (16-byte chunk c of row e at
+                // chunk c ^ bit 2 of e): the 8 rows of a quarter-warp's load
+                // cover all 8 bank groups
                 const uint8_t* bsrc = bits + (size_t)r * kTcBitStage + boff;
-                const uint4 a0 = *reinterpret_cast<const uint4*>(bsrc);
-                const uint4 a1 = *reinterpret_cast<const uint4*>(bsrc + 16);
+                const uint4 a0 = *reinterpret_cast<const uint4*>(bsrc + bsw);
+                const uint4 a1 = *reinterpret_cast<const uint4*>(bsrc + (16u ^ bsw));
                 uint32_t wv[kTcKW] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bempty[r]);
@@ -426,7 +431,7 @@ static int make_map(CUtensorMap* map, const uint32_t* tids, int L, int64_t tiles
     cuuint32_t box[3] = {(cuuint32_t)kTcKW, (cuuint32_t)box_items, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(tids), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("pair_tc: cuTensorMapEncodeTiled failed (%d)", (int)r);
