@@ -8,8 +8,9 @@
 // becomes the 4-bit value 1.0 = 0b0010), every E8M0 block scale 1.0, f32
 // accumulators in TMEM, exact because a unit spans fewer than 2^24 rows:
 //
-//   * a persistent CTA per SM walks an equal share of (128 x 256 output tile
-//     of the upper triangle, 8-word stage of the chunk) space;
+//   * a persistent CTA per SM owns a slice of the chunk's 8-word stages for
+//     one 128 x 256 output tile of the upper triangle (G / T or G / T + 1
+//     CTAs per tile);
 //   * warp 13 streams the bits of the coming stages into a shared-memory ring
 //     with TMA (cp.async.bulk.tensor over a 3-D view of the tids tiles: word,
 //     item, tile — items past L come back zero-filled; 32-byte swizzle, so
@@ -168,7 +169,52 @@ struct TcWalk {
         w += sg->st1 - sg->st0;
         return true;
     }
+    // The CTA's share.  With at least one CTA per tile, the grid is split
+    // tile by tile (tile t gets G / T or G / T + 1 CTAs, each a contiguous
+    // slice of its stages): every CTA then owns ONE segment, so no CTA drains
+    // and refills its accumulator mid-way (up to 1 / (G / T) more stages for
+    // the busiest CTA, against an epilogue of ~8 us).  Fewer CTAs than tiles:
+    // the flat equal split of (tile, stage) space.
+    __device__ __forceinline__ void share(int b, int G) {
+        const int T = tt.T;
+        if (G >= T) {
+            const int per = G / T, extra = G % T;  // tiles t < extra get per + 1 CTAs
+            const int big = extra * (per + 1);
+            int t, i, c;
+            if (b < big) {
+                t = b / (per + 1);
+                i = b - t * (per + 1);
+                c = per + 1;
+            } else {
+                t = extra + (b - big) / per;
+                i = (b - big) - (t - extra) * per;
+                c = per;
+            }
+            w = (int64_t)t * nst + nst * i / c;
+            we = (int64_t)t * nst + nst * (i + 1) / c;
+        } else {
+            const int64_t W = (int64_t)T * nst;
+            w = W * b / G;
+            we = W * (b + 1) / G;
+        }
+    }
 };
+
+#ifdef DIC_LAB_TIMING
+// lab build: per-CTA phase stamps (globaltimer ns): start, TMEM ready,
+// first stage issued, main loop done (accumulator full), epilogue done, exit
+__device__ unsigned long long g_lab_tc[1024][6];
+#define TC_STAMP(i)                                                          \
+    do {                                                                     \
+        unsigned long long _t;                                               \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));               \
+        g_lab_tc[blockIdx.x][i] = _t;                                        \
+    } while (0)
+#else
+#define TC_STAMP(i) \
+    do {            \
+    } while (0)
+#endif
 
 template <int TW>
 __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -186,6 +232,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
         geom = chunk_geom(f, l);
     }
     extern __shared__ __align__(1024) uint8_t smem[];
+    if (threadIdx.x == 0) TC_STAMP(0);
     uint8_t* ops = smem + 1024;  // [stage][A: 4 MMAs x 4 KB][B: 4 MMAs x 8 KB]
     uint8_t* bits = ops + (size_t)kTcStages * kTcStageBytes;  // [bit stage][A items x 8 words][B items x 8 words]
     uint32_t* xpose = reinterpret_cast<uint32_t*>(bits + (size_t)kTcBitStages * kTcBitStage);
@@ -203,9 +250,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
     const int64_t g0 = geom.g_first & ~(int64_t)(kTcKW - 1);
     walk.nst = (geom.g_last - g0) / kTcKW + 1;
     walk.cap = ((int64_t)1 << 23) / (32 * kTcKW);
-    const int64_t W = (int64_t)walk.tt.T * walk.nst;
-    walk.w = W * blockIdx.x / gridDim.x;
-    walk.we = W * (blockIdx.x + 1) / gridDim.x;
+    walk.share(blockIdx.x, gridDim.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
@@ -239,6 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) TC_STAMP(1);
 
     if (warp == 0) {
         // ---------------- MMA issuer
@@ -261,6 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
                                umma_desc(sb + kk * kTcBStep, kTcBStep / 2, 128), (st > sg.st0 || kk > 0) ? 1u : 0u,
                                tmem + 256u, tmem + 384u);
                     tc_commit(&empty[s]);  // the stage's buffers are free once these MMAs are done
+                    if (st == sg.st0 && ue == 0) TC_STAMP(2);
                     if (++s == kTcStages) {
                         s = 0;
                         ph ^= 1u;
@@ -368,6 +415,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
             if (warp <= 8) {
                 mbar_wait(acc_full, ue & 1);
                 tc_fence_after();
+                if (threadIdx.x == 32) TC_STAMP(3);
                 const int q = warp & 3, half = (warp - 1) >> 2;
                 const int ar = sg.a0 + q * 32;  // first row of this warp's lanes
                 for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
@@ -391,17 +439,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) pair_tc_kernel(const __grid_con
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acc_empty);
+                if (threadIdx.x == 32) TC_STAMP(4);
             }
             ++ue;
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TC_STAMP(5);
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcCols));
     }
 }
+
+#ifdef DIC_LAB_TIMING
+extern "C" int dic_lab_tc_stamps(unsigned long long* host) {
+    cudaDeviceSynchronize();
+    DIC_CUDA(cudaMemcpyFromSymbol(host, g_lab_tc, sizeof(g_lab_tc)));
+    return DIC_OK;
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // host: tensor maps over the tids tiles (a 3-D view: word-in-row x item x
