@@ -277,10 +277,19 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
     const int64_t total = sdoff[kuse];
     // pair counts come from the triangle while the pair bucket is dense
     const bool dense = pa.tri != nullptr && 2 * (int64_t)stat[S_HEAD + 2 * KS + 2] >= pa.tri_len;
+    // per-CTA tallies: one global atomic per CTA and counter at the end (a
+    // per-warp atomic on the same status word serialises at the L2 slice:
+    // 15.6k of them per stop during the 500k-slot pair wave)
+    __shared__ unsigned long long s_rem[kDoffMax];
+    __shared__ unsigned long long s_cnt[3];  // pruned, finalized, survivors
+    for (int i = threadIdx.x; i < kuse; i += blockDim.x) s_rem[i] = 0;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned n_pr = 0, n_fi = 0, n_su = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t span = ((total + stride - 1) / stride) * stride;  // uniform trip count for the warp votes
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < span; g += stride) {
-        bool pruned = false, fin = false, surv = false, gone = false;
+        bool gone = false;
         int bk = 0;
         if (g < total) {
             while (bk + 1 < kuse && g >= sdoff[bk + 1]) ++bk;
@@ -317,14 +326,14 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
                         frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r;
                     } else if (bound && iv < stop_max && s + interval * (stop_max - iv) < need) {
                         sh = NIL;
-                        pruned = true;
+                        ++n_pr;
                     }
                 }
                 if (is_dashed(sh)) {
-                    surv = true;
+                    ++n_su;
                     if (iv == stop_max) {
                         sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
-                        fin = true;
+                        ++n_fi;
                     }
                 }
                 R.shape[r] = sh;
@@ -333,21 +342,29 @@ __global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab
             keep[g] = kept ? 1 : 0;
             gone = !kept;
         }
-        const unsigned full = 0xFFFFFFFFu;
-        const unsigned pr = __ballot_sync(full, pruned), fi = __ballot_sync(full, fin);
-        const unsigned su = __ballot_sync(full, surv);
-        if ((threadIdx.x & 31) == 0) {
-            if (pr) atomicAdd(&stat[S_NPRUNED], (unsigned long long)__popc(pr));
-            if (fi) atomicAdd(&stat[S_NFINAL], (unsigned long long)__popc(fi));
-            if (su) atomicAdd(&stat[S_SURV], (unsigned long long)__popc(su));
-        }
-        // removed[k], aggregated over the lanes of the same bucket
-        const unsigned gm = __ballot_sync(full, gone);
+        // removed[k], aggregated over the lanes of the same bucket (shared atomics)
+        const unsigned gm = __ballot_sync(0xFFFFFFFFu, gone);
         if (gone) {
             const unsigned same = __match_any_sync(gm, bk);
-            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&stat[S_HEAD + bk], (unsigned long long)__popc(same));
+            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_rem[bk], (unsigned long long)__popc(same));
         }
     }
+    n_pr = __reduce_add_sync(0xFFFFFFFFu, n_pr);
+    n_fi = __reduce_add_sync(0xFFFFFFFFu, n_fi);
+    n_su = __reduce_add_sync(0xFFFFFFFFu, n_su);
+    if ((threadIdx.x & 31) == 0) {
+        if (n_pr) atomicAdd(&s_cnt[0], (unsigned long long)n_pr);
+        if (n_fi) atomicAdd(&s_cnt[1], (unsigned long long)n_fi);
+        if (n_su) atomicAdd(&s_cnt[2], (unsigned long long)n_su);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_cnt[0]) atomicAdd(&stat[S_NPRUNED], s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&stat[S_NFINAL], s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&stat[S_SURV], s_cnt[2]);
+    }
+    for (int i = threadIdx.x; i < kuse; i += blockDim.x)
+        if (s_rem[i]) atomicAdd(&stat[S_HEAD + i], s_rem[i]);
 }
 
 // Order-preserving in-place compaction (compact_dashed, itemsets.py:130-132)
@@ -430,7 +447,8 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
                                        unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
                                        int32_t* __restrict__ tmp_size, int64_t tmp_cap,
                                        unsigned long long* __restrict__ stat, int KS, int64_t rec_cap, int64_t hcap,
-                                       const int64_t* __restrict__ bcap) {
+                                       const int64_t* __restrict__ bcap, const int32_t* __restrict__ prank,
+                                       int64_t prec0) {
     // nothing promoted: no joins, OVERFLOW stays 0 (reset by the last status)
     if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
     const int64_t total = (int64_t)stat[S_NFRONT] * L;
@@ -463,10 +481,22 @@ __global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, con
             // the subset test rejects almost every join (its first subset
             // is rarely a box yet), so it runs before the "already known"
             // lookup; the admitted set is the same in either order
-            for (int q = 0; q < k && ok; ++q) {
-                const int d = its[q];
-                const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, k, l, d, k);
-                ok = e >= 0 && is_box(R.shape[e]);
+            if (k == 2 && prank) {
+                // a pair source (the pair wave's joins): its immediate subsets
+                // {a, l} and {b, l} are seeded pairs of frequent items, whose
+                // record ids follow from the items' level1 ranks (record
+                // prec0 + triangle slot, seed_pairs_kernel): one load each
+                // instead of a hash probe chain.  l = level1[j] has rank j.
+                const int64_t ra = prank[its[0]], rb = prank[its[1]];
+                const int64_t pa = ra < j ? tri_pos(ra, j, L) : tri_pos(j, ra, L);
+                const int64_t pb = rb < j ? tri_pos(rb, j, L) : tri_pos(j, rb, L);
+                ok = is_box(R.shape[prec0 + pb]) && is_box(R.shape[prec0 + pa]);
+            } else {
+                for (int q = 0; q < k && ok; ++q) {
+                    const int d = its[q];
+                    const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, k, l, d, k);
+                    ok = e >= 0 && is_box(R.shape[e]);
+                }
             }
             if (!ok) continue;
             if (ht_find_items(ht, hmask, R, W, hc, its, k, l, -1, k + 1) >= 0) continue;  // already known
@@ -1367,7 +1397,8 @@ int candidate_step(dic_engine* e, cudaStream_t s) {
     unsigned long long* st = e->d_stat;
     eval_candidates_kernel<<<G, 256, 0, s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
                                                  (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
-                                                 e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap);
+                                                 e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap, e->rank,
+                                                 (int64_t)e->m);
     ::dic::note_launch();
     dedup_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht, (uint64_t)e->hcap - 1, st,
                                    e->tmp_slot, e->tmp_keys, e->ins_k);
