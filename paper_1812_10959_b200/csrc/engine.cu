@@ -101,7 +101,7 @@ enum : int {
     S_NREC = 7,      // records (persistent)
     S_ABORT = 8,     // persistent: set with OVERFLOW, cleared by the host's replay
     S_SCRATCH = 9,   // scratch word (result collection)
-    S_DONE = 10,     // eval blocks finished (last one runs the capacity check)
+    S_DONE = 10,     // (unused)
     S_SEQ = 11,      // persistent: stops completed (the status kernel advances it)
     S_HEAD = 12
 };
@@ -119,6 +119,7 @@ struct Records {
     int64_t* intervals = nullptr;
     int32_t* size = nullptr;
     uint8_t* shape = nullptr;
+    uint16_t* items = nullptr;  // [cap][8] ascending item ids of itemsets of <= 8 items (zero padded)
     int64_t cap = 0;
 };
 
@@ -148,7 +149,8 @@ __device__ __forceinline__ int32_t ht_lookup(const hent_t* __restrict__ ht, uint
         const hent_t x = ht[slot];
         const int32_t e = hent_id(x);
         if (e == kEmpty) return -1;
-        if (hent_tag(x) == tag && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
+        // (temporary entries: this stop's unpublished joins, never a record)
+        if (hent_tag(x) == tag && !(e & kTempFlag) && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
         slot = (slot + 1) & hmask;
     }
 }
@@ -158,7 +160,6 @@ __device__ __forceinline__ int32_t ht_lookup(const hent_t* __restrict__ ht, uint
 // mask: a record of the same size holding every item of the set IS the set.
 // The per-item bit loads are independent, so a confirmation costs one memory
 // latency instead of W dependent word compares.
-constexpr int kEvalK = 24;  // frontier itemsets up to this size take the item-list path
 __device__ __forceinline__ int32_t ht_find_items(const hent_t* __restrict__ ht, uint64_t hmask, const Records& R,
                                                  int W, uint64_t h, const int* its, int k, int add, int drop,
                                                  int size) {
@@ -168,7 +169,7 @@ __device__ __forceinline__ int32_t ht_find_items(const hent_t* __restrict__ ht, 
         const hent_t x = ht[slot];
         const int32_t e = hent_id(x);
         if (e == kEmpty) return -1;
-        if (hent_tag(x) == tag && R.size[e] == size) {
+        if (hent_tag(x) == tag && !(e & kTempFlag) && R.size[e] == size) {
             const unsigned long long* rm = R.mask + (int64_t)e * W;
             bool ok = add < 0 || ((rm[add >> 6] >> (add & 63)) & 1ull);
             for (int q = 0; q < k; ++q) {
@@ -207,6 +208,7 @@ __global__ void seed_singletons_kernel(Records R, int W, int m, const int64_t* _
     if (i >= m) return;
     for (int w = 0; w < W; ++w) R.mask[(int64_t)i * W + w] = (w == (i >> 6)) ? (1ull << (i & 63)) : 0ull;
     R.hash[i] = zob((uint32_t)i);
+    for (int q = 0; q < 8; ++q) R.items[(int64_t)i * 8 + q] = q == 0 ? (uint16_t)i : (uint16_t)0;
     R.size[i] = 1;
     R.support[i] = counts[i];
     R.intervals[i] = stop_max;
@@ -235,6 +237,7 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
         R.mask[r * W + w] = x;
     }
     R.hash[r] = zob(ia) ^ zob(ib);
+    *reinterpret_cast<uint4*>(R.items + r * 8) = make_uint4((uint32_t)ia | ((uint32_t)ib << 16), 0u, 0u, 0u);
     R.size[r] = 2;
     R.support[r] = 0;
     R.intervals[r] = 0;
@@ -245,16 +248,32 @@ __global__ void seed_pairs_kernel(Records R, int W, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// per stop (every kernel: no-op while the abort flag is up)
+// per stop: ONE persistent cooperative kernel runs the whole checkpoint half
 // ---------------------------------------------------------------------------
-// support += delta, intervals += 1 (count_support_interval), then prune
-// (engine.py:292-310) and check_full_pass (:380-388), grid-stride over every
-// bucket slot.  Slots already dead (left the dashed vector at an earlier
-// stop, compaction pending) are only marked not-kept.  keep[g] = still dashed.
+// count_support_interval's "support += delta" and everything _run does after
+// it at a stop (engine.py:430-441: prune, make_candidates, peak_dashed,
+// check_full_pass) as the phases of one kernel, one CTA per SM, separated by
+// grid-wide barriers instead of kernel boundaries:
+//
+//   P1  apply      support += delta, intervals += 1, prune, check_full_pass,
+//                  keep flags, frontier (every CTA, grid-stride over the slots)
+//   --- barrier ---
+//   P2  compaction of the buckets the last status flagged (CTA k = bucket k)
+//       evaluation of the frontier x level1 joins (every CTA, after its bucket)
+//   --- barrier ---  (nothing promoted: straight to the status)
+//   P3  all-or-nothing capacity check (every CTA, same inputs, same verdict),
+//       dedup: one owner per distinct admitted mask
+//   --- barrier ---
+//   P4  canonical commit: one warp per new candidate ranks it and writes it
+//   last CTA out   bucket sizes after the commit, the stop's status snapshot
+//
+// Five kernel launches per stop became one: what is left of a phase is its
+// dependent-load chain (a few microseconds) plus ~1 us per barrier.  The
+// overflow replay (dic_engine_poll) runs the same kernel from P2's join
+// evaluation on (replay = 1).
 struct PairArgs {  // the dense pair triangle (tri == nullptr: none)
     unsigned long long* tri;
     const int32_t* rank;
-    uint16_t* const* items_tab;
     int64_t L, tri_len;
     int64_t rec0;  // record id of seeded pair 0: pair p = record rec0 + p = triangle slot p
 };
@@ -263,133 +282,241 @@ __device__ __forceinline__ int64_t tri_pos(int64_t a, int64_t b, int64_t L) {
     return a * L - a * (a + 1) / 2 + (b - a - 1);
 }
 
-__global__ void apply_prune_finalize_kernel(int32_t* const* __restrict__ rec_tab, const int64_t* __restrict__ doff,
-                                            int kuse, unsigned long long* __restrict__ delta, Records R,
-                                            int64_t need, int64_t interval, int64_t stop_max, int bound,
-                                            int32_t* __restrict__ frontier, int32_t* __restrict__ keep,
-                                            unsigned long long* __restrict__ stat, PairArgs pa, int KS) {
-    if (stat[S_ABORT]) return;
-    // the bucket offsets in shared memory: each slot's bucket search is then
-    // a few shared loads instead of a chain of dependent global ones
-    __shared__ int64_t sdoff[kDoffMax + 1];
-    for (int i = threadIdx.x; i <= kuse; i += blockDim.x) sdoff[i] = doff[i];
+struct JoinRec;
+
+constexpr int kCkptThreads = 1024;    // one CTA per SM
+constexpr int kCompactItems = 16384;  // staged item ids per compaction chunk (32 KB)
+
+// Buffers written by one phase and read by a later one are reached through
+// plain (not __restrict__ const) pointers: loads must stay coherent across the
+// grid barriers, which the non-coherent read-only path is not.
+struct CkptArgs {
+    int32_t* const* rec_tab;      // per-size bucket tables
+    uint16_t* const* items_tab;
+    const int64_t* bcap;
+    int64_t* doff;                // per-size delta offsets (rewritten by the status)
+    unsigned long long* delta;
+    Records R;
+    int64_t need, interval, stop_max;
+    int32_t* frontier;
+    int32_t* keep;
+    unsigned long long* stat;
+    PairArgs pa;
+    const int32_t* level1;
+    hent_t* ht;
+    uint64_t hmask;
+    JoinRec* joins;               // this stop's admitted joins (eval -> commit)
+    int64_t tmp_cap, rec_cap, hcap;
+    unsigned long long* ins_k;    // [kDoffMax] new candidates by size (eval -> commit)
+    unsigned long long* ring;     // host-mapped status ring
+    int64_t ring_words;
+    unsigned long long* sync;     // [0] grid-barrier arrivals, [1] CTAs out (both zero between launches),
+                                  // [2] CTA 0's verdict of a small stop, tagged with the stop's sequence number
+    int32_t W, KS, kuse_issue, kuse, bound, replay;
+};
+
+struct CkptSmem {
+    int64_t doff[kDoffMax + 1];         // apply: bucket offsets; commit: start[]
+    int64_t bn0[kDoffMax];              // commit: bucket fill before the commit
+    int32_t* rec[kDoffMax];             // apply: bucket record tables
+    unsigned long long rem[kDoffMax];   // apply: dead slots per bucket (this CTA)
+    unsigned long long cnt[3];          // apply: pruned, finalized, survivors (this CTA)
+    uint16_t items[kCompactItems];      // compaction staging
+    int32_t pos[kCkptThreads];
+    int32_t wsum[32];
+    int32_t ctotal;
+    int64_t nrec0;
+    int flag;
+};
+
+#ifdef DIC_LAB_TIMING
+// lab build: per-stop phase stamps of CTA 0 (globaltimer ns), slot S_SEQ % 512
+__device__ unsigned long long g_lab_commit[512][8];
+#define CKPT_STAMP(i)                                                                        \
+    do {                                                                                     \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                                           \
+            unsigned long long _t;                                                           \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
+            g_lab_commit[a.stat[S_SEQ] % 512][i] = _t;                                       \
+        }                                                                                    \
+    } while (0)
+#else
+#define CKPT_STAMP(i) \
+    do {              \
+    } while (0)
+#endif
+
+// Grid-wide barrier of the co-resident CTAs of a cooperative launch: arrival
+// counter in global memory, target = arrivals expected so far.  Thread 0
+// publishes the CTA's writes (fence), arrives, spins, then fences again before
+// releasing the CTA, so every write before the barrier is visible to every
+// thread after it.
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
     __syncthreads();
-    const int64_t total = sdoff[kuse];
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// P1.  support += delta, intervals += 1 (count_support_interval), then prune
+// (engine.py:292-310) and check_full_pass (:380-388) over every bucket slot.
+// Slots already dead (left the dashed vector at an earlier stop, compaction
+// pending) are only marked not-kept.  keep[g] = still dashed.  A thread takes
+// four slots at a time and issues each level of their dependent loads
+// (record id -> record fields and count) together.
+__device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int cta, int nctas) {
+    unsigned long long* stat = a.stat;
+    const int kuse = a.kuse_issue;
+    const Records& R = a.R;
+    for (int i = threadIdx.x; i <= kuse; i += blockDim.x) sm.doff[i] = a.doff[i];
+    for (int i = threadIdx.x; i < kuse; i += blockDim.x) {
+        sm.rem[i] = 0;
+        sm.rec[i] = a.rec_tab[i];
+    }
+    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t total = sm.doff[kuse];
     // pair counts come from the triangle while the pair bucket is dense
-    const bool dense = pa.tri != nullptr && 2 * (int64_t)stat[S_HEAD + 2 * KS + 2] >= pa.tri_len;
-    // per-CTA tallies: one global atomic per CTA and counter at the end (a
-    // per-warp atomic on the same status word serialises at the L2 slice:
-    // 15.6k of them per stop during the 500k-slot pair wave)
-    __shared__ unsigned long long s_rem[kDoffMax];
-    __shared__ unsigned long long s_cnt[3];  // pruned, finalized, survivors
-    for (int i = threadIdx.x; i < kuse; i += blockDim.x) s_rem[i] = 0;
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
+    const bool dense = a.pa.tri != nullptr && 2 * (int64_t)stat[S_HEAD + 2 * a.KS + 2] >= a.pa.tri_len;
     unsigned n_pr = 0, n_fi = 0, n_su = 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t span = ((total + stride - 1) / stride) * stride;  // uniform trip count for the warp votes
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < span; g += stride) {
-        bool gone = false;
-        int bk = 0;
-        if (g < total) {
-            while (bk + 1 < kuse && g >= sdoff[bk + 1]) ++bk;
-            const int64_t c = g - sdoff[bk];
-            const int32_t r = rec_tab[bk][c];
-            uint8_t sh = R.shape[r];
-            bool kept = false;
-            int64_t dg = 0;
-            if (!(bk == 2 && dense)) {
-                // (dense pairs are counted into the triangle: their delta slots stay zero)
-                dg = (int64_t)delta[g];
-                delta[g] = 0;  // the buffer is zero again for the next stop's count
-            } else {
-                // until the bucket is first compacted, slot c still holds the
-                // seeded pair c (record rec0 + c, triangle slot c): no item /
-                // rank lookups on the dependent-load chain
-                int64_t p = c;
-                if ((int64_t)r != pa.rec0 + c) {
-                    const uint16_t* it = pa.items_tab[2] + 2 * c;
-                    p = tri_pos(pa.rank[it[0]], pa.rank[it[1]], pa.L);
-                }
-                dg = (int64_t)pa.tri[p];
-                pa.tri[p] = 0;  // each pair has one slot: zero again for the next stop
+    constexpr int B = 4;
+    const int64_t nth = (int64_t)nctas * blockDim.x;
+    const int64_t tid = (int64_t)cta * blockDim.x + threadIdx.x;
+    const int64_t iters = (total + nth * B - 1) / (nth * B);  // uniform trip count for the warp votes
+    for (int64_t it = 0; it < iters; ++it) {
+        int64_t g[B], c[B];
+        int bk[B];
+        int32_t r[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            g[i] = (it * B + i) * nth + tid;
+            bk[i] = 0;
+            c[i] = 0;
+            r[i] = -1;
+            if (g[i] < total) {
+                int b = 0;
+                while (b + 1 < kuse && g[i] >= sm.doff[b + 1]) ++b;
+                bk[i] = b;
+                c[i] = g[i] - sm.doff[b];
+                r[i] = sm.rec[b][c[i]];
             }
-            if (is_dashed(sh)) {
-                const int64_t s = R.support[r] + dg;
-                const int64_t iv = R.intervals[r] + 1;
-                R.support[r] = s;
-                R.intervals[r] = iv;
-                if (sh == DASHED_CIRCLE) {
-                    if (s >= need) {
-                        sh = DASHED_BOX;
-                        // order among promoted records is irrelevant to results and stats
-                        frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r;
-                    } else if (bound && iv < stop_max && s + interval * (stop_max - iv) < need) {
-                        sh = NIL;
-                        ++n_pr;
-                    }
-                }
-                if (is_dashed(sh)) {
-                    ++n_su;
-                    if (iv == stop_max) {
-                        sh = s >= need ? SOLID_BOX : SOLID_CIRCLE;
-                        ++n_fi;
-                    }
-                }
-                R.shape[r] = sh;
-                kept = is_dashed(sh);
-            }
-            keep[g] = kept ? 1 : 0;
-            gone = !kept;
         }
-        // removed[k], aggregated over the lanes of the same bucket (shared atomics)
-        const unsigned gm = __ballot_sync(0xFFFFFFFFu, gone);
-        if (gone) {
-            const unsigned same = __match_any_sync(gm, bk);
-            if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_rem[bk], (unsigned long long)__popc(same));
+        uint8_t sh[B];
+        int64_t sup[B], iv[B], dg[B], tp[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            sh[i] = NIL;
+            sup[i] = iv[i] = dg[i] = 0;
+            tp[i] = -1;
+            if (r[i] >= 0) {
+                sh[i] = R.shape[r[i]];
+                sup[i] = R.support[r[i]];
+                iv[i] = R.intervals[r[i]];
+                if (!(bk[i] == 2 && dense)) {
+                    // (dense pairs are counted into the triangle: their delta slots stay zero)
+                    dg[i] = (int64_t)a.delta[g[i]];
+                } else {
+                    // until the bucket is first compacted, slot c still holds the
+                    // seeded pair c (record rec0 + c, triangle slot c): no item /
+                    // rank lookups on the dependent-load chain
+                    int64_t p = c[i];
+                    if ((int64_t)r[i] != a.pa.rec0 + c[i]) {
+                        const uint16_t* its = a.items_tab[2] + 2 * c[i];
+                        p = tri_pos(a.pa.rank[its[0]], a.pa.rank[its[1]], a.pa.L);
+                    }
+                    tp[i] = p;
+                    dg[i] = (int64_t)a.pa.tri[p];
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            bool gone = false;
+            if (r[i] >= 0) {
+                // the count buffers are zero again for the next stop's count
+                if (dg[i]) {
+                    if (tp[i] >= 0) a.pa.tri[tp[i]] = 0;
+                    else a.delta[g[i]] = 0;
+                }
+                uint8_t s = sh[i];
+                bool kept = false;
+                if (is_dashed(s)) {
+                    const int64_t sp = sup[i] + dg[i];
+                    const int64_t v = iv[i] + 1;
+                    if (dg[i]) R.support[r[i]] = sp;
+                    R.intervals[r[i]] = v;
+                    if (s == DASHED_CIRCLE) {
+                        if (sp >= a.need) {
+                            s = DASHED_BOX;
+                            // order among promoted records is irrelevant to results and stats
+                            a.frontier[atomicAdd(&stat[S_NFRONT], 1ull)] = r[i];
+                        } else if (a.bound && v < a.stop_max && sp + a.interval * (a.stop_max - v) < a.need) {
+                            s = NIL;
+                            ++n_pr;
+                        }
+                    }
+                    if (is_dashed(s)) {
+                        ++n_su;
+                        if (v == a.stop_max) {
+                            s = sp >= a.need ? SOLID_BOX : SOLID_CIRCLE;
+                            ++n_fi;
+                        }
+                    }
+                    if (s != sh[i]) R.shape[r[i]] = s;
+                    kept = is_dashed(s);
+                }
+                a.keep[g[i]] = kept ? 1 : 0;
+                gone = !kept;
+            }
+            // removed[k], aggregated over the lanes of the same bucket (shared atomics)
+            const unsigned gm = __ballot_sync(0xFFFFFFFFu, gone);
+            if (gone) {
+                const unsigned same = __match_any_sync(gm, bk[i]);
+                if ((threadIdx.x & 31) == __ffs(same) - 1)
+                    atomicAdd(&sm.rem[bk[i]], (unsigned long long)__popc(same));
+            }
         }
     }
+    // per-CTA tallies: one global atomic per CTA and counter (a per-warp atomic
+    // on the same status word serialises at the L2 slice)
     n_pr = __reduce_add_sync(0xFFFFFFFFu, n_pr);
     n_fi = __reduce_add_sync(0xFFFFFFFFu, n_fi);
     n_su = __reduce_add_sync(0xFFFFFFFFu, n_su);
     if ((threadIdx.x & 31) == 0) {
-        if (n_pr) atomicAdd(&s_cnt[0], (unsigned long long)n_pr);
-        if (n_fi) atomicAdd(&s_cnt[1], (unsigned long long)n_fi);
-        if (n_su) atomicAdd(&s_cnt[2], (unsigned long long)n_su);
+        if (n_pr) atomicAdd(&sm.cnt[0], (unsigned long long)n_pr);
+        if (n_fi) atomicAdd(&sm.cnt[1], (unsigned long long)n_fi);
+        if (n_su) atomicAdd(&sm.cnt[2], (unsigned long long)n_su);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (s_cnt[0]) atomicAdd(&stat[S_NPRUNED], s_cnt[0]);
-        if (s_cnt[1]) atomicAdd(&stat[S_NFINAL], s_cnt[1]);
-        if (s_cnt[2]) atomicAdd(&stat[S_SURV], s_cnt[2]);
+        if (sm.cnt[0]) atomicAdd(&stat[S_NPRUNED], sm.cnt[0]);
+        if (sm.cnt[1]) atomicAdd(&stat[S_NFINAL], sm.cnt[1]);
+        if (sm.cnt[2]) atomicAdd(&stat[S_SURV], sm.cnt[2]);
     }
     for (int i = threadIdx.x; i < kuse; i += blockDim.x)
-        if (s_rem[i]) atomicAdd(&stat[S_HEAD + i], s_rem[i]);
+        if (sm.rem[i]) atomicAdd(&stat[S_HEAD + i], sm.rem[i]);
 }
 
-// Order-preserving in-place compaction (compact_dashed, itemsets.py:130-132)
-// of every bucket the previous status flagged, one CTA per bucket: chunks of
-// E slots are scanned (keep flags of this stop's apply), staged in shared
-// memory and written back to their compacted positions, which never pass the
-// chunk being read.  bn[k] = kept, removed[k] = cflag[k] = 0.
-constexpr int kCompactThreads = 1024;
-constexpr int kCompactItems = 16384;  // staged item ids per chunk (32 KB)
-__global__ void __launch_bounds__(kCompactThreads) compact_flagged_kernel(
-    int32_t* const* __restrict__ rec_tab, uint16_t* const* __restrict__ items_tab,
-    const int64_t* __restrict__ doff, const int32_t* __restrict__ keep_all, unsigned long long* stat, int KS) {
-    const int k = blockIdx.x;
-    unsigned long long* cflag = stat + S_HEAD + 3 * KS;
-    if (stat[S_ABORT] || !cflag[k]) return;
-    __shared__ uint16_t sitems[kCompactItems];
-    __shared__ int32_t spos[kCompactThreads];
-    __shared__ int32_t wsum[32];
-    __shared__ int32_t ctotal;
-    unsigned long long* bn = stat + S_HEAD + 2 * KS;
+// P2a.  Order-preserving in-place compaction (compact_dashed,
+// itemsets.py:130-132) of bucket k by one CTA: chunks of E slots are scanned
+// (keep flags of this stop's apply), staged in shared memory and written back
+// to their compacted positions, which never pass the chunk being read.
+// bn[k] = kept, removed[k] = cflag[k] = 0.
+__device__ __forceinline__ void compact_bucket(const CkptArgs& a, CkptSmem& sm, int k) {
+    unsigned long long* stat = a.stat;
+    unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
     const int64_t n = (int64_t)bn[k];
-    const int32_t* keep = keep_all + doff[k];
-    int32_t* rec = rec_tab[k];
-    uint16_t* items = items_tab[k];
-    const int E = min(kCompactThreads, kCompactItems / k);
+    const int32_t* keep = a.keep + a.doff[k];
+    int32_t* rec = a.rec_tab[k];
+    uint16_t* items = a.items_tab[k];
+    const int E = min(kCkptThreads, kCompactItems / k);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int64_t out = 0;
     for (int64_t base = 0; base < n; base += E) {
@@ -399,30 +526,30 @@ __global__ void __launch_bounds__(kCompactThreads) compact_flagged_kernel(
         const int kp = valid ? keep[base + e] : 0;
         const int32_t r = valid ? rec[base + e] : 0;
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, kp);
-        if (lane == 0) wsum[wid] = __popc(bal);
-        for (int j = threadIdx.x; j < cnt * k; j += kCompactThreads) sitems[j] = items[base * k + j];
+        if (lane == 0) sm.wsum[wid] = __popc(bal);
+        for (int j = threadIdx.x; j < cnt * k; j += kCkptThreads) sm.items[j] = items[base * k + j];
         __syncthreads();
         if (wid == 0) {
-            const int v = wsum[lane];
+            const int v = sm.wsum[lane];
             int x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
                 if (lane >= o) x += y;
             }
-            wsum[lane] = x - v;  // exclusive
-            if (lane == 31) ctotal = x;
+            sm.wsum[lane] = x - v;  // exclusive
+            if (lane == 31) sm.ctotal = x;
         }
         __syncthreads();
-        const int pos = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
-        spos[e] = kp ? pos : -1;
-        const int total = ctotal;
+        const int pos = sm.wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+        sm.pos[e] = kp ? pos : -1;
+        const int total = sm.ctotal;
         __syncthreads();
         if (kp) rec[out + pos] = r;
-        for (int j = threadIdx.x; j < cnt * k; j += kCompactThreads) {
-            const int c = j / k;
-            const int p = spos[c];
-            if (p >= 0) items[(out + p) * k + (j - c * k)] = sitems[j];
+        for (int j = threadIdx.x; j < cnt * k; j += kCkptThreads) {
+            const int cc = j / k;
+            const int p = sm.pos[cc];
+            if (p >= 0) items[(out + p) * k + (j - cc * k)] = sm.items[j];
         }
         __syncthreads();
         out += total;
@@ -430,174 +557,49 @@ __global__ void __launch_bounds__(kCompactThreads) compact_flagged_kernel(
     if (threadIdx.x == 0) {
         bn[k] = (unsigned long long)out;
         stat[S_HEAD + k] = 0;  // removed: none left
-        cflag[k] = 0;
+        stat[S_HEAD + 3 * a.KS + k] = 0;  // cflag
     }
 }
 
-// make_candidates (engine.py:320-369), evaluation: grid-stride over
-// (frontier f, level1 item j) pairs, sizes read from the status words.
+// P2b.  make_candidates (engine.py:320-369): evaluation of the
+// (frontier f, level1 item j) joins, and — in the same pass — the claim of
+// every admitted join in the hash index.
+//
 // Admission needs cand not in known and every immediate subset known with a
 // box shape; the subset equal to src is a box by construction (it was just
-// promoted) and is skipped.
-__device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap, int64_t hcap,
-                               const int64_t* __restrict__ bcap);
-
-__global__ void eval_candidates_kernel(const int32_t* __restrict__ frontier, const int32_t* __restrict__ level1,
-                                       int64_t L, int W, Records R, const hent_t* __restrict__ ht, uint64_t hmask,
-                                       unsigned long long* __restrict__ tmp_mask, uint64_t* __restrict__ tmp_hash,
-                                       int32_t* __restrict__ tmp_size, int64_t tmp_cap,
-                                       unsigned long long* __restrict__ stat, int KS, int64_t rec_cap, int64_t hcap,
-                                       const int64_t* __restrict__ bcap, const int32_t* __restrict__ prank,
-                                       int64_t prec0) {
-    // nothing promoted: no joins, OVERFLOW stays 0 (reset by the last status)
-    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
-    const int64_t total = (int64_t)stat[S_NFRONT] * L;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t f = t / L, j = t - f * L;
-        const int32_t src = frontier[f];
-        const int l = level1[j];
-        const unsigned long long* sm = R.mask + (int64_t)src * W;
-        if ((sm[l >> 6] >> (l & 63)) & 1ull) continue;  // cand == base
-        const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
-        const MaskView cand{sm, l, -1};
-        const int ks = R.size[src];
-        bool ok = true;
-        if (ks < kEvalK && W <= 16) {
-            // item-list path: src's words loaded together, its ids extracted once
-            unsigned long long wv[16];
-#pragma unroll
-            for (int w = 0; w < 16; ++w) wv[w] = w < W ? sm[w] : 0ull;
-            int its[kEvalK];
-            int k = 0;
-#pragma unroll
-            for (int w = 0; w < 16; ++w) {
-                unsigned long long x = wv[w];
-                while (x && k < kEvalK) {
-                    its[k++] = w * 64 + __ffsll((long long)x) - 1;
-                    x &= x - 1;
-                }
-            }
-            // the subset test rejects almost every join (its first subset
-            // is rarely a box yet), so it runs before the "already known"
-            // lookup; the admitted set is the same in either order
-            if (k == 2 && prank) {
-                // a pair source (the pair wave's joins): its immediate subsets
-                // {a, l} and {b, l} are seeded pairs of frequent items, whose
-                // record ids follow from the items' level1 ranks (record
-                // prec0 + triangle slot, seed_pairs_kernel): one load each
-                // instead of a hash probe chain.  l = level1[j] has rank j.
-                const int64_t ra = prank[its[0]], rb = prank[its[1]];
-                const int64_t pa = ra < j ? tri_pos(ra, j, L) : tri_pos(j, ra, L);
-                const int64_t pb = rb < j ? tri_pos(rb, j, L) : tri_pos(j, rb, L);
-                ok = is_box(R.shape[prec0 + pb]) && is_box(R.shape[prec0 + pa]);
-            } else {
-                for (int q = 0; q < k && ok; ++q) {
-                    const int d = its[q];
-                    const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, k, l, d, k);
-                    ok = e >= 0 && is_box(R.shape[e]);
-                }
-            }
-            if (!ok) continue;
-            if (ht_find_items(ht, hmask, R, W, hc, its, k, l, -1, k + 1) >= 0) continue;  // already known
-        } else {
-        for (int w = 0; w < W && ok; ++w) {
-            unsigned long long x = cand.word(w);
-            while (x) {
-                const int bit = w * 64 + __ffsll((long long)x) - 1;
-                x &= x - 1;
-                if (bit == l) continue;
-                const MaskView sub{sm, l, bit};
-                const int32_t e = ht_lookup(ht, hmask, R, W, hc ^ zob((uint32_t)bit), sub);
-                if (e < 0 || !is_box(R.shape[e])) {
-                    ok = false;
-                    break;
-                }
-            }
-        }
-        if (ok && ht_lookup(ht, hmask, R, W, hc, cand) >= 0) continue;  // already known
-        }
-        if (!ok) continue;
-        const unsigned long long pos = atomicAdd(&stat[S_NADM], 1ull);
-        const int sz = R.size[src] + 1;
-        atomicAdd(&stat[S_HEAD + KS + sz], 1ull);  // adm[sz]
-        if ((int64_t)pos < tmp_cap) {
-            for (int w = 0; w < W; ++w) tmp_mask[(int64_t)pos * W + w] = cand.word(w);
-            tmp_hash[pos] = hc;
-            tmp_size[pos] = sz;
-        }
-    }
-    // the last block to finish runs the all-or-nothing capacity check
-    __shared__ int last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(&stat[S_DONE], 1ull) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last) {
-        __threadfence();
-        check_capacity(stat, KS, tmp_cap, rec_cap, hcap, bcap);
-        if (threadIdx.x == 0) stat[S_DONE] = 0;
-    }
-}
-
-// All-or-nothing capacity check for the candidate step (run by the last
-// eval block); an overflow also raises the abort flag so every later stop is
-// skipped until the host's replay.
-__device__ void check_capacity(unsigned long long* stat, int KS, int64_t tmp_cap, int64_t rec_cap, int64_t hcap,
-                               const int64_t* __restrict__ bcap) {
-    __shared__ int over;
-    if (threadIdx.x == 0) {
-        const unsigned long long na = *(volatile unsigned long long*)&stat[S_NADM];
-        over = (int64_t)na > tmp_cap || (int64_t)(stat[S_NREC] + na) > rec_cap ||
-               (int64_t)(stat[S_NREC] + na) * 2 > hcap;
-    }
-    __syncthreads();
-    const volatile unsigned long long* adm = stat + S_HEAD + KS;
-    const unsigned long long* bn = stat + S_HEAD + 2 * KS;
-    for (int k = threadIdx.x; k < KS; k += blockDim.x) {
-        const unsigned long long ak = adm[k];
-        if (ak && (int64_t)(bn[k] + ak) > bcap[k]) over = 1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        stat[S_OVERFLOW] = over ? 1ull : 0ull;
-        if (over) stat[S_ABORT] = 1ull;
-    }
-}
-
-// Candidate commit, in two kernels, with a CANONICAL result: the record ids
-// and bucket positions of a stop's new candidates depend only on the SET of
-// candidates, never on thread timing.  Sharded engines reduce their counts
-// slot by slot, so every rank must lay its buckets out identically
-// (the reference reduces per record, engine.py:268-270); with atomics
-// deciding the order, ranks would add up counts of different itemsets.
+// promoted) and is skipped.  The subset test rejects almost every join (its
+// first subset is rarely a box yet), so it runs first; the admitted set is the
+// same in either order.
 //
-// 1. dedup: the thread whose CAS claims a hash slot for a mask owns that
-//    candidate (a temporary entry kTempFlag | join index until commit); a
-//    thread meeting an occupied slot compares masks and drops its join as a
-//    duplicate (all duplicates carry the same mask, so which join wins does
-//    not matter).  Owners write their sort key to keys[] (in arbitrary order)
-//    and are counted per size in ins_k[].  No record is published in this
-//    kernel, so a non-temporary entry always names a record of an earlier stop.
-// 2. rank_commit_status: the owners are ranked by (size, item ids ascending)
-//    — the order of make_candidates' lexicographic joins, which also makes
-//    candidates sharing a prefix contiguous for the count kernel — and the
-//    one of rank i gets record id nrec + i and position bn[size] + (its rank
-//    within its size); then the records, bucket entries and hash entries are
-//    written.  A rank is a count of smaller keys, one warp per candidate
-//    (N^2 / 32 warp steps spread over the GPU: a few microseconds for the
-//    hundreds of joins a stop commits; no sort, no serial phase).
-
-// Sort key of a candidate: (size, first seven item ids), 16 bits per id, in
-// two words compared high word first; equal keys (size >= 8 sharing seven
-// ids) fall back to the masks, where the lexicographically smaller item list
-// is the one holding the lowest bit in which the two masks differ.
-struct CandKey {
-    unsigned long long hi, lo;
-    int32_t t;  // join index (tmp slot)
+// A join that passes walks cand's probe chain once: an existing record with
+// cand's mask -> already known, drop; a temporary entry (kTempFlag | join
+// index) with cand's mask -> another source produced the same candidate at
+// this stop, drop (all duplicates carry the same mask, so which join wins
+// does not matter); an empty slot -> allocate a join record, publish it
+// (fence) and CAS the slot: the winner owns the candidate.  No record is
+// published before the commit, so a non-temporary entry always names a record
+// of an earlier stop, and a subset lookup that meets a temporary entry just
+// keeps probing (a fresh candidate is no box: the join fails either way, as
+// in the reference, where it is a DASHED_CIRCLE).  The all-or-nothing
+// capacity check follows the phase; if it fails the host rebuilds the index
+// from the records (dropping the temporary entries) and replays.
+struct JoinRec {
+    unsigned long long hi, lo;  // sort key (size, first seven ids, 16 bits each); hi == ~0: duplicate, no candidate
+    uint64_t hash;
+    int64_t slot;  // hash slot the owner claimed
+    int32_t src;   // source record: the candidate is src's itemset + {l}
+    uint16_t l, size;
 };
+
+__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ bool views_same(const MaskView& x, const MaskView& y, int W) {
+    unsigned long long d = 0;
+    for (int w = 0; w < W; ++w) d |= x.word(w) ^ y.word(w);  // no early exit: the loads go out together
+    return d == 0;
+}
 
 __device__ __forceinline__ void key_take(int w, unsigned long long x, int& j, unsigned long long& hi,
                                          unsigned long long& lo) {
@@ -610,107 +612,309 @@ __device__ __forceinline__ void key_take(int w, unsigned long long x, int& j, un
     }
 }
 
-__device__ __forceinline__ CandKey cand_key(const unsigned long long* __restrict__ mk, int sz, int W, int32_t t) {
-    CandKey k;
-    k.t = t;
-    unsigned long long hi = (unsigned long long)(uint32_t)sz << 48, lo = 0;
-    int j = 0;
-    if (W <= 16) {
-        // every word loaded before the first use (a loop with an early exit
-        // would chain W dependent L2 latencies)
-        unsigned long long v[16];
-#pragma unroll
-        for (int w = 0; w < 16; ++w) v[w] = w < W ? mk[w] : 0ull;
-#pragma unroll
-        for (int w = 0; w < 16; ++w) key_take(w, v[w], j, hi, lo);
-    } else {
-        for (int w = 0; w < W && j < 7; ++w) key_take(w, mk[w], j, hi, lo);
+// Claim cand = src + {l} (hash hc, sz items, sort key (hi, lo)) in the index,
+// or find it there.  Temporary entries of this stop's other joins are compared
+// by mask (both are views of records of earlier stops).
+__device__ __noinline__ void claim_join(const CkptArgs& a, int32_t src, int l, uint64_t hc, int sz,
+                                        unsigned long long hi, unsigned long long lo, const int* its, int k) {
+    unsigned long long* stat = a.stat;
+    const Records& R = a.R;
+    const int W = a.W;
+    const uint32_t tag = (uint32_t)(hc >> 32);
+    const MaskView cand{R.mask + (int64_t)src * W, l, -1};
+    uint64_t slot = mix64(hc) & a.hmask;
+    int64_t t = -1;
+    hent_t x = ldv(a.ht + slot);
+    while (true) {
+        if (x == kEmptyEnt) {
+            if (t < 0) {
+                t = (int64_t)atomicAdd(&stat[S_NADM], 1ull);
+                atomicAdd(&stat[S_HEAD + a.KS + sz], 1ull);  // adm[sz]
+                if (t >= a.tmp_cap) return;                  // the capacity check will see NADM
+                JoinRec* j = a.joins + t;
+                j->hi = hi;
+                j->lo = lo;
+                j->hash = hc;
+                j->src = src;
+                j->l = (uint16_t)l;
+                j->size = (uint16_t)sz;
+                __threadfence();  // the record before the entry that names it
+            }
+            x = atomicCAS(a.ht + slot, kEmptyEnt, hent(hc, kTempFlag | (int32_t)t));
+            if (x == kEmptyEnt) {  // owner
+                a.joins[t].slot = (int64_t)slot;
+                atomicAdd(&stat[S_NINS], 1ull);
+                atomicAdd(&a.ins_k[sz], 1ull);
+                return;
+            }
+            // another thread took the slot first: examine its entry
+        }
+        if (hent_tag(x) == tag) {
+            const int32_t e = hent_id(x);
+            bool same;
+            if (e & kTempFlag) {
+                const JoinRec* o = a.joins + (e & ~kTempFlag);
+                // (L2 loads: the record was published by another SM during this phase)
+                const uint64_t oh = ldv(reinterpret_cast<const unsigned long long*>(&o->hash));
+                const unsigned long long ow = ldv(reinterpret_cast<const unsigned long long*>(&o->src));
+                same = oh == hc && (int)((ow >> 48) & 0xFFFFu) == sz &&
+                       views_same(MaskView{R.mask + (int64_t)(int32_t)(uint32_t)ow * W, (int)((ow >> 32) & 0xFFFFu), -1},
+                                  cand, W);
+            } else if (its) {
+                // a record of the same size holding every item of cand IS cand
+                same = R.size[e] == sz;
+                if (same) {
+                    const unsigned long long* rm = R.mask + (int64_t)e * W;
+                    bool ok = ((rm[l >> 6] >> (l & 63)) & 1ull) != 0;
+                    for (int q = 0; q < k; ++q) ok &= ((rm[its[q] >> 6] >> (its[q] & 63)) & 1ull) != 0;
+                    same = ok;
+                }
+            } else {
+                same = mask_eq(R.mask + (int64_t)e * W, cand, W);
+            }
+            if (same) {
+                if (t >= 0) a.joins[t].hi = ~0ull;  // the join slot stays unused
+                return;
+            }
+        }
+        slot = (slot + 1) & a.hmask;
+        x = ldv(a.ht + slot);
     }
-    k.hi = hi;
-    k.lo = lo;
-    return k;
 }
 
-__device__ __forceinline__ bool cand_less(const CandKey& a, const CandKey& b,
-                                          const unsigned long long* __restrict__ tmp_mask, int W) {
-    if (a.hi != b.hi) return a.hi < b.hi;
-    if (a.lo != b.lo) return a.lo < b.lo;
-    if (a.t == b.t) return false;
-    const unsigned long long* x = tmp_mask + (int64_t)a.t * W;
-    const unsigned long long* y = tmp_mask + (int64_t)b.t * W;
-    for (int w = 0; w < W; ++w) {
-        const unsigned long long d = x[w] ^ y[w];
-        if (d) return (x[w] & (d & (~d + 1))) != 0;
-    }
-    return false;  // equal masks: impossible after dedup
-}
-
-__global__ void dedup_kernel(int W, const unsigned long long* __restrict__ tmp_mask,
-                             const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
-                             const Records R, hent_t* ht, uint64_t hmask, unsigned long long* stat,
-                             int64_t* __restrict__ tmp_slot, CandKey* __restrict__ keys,
-                             unsigned long long* __restrict__ ins_k) {
-    if (stat[S_ABORT] || stat[S_NFRONT] == 0) return;
-    const int64_t na = (int64_t)stat[S_NADM];
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t h = tmp_hash[t];
-        const unsigned long long* mk = tmp_mask + t * W;
-        uint64_t slot = mix64(h) & hmask;
-        while (true) {
-            const hent_t pe = atomicCAS(ht + slot, kEmptyEnt, hent(h, kTempFlag | (int32_t)t));
-            if (pe == kEmptyEnt) {
-                tmp_slot[t] = (int64_t)slot;
-                const int sz = tmp_size[t];
-                keys[atomicAdd(&stat[S_NINS], 1ull)] = cand_key(mk, sz, W, (int32_t)t);
-                atomicAdd(&ins_k[sz], 1ull);
-                break;
+__device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, int cta, int nctas) {
+    const Records& R = a.R;
+    const int W = a.W;
+    const int64_t L = a.pa.L;
+    const hent_t* ht = a.ht;
+    const uint64_t hmask = a.hmask;
+    const int32_t* prank = a.pa.rank;
+    const int64_t prec0 = a.pa.rec0;
+    const int64_t total = nfront * L;
+    for (int64_t t = (int64_t)cta * blockDim.x + threadIdx.x; t < total; t += (int64_t)nctas * blockDim.x) {
+        const int64_t f = t / L, j = t - f * L;
+        const int32_t src = a.frontier[f];
+        const int l = a.level1[j];
+        const int ks = R.size[src];
+        if (ks <= 7) {
+            // item-list path: src's ascending ids in one 16-byte load
+            const uint4 iv = *reinterpret_cast<const uint4*>(R.items + (int64_t)src * 8);
+            int its[8] = {(int)(iv.x & 0xFFFFu), (int)(iv.x >> 16), (int)(iv.y & 0xFFFFu), (int)(iv.y >> 16),
+                          (int)(iv.z & 0xFFFFu), (int)(iv.z >> 16), (int)(iv.w & 0xFFFFu), (int)(iv.w >> 16)};
+            bool in = false;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) in |= q < ks && its[q] == l;
+            if (in) continue;  // cand == base
+            bool ok = true;
+            if (ks == 2 && prank) {
+                // a pair source (the pair wave's joins): its immediate subsets
+                // {a, l} and {b, l} are seeded pairs of frequent items, whose
+                // record ids follow from the items' level1 ranks (record
+                // prec0 + triangle slot, seed_pairs_kernel): one load each
+                // instead of a hash probe chain.  l = level1[j] has rank j.
+                const int64_t ra = prank[its[0]], rb = prank[its[1]];
+                const int64_t pa = ra < j ? tri_pos(ra, j, L) : tri_pos(j, ra, L);
+                const int64_t pb = rb < j ? tri_pos(rb, j, L) : tri_pos(j, rb, L);
+                const uint8_t sb = R.shape[prec0 + pb], sa = R.shape[prec0 + pa];  // (both loads at once)
+                ok = is_box(sb) & is_box(sa);
             }
-            const int32_t prev = hent_id(pe);
-            bool same = hent_tag(pe) == (uint32_t)(h >> 32);
-            if (same && (prev & kTempFlag)) {
-                const int64_t o = prev & ~kTempFlag;
-                same = tmp_hash[o] == h;
-                for (int w = 0; same && w < W; ++w) same = tmp_mask[o * W + w] == mk[w];
-            } else if (same) {
-                for (int w = 0; same && w < W; ++w) same = R.mask[(int64_t)prev * W + w] == mk[w];
+            if (!ok) continue;
+            const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
+            if (!(ks == 2 && prank)) {
+                for (int q = 0; q < ks && ok; ++q) {
+                    const int d = its[q];
+                    const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, ks, l, d, ks);
+                    ok = e >= 0 && is_box(R.shape[e]);
+                }
+                if (!ok) continue;
             }
-            if (same) break;  // duplicate of a join owned by another thread
-            slot = (slot + 1) & hmask;
+            // sort key from the merged ascending list
+            int p = 0;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) p += (q < ks && its[q] < l) ? 1 : 0;
+            unsigned long long hi = (unsigned long long)(uint32_t)(ks + 1) << 48, lo = 0;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) {
+                if (q <= ks) {
+                    const unsigned long long it = (unsigned long long)(q < p ? its[q] : (q == p ? l : its[q > 0 ? q - 1 : 0]));
+                    if (q < 3) hi |= it << (32 - 16 * q);
+                    else lo |= it << (48 - 16 * (q - 3));
+                }
+            }
+            claim_join(a, src, l, hc, ks + 1, hi, lo, its, ks);
+        } else {
+            // large itemsets: masks all the way
+            const unsigned long long* sm = R.mask + (int64_t)src * W;
+            if ((sm[l >> 6] >> (l & 63)) & 1ull) continue;  // cand == base
+            const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
+            const MaskView cand{sm, l, -1};
+            bool ok = true;
+            for (int w = 0; w < W && ok; ++w) {
+                unsigned long long x = cand.word(w);
+                while (x) {
+                    const int bit = w * 64 + __ffsll((long long)x) - 1;
+                    x &= x - 1;
+                    if (bit == l) continue;
+                    const MaskView sub{sm, l, bit};
+                    const int32_t e = ht_lookup(ht, hmask, R, W, hc ^ zob((uint32_t)bit), sub);
+                    if (e < 0 || !is_box(R.shape[e])) {
+                        ok = false;
+                        break;
+                    }
+                }
+            }
+            if (!ok) continue;
+            unsigned long long hi = (unsigned long long)(uint32_t)(ks + 1) << 48, lo = 0;
+            int q = 0;
+            for (int w = 0; w < W && q < 7; ++w) key_take(w, cand.word(w), q, hi, lo);
+            claim_join(a, src, l, hc, ks + 1, hi, lo, nullptr, 0);
         }
     }
 }
 
-// Commit the candidate of rank `rank` (0-based over the stop's new candidates
-// in canonical order): record nrec0 + rank at bucket slot bn0[sz] + rank -
-// start[sz], then publish its record id in the hash slot it claimed.
-__device__ __noinline__ void commit_rank(int W, int64_t rank, int32_t t, const unsigned long long* __restrict__ tmp_mask,
-                                         const uint64_t* __restrict__ tmp_hash, const int32_t* __restrict__ tmp_size,
-                                         const int64_t* __restrict__ tmp_slot, Records R, hent_t* ht, int64_t nrec0,
-                                         const int64_t* start, const int64_t* bn0,
-                                         int32_t* const* __restrict__ b_rec_tab,
-                                         uint16_t* const* __restrict__ b_items_tab) {
-    const int64_t r = nrec0 + rank;
-    const int sz = tmp_size[t];
-    const uint64_t h = tmp_hash[t];
-    const unsigned long long* mk = tmp_mask + (int64_t)t * W;
-    R.hash[r] = h;
-    R.size[r] = sz;
-    R.support[r] = 0;
-    R.intervals[r] = 0;
-    R.shape[r] = DASHED_CIRCLE;
-    const int64_t pos = bn0[sz] + (rank - start[sz]);
-    b_rec_tab[sz][pos] = (int32_t)r;
-    uint16_t* it = b_items_tab[sz] + pos * sz;
-    int j = 0;
-    for (int w = 0; w < W; ++w) {
-        unsigned long long x = mk[w];
-        R.mask[r * W + w] = x;
-        while (x) {
-            it[j++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
-            x &= x - 1;
+// All-or-nothing capacity check of the candidate step: the joins, the records
+// and hash load after them, every bucket's room.  Every CTA evaluates it on
+// the same (stable) inputs; CTA 0 records the verdict.  An overflow also
+// raises the abort flag so every later stop is skipped until the host's replay.
+__device__ __forceinline__ bool capacity_over(const CkptArgs& a, CkptSmem& sm) {
+    unsigned long long* stat = a.stat;
+    const int KS = a.KS;
+    if (threadIdx.x == 0) {
+        const unsigned long long na = ldv(stat + S_NADM), nr = ldv(stat + S_NREC);
+        sm.flag = (int64_t)na > a.tmp_cap || (int64_t)(nr + na) > a.rec_cap || (int64_t)(nr + na) * 2 > a.hcap;
+    }
+    __syncthreads();
+    const unsigned long long* adm = stat + S_HEAD + KS;
+    const unsigned long long* bn = stat + S_HEAD + 2 * KS;
+    // a stop's joins are one item larger than a live itemset, i.e. <= kuse items
+    const int lim = min(KS, a.kuse + 1);
+    for (int k = threadIdx.x; k < lim; k += blockDim.x) {
+        const unsigned long long ak = ldv(adm + k);
+        if (ak && (int64_t)(ldv(bn + k) + ak) > a.bcap[k]) sm.flag = 1;
+    }
+    __syncthreads();
+    const bool over = sm.flag != 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        stat[S_OVERFLOW] = over ? 1ull : 0ull;
+        if (over) stat[S_ABORT] = 1ull;
+    }
+    return over;
+}
+
+// P3.  Candidate commit with a CANONICAL result: the record ids and bucket
+// positions of a stop's new candidates depend only on the SET of candidates,
+// never on thread timing.  Sharded engines reduce their counts slot by slot,
+// so every rank must lay its buckets out identically (the reference reduces
+// per record, engine.py:268-270); with atomics deciding the order, ranks
+// would add up counts of different itemsets.
+//
+// The owning joins are ranked by (size, item ids ascending) — the order of
+// make_candidates' lexicographic joins, which also makes candidates sharing a
+// prefix contiguous for the count kernel — and the one of rank i gets record
+// id nrec + i and position bn[size] + (its rank within its size); then the
+// record, bucket entry and hash entry are written by its warp.  A rank is a
+// count of smaller keys, one warp per candidate (N^2 / 32 warp steps spread
+// over the GPU: a few microseconds for the hundreds of joins a stop commits;
+// no sort, no serial phase).  Equal keys (size >= 8 sharing seven ids) fall
+// back to the masks, where the lexicographically smaller item list is the one
+// holding the lowest bit in which the two masks differ.
+__device__ __noinline__ bool join_less_slow(const CkptArgs& a, const JoinRec& x, const JoinRec& y) {
+    const MaskView vx{a.R.mask + (int64_t)x.src * a.W, (int)x.l, -1};
+    const MaskView vy{a.R.mask + (int64_t)y.src * a.W, (int)y.l, -1};
+    for (int w = 0; w < a.W; ++w) {
+        const unsigned long long xw = vx.word(w), d = xw ^ vy.word(w);
+        if (d) return (xw & (d & (~d + 1))) != 0;
+    }
+    return false;  // equal masks: impossible among owners
+}
+
+__device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, int64_t na, int cta, int nctas) {
+    unsigned long long* stat = a.stat;
+    const Records& R = a.R;
+    const int W = a.W;
+    unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
+    const int top = a.kuse < kDoffMax ? a.kuse : kDoffMax;  // sizes that can hold candidates
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t* start = sm.doff;
+    // start[k] = new candidates of sizes < k: warp 0 scans 32 sizes per step
+    if (wid == 0) {
+        int64_t carry = 0;
+        for (int k0 = 0; k0 < top; k0 += 32) {
+            const int k = k0 + lane;
+            const int64_t v = k < top ? (int64_t)ldv(a.ins_k + k) : 0;
+            int64_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (k < top) {
+                start[k] = carry + x - v;
+                sm.bn0[k] = (int64_t)ldv(bn + k);
+            }
+            carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+        }
+        if (lane == 0) sm.nrec0 = (int64_t)ldv(stat + S_NREC);
+    }
+    __syncthreads();
+    // one warp per join: an owner's rank is the number of owners with smaller keys
+    constexpr int kWarps = kCkptThreads / 32;
+    const int64_t warps = (int64_t)nctas * kWarps;
+    // consecutive joins go to different CTAs (every SM takes part even when
+    // the stop commits only a few)
+    for (int64_t e = (int64_t)wid * nctas + cta; e < na; e += warps) {
+        const JoinRec je = a.joins[e];
+        if (je.hi == ~0ull) continue;  // duplicate
+        unsigned cnt = 0;
+        for (int64_t j = lane; j < na; j += 32) {
+            const unsigned long long hj = a.joins[j].hi, lj = a.joins[j].lo;
+            bool less = hj != je.hi ? hj < je.hi : lj < je.lo;  // (~0 is never smaller)
+            if (hj == je.hi && lj == je.lo && j != e) less = join_less_slow(a, a.joins[j], je);
+            cnt += less ? 1u : 0u;
+        }
+        cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+        // record nrec0 + rank at bucket slot bn0[sz] + rank - start[sz]; its
+        // record id replaces the temporary entry in the hash slot it claimed
+        const int sz = je.size;
+        const int64_t r = sm.nrec0 + cnt;
+        const int64_t pos = sm.bn0[sz] + ((int64_t)cnt - start[sz]);
+        const unsigned long long* smk = R.mask + (int64_t)je.src * W;
+        for (int w = lane; w < W; w += 32) {
+            unsigned long long x = smk[w];
+            if (w == (je.l >> 6)) x |= 1ull << (je.l & 63);
+            R.mask[r * W + w] = x;
+        }
+        uint16_t* bit = a.items_tab[sz] + pos * sz;
+        if (sz <= 8) {
+            // the ascending ids: src's list with l merged in; lane q holds item q
+            const uint16_t* si = R.items + (int64_t)je.src * 8;
+            const int mine = lane < sz - 1 ? (int)si[lane] : 0x10000;
+            const int p = __popc(__ballot_sync(0xFFFFFFFFu, mine < (int)je.l));
+            const int up = __shfl_up_sync(0xFFFFFFFFu, mine, 1);
+            const int it = lane < p ? mine : (lane == p ? (int)je.l : up);
+            if (lane < sz) bit[lane] = (uint16_t)it;
+            if (lane < 8) R.items[r * 8 + lane] = lane < sz ? (uint16_t)it : (uint16_t)0;
+        } else if (lane == 0) {
+            int q = 0;
+            for (int w = 0; w < W; ++w) {
+                unsigned long long x = smk[w];
+                if (w == (je.l >> 6)) x |= 1ull << (je.l & 63);
+                while (x) {
+                    bit[q++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
+                    x &= x - 1;
+                }
+            }
+        }
+        if (lane == 0) {
+            R.hash[r] = je.hash;
+            R.size[r] = sz;
+            R.support[r] = 0;
+            R.intervals[r] = 0;
+            R.shape[r] = DASHED_CIRCLE;
+            a.rec_tab[sz][pos] = (int32_t)r;
+            a.ht[je.slot] = hent(je.hash, (int32_t)r);
         }
     }
-    ht[tmp_slot[t]] = hent(h, (int32_t)r);
 }
 
 // The stop's status into its (host-mapped, pinned) ring slot S_SEQ % kRing:
@@ -722,7 +926,7 @@ __device__ __noinline__ void commit_rank(int W, int64_t rank, int32_t t, const u
 // ring == nullptr: reset only (engine seeding).
 __device__ void status_body(unsigned long long* __restrict__ stat, int KS, int kuse,
                             unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
-    __shared__ int64_t sh[kDoffMax];
+    __shared__ int64_t sh[1];
     if (ring) {
         unsigned long long* slot = ring + (int64_t)(stat[S_SEQ] % kRing) * ring_words;
         for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
@@ -778,100 +982,134 @@ __global__ void status_kernel(unsigned long long* __restrict__ stat, int KS, int
     status_body(stat, KS, kuse, ring, ring_words, doff);
 }
 
-#ifdef DIC_LAB_TIMING
-// lab build: per-stop phase stamps of commit_status (globaltimer ns), slot S_SEQ % 512
-__device__ unsigned long long g_lab_commit[512][8];
-#define COMMIT_STAMP(i)                                                                      \
-    do {                                                                                     \
-        if (threadIdx.x == 0) {                                                              \
-            unsigned long long _t;                                                           \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
-            g_lab_commit[stat[S_SEQ] % 512][i] = _t;                                         \
-        }                                                                                    \
-    } while (0)
-#else
-#define COMMIT_STAMP(i) \
-    do {                \
-    } while (0)
-#endif
+// Stops with few live slots (the long tail of a run: tens to a few thousand
+// dashed itemsets) are run by CTA 0 alone, with CTA-level barriers: a
+// grid-wide barrier costs ~1.5 us, more than such a phase's whole work.  The
+// other CTAs wait for CTA 0's verdict after the apply — "done without you"
+// or, when the stop promoted enough itemsets for the joins to need the grid,
+// "join in" — published as a word tagged with the stop's sequence number.
+constexpr int64_t kSmallSlots = 2048;  // <= 2 slots per thread of one CTA
+constexpr int64_t kSoloJoins = 2048;   // <= 2 joins per thread of one CTA
 
-// The stop's canonical commit, then its status.  ins_k[0, kDoffMax): new
-// candidates by size (dedup); ins_k[kDoffMax]: CTAs done (the last CTA out
-// finalises the sizes and writes the status).
-constexpr int kCommitThreads = 256;
-__global__ void __launch_bounds__(kCommitThreads) rank_commit_status_kernel(
-    int W, const unsigned long long* __restrict__ tmp_mask, const uint64_t* __restrict__ tmp_hash,
-    const int32_t* __restrict__ tmp_size, const int64_t* __restrict__ tmp_slot, const CandKey* __restrict__ keys,
-    Records R, hent_t* ht, unsigned long long* stat, int KS, int kuse, unsigned long long* ins_k,
-    int32_t* const* __restrict__ b_rec_tab, uint16_t* const* __restrict__ b_items_tab,
-    unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
-    __shared__ int64_t start[kDoffMax], bn0[kDoffMax];
-    __shared__ int64_t nrec0;
-    __shared__ int last;
-    COMMIT_STAMP(0);
-    const int64_t N = (stat[S_ABORT] || stat[S_NFRONT] == 0) ? 0 : (int64_t)stat[S_NINS];
-    if (N == 0) {
-        if (blockIdx.x == 0) status_body(stat, KS, kuse, ring, ring_words, doff);
+__global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __grid_constant__ CkptArgs a) {
+    __shared__ CkptSmem sm;
+    unsigned long long* stat = a.stat;
+    // a stop skipped by the overflow recovery: only its (unchanged) status
+    if (stat[S_ABORT]) {
+        if (blockIdx.x == 0) status_body(stat, a.KS, a.kuse, a.ring, a.ring_words, a.doff);
         return;
     }
-    unsigned long long* bn = stat + S_HEAD + 2 * KS;
-    const int top = kuse < kDoffMax ? kuse : kDoffMax;  // sizes that can hold candidates
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // start[k] = new candidates of sizes < k: warp 0 scans 32 sizes per step
-    if (wid == 0) {
-        int64_t carry = 0;
-        for (int k0 = 0; k0 < top; k0 += 32) {
-            const int k = k0 + lane;
-            const int64_t v = k < top ? (int64_t)ins_k[k] : 0;
-            int64_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (k < top) {
-                start[k] = carry + x - v;
-                bn0[k] = (int64_t)bn[k];
-            }
-            carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+    const unsigned long long G = gridDim.x;
+    const unsigned long long tag = (stat[S_SEQ] + 1) << 2;
+    unsigned long long nbar = 0;
+    const bool small = !a.replay && G > 1 && a.doff[a.kuse_issue] <= kSmallSlots;
+    bool solo = false;
+    CKPT_STAMP(0);
+    if (!a.replay) {
+        if (!small) {
+            apply_phase(a, sm, blockIdx.x, gridDim.x);
+            grid_barrier(a.sync, G * ++nbar);
+        } else if (blockIdx.x == 0) {
+            apply_phase(a, sm, 0, 1);
+            __syncthreads();
         }
-        if (lane == 0) nrec0 = (int64_t)stat[S_NREC];
     }
-    __syncthreads();
-    COMMIT_STAMP(1);
-    // one warp per candidate: its rank is the number of smaller keys
-    const int64_t warps = (int64_t)gridDim.x * (kCommitThreads / 32);
-    for (int64_t e = (int64_t)blockIdx.x * (kCommitThreads / 32) + wid; e < N; e += warps) {
-        const CandKey ke = keys[e];
-        unsigned cnt = 0;
-        for (int64_t j = lane; j < N; j += 32) cnt += cand_less(keys[j], ke, tmp_mask, W) ? 1u : 0u;
-        cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-        if (lane == 0)
-            commit_rank(W, (int64_t)cnt, ke.t, tmp_mask, tmp_hash, tmp_size, tmp_slot, R, ht, nrec0, start, bn0,
-                        b_rec_tab, b_items_tab);
+    CKPT_STAMP(1);
+    if (small) {
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) {
+                sm.flag = (int64_t)ldv(stat + S_NFRONT) * a.pa.L <= kSoloJoins;
+                // release: the apply's writes before the verdict
+                const unsigned long long v = tag | (sm.flag ? 1ull : 2ull);
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sync + 2), "l"(v) : "memory");
+            }
+            __syncthreads();
+            solo = sm.flag != 0;
+        } else {
+            if (threadIdx.x == 0) {
+                unsigned long long v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.sync + 2) : "memory");
+                } while ((v & ~3ull) != tag);
+                sm.flag = (v & 3ull) == 1ull;
+            }
+            __syncthreads();
+            if (sm.flag) return;  // CTA 0 finishes the stop alone
+        }
     }
-    COMMIT_STAMP(2);
+    const int cta = solo ? 0 : (int)blockIdx.x, nctas = solo ? 1 : (int)gridDim.x;
+    const int64_t nfront = (int64_t)ldv(stat + S_NFRONT);
+    if (!a.replay) {
+        const unsigned long long* cflag = stat + S_HEAD + 3 * a.KS;
+        const int kc = min(a.kuse_issue, a.KS);
+        if (solo) {
+            // every flag loaded at once (a loop of dependent-latency loads otherwise)
+            if (threadIdx.x < kc) sm.pos[threadIdx.x] = cflag[threadIdx.x] != 0;
+            __syncthreads();
+            for (int k = 1; k < kc; ++k)
+                if (sm.pos[k]) compact_bucket(a, sm, k);
+        } else {
+            for (int k = 1 + cta; k < kc; k += nctas)
+                if (cflag[k]) compact_bucket(a, sm, k);
+        }
+    }
+    int64_t N = 0;
+    if (nfront > 0) {
+        eval_phase(a, nfront, cta, nctas);
+        CKPT_STAMP(7);
+        if (solo) {
+            __syncthreads();
+        } else {
+            grid_barrier(a.sync, G * ++nbar);
+        }
+        CKPT_STAMP(2);
+        if (!capacity_over(a, sm)) {
+            N = (int64_t)ldv(stat + S_NINS);
+            if (N > 0) commit_phase(a, sm, (int64_t)ldv(stat + S_NADM), cta, nctas);
+        }
+    }
+    CKPT_STAMP(3);
     // the last CTA out: sizes after the commit, then the stop's status
     __syncthreads();
+    if (!solo) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            sm.flag = atomicAdd(&a.sync[1], 1ull) == G - 1;
+        }
+        __syncthreads();
+        if (!sm.flag) return;
+        if (threadIdx.x == 0) __threadfence();
+        __syncthreads();
+    }
+    if (N > 0) {
+        unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
+        const int top = a.kuse < kDoffMax ? a.kuse : kDoffMax;
+        for (int k = threadIdx.x; k < top; k += blockDim.x) {
+            const unsigned long long n = ldv(a.ins_k + k);
+            if (n) bn[k] = ldv(bn + k) + n;
+            a.ins_k[k] = 0;
+        }
+        if (threadIdx.x == 0) stat[S_NREC] = ldv(stat + S_NREC) + (unsigned long long)N;
+    }
     if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(&ins_k[kDoffMax], 1ull) == gridDim.x - 1;
+        a.sync[0] = 0;
+        a.sync[1] = 0;
+        __threadfence();  // also drops this SM's L1 copies of the status words (updated by atomics at L2)
     }
     __syncthreads();
-    if (!last) return;
-    __threadfence();
-    for (int k = threadIdx.x; k < top; k += blockDim.x) {
-        const unsigned long long a = *(volatile unsigned long long*)&ins_k[k];
-        if (a) bn[k] = (unsigned long long)(bn0[k] + (int64_t)a);
-        ins_k[k] = 0;
-    }
+    CKPT_STAMP(4);
+#ifdef DIC_LAB_TIMING
+    const unsigned long long lab_seq = stat[S_SEQ];
+#endif
+    status_body(stat, a.KS, a.kuse, a.ring, a.ring_words, a.doff);
+#ifdef DIC_LAB_TIMING
     if (threadIdx.x == 0) {
-        stat[S_NREC] = (unsigned long long)(nrec0 + N);
-        ins_k[kDoffMax] = 0;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_lab_commit[lab_seq % 512][5] = t;
+        g_lab_commit[lab_seq % 512][6] = (unsigned long long)(small ? (solo ? 2 : 1) : 0);
     }
-    __syncthreads();
-    COMMIT_STAMP(3);
-    status_body(stat, KS, kuse, ring, ring_words, doff);
+#endif
 }
 
 struct TableUpdate {
@@ -933,7 +1171,7 @@ struct GraphKey {
     const unsigned long long* delta_p;  // fused reduction: the count graph's target
     const int32_t* keep;
     const int32_t* frontier;
-    const unsigned long long* tmp_mask;
+    const void* joins;
     int64_t tmp_cap;
     int64_t kuse_status;
     const int64_t* sched;
@@ -980,6 +1218,7 @@ struct dic_engine {
     int64_t* d_bcap = nullptr;
     int64_t* d_doff = nullptr;     // [KS + 1] per-stop delta offsets
     unsigned long long* d_stat = nullptr;  // status words (see S_*)
+    unsigned long long* d_sync = nullptr;  // checkpoint kernel: grid-barrier arrivals, CTAs out
     int64_t slot_cap = 0;          // >= sum of bucket capacities: delta / keep / frontier size
 
     int32_t* level1 = nullptr;
@@ -988,11 +1227,7 @@ struct dic_engine {
     int32_t* keep = nullptr;
     unsigned long long* delta = nullptr;
 
-    unsigned long long* tmp_mask = nullptr;
-    uint64_t* tmp_hash = nullptr;
-    int32_t* tmp_size = nullptr;
-    int64_t* tmp_slot = nullptr;          // hash slot claimed by each owning join (dedup)
-    CandKey* tmp_keys = nullptr;          // sort keys of the owning joins (dedup -> rank_commit_status)
+    JoinRec* joins = nullptr;             // the stop's admitted joins (checkpoint kernel: eval -> commit)
     int64_t tmp_cap = 0;
     unsigned long long* ins_k = nullptr;  // [kDoffMax + 2] new candidates by size (dedup -> commit_status)
 
@@ -1159,7 +1394,19 @@ int grow_records(dic_engine* e, int64_t need_cap) {
     if ((rc = dgrow(&R.intervals, oc, nc, e->s))) return rc;
     if ((rc = dgrow(&R.size, oc, nc, e->s))) return rc;
     if ((rc = dgrow(&R.shape, oc, nc, e->s))) return rc;
+    if ((rc = dgrow(&R.items, oc * 8, nc * 8, e->s))) return rc;
     R.cap = nc;
+    return DIC_OK;
+}
+
+// the hash index rebuilt from the records (the device's count)
+int rebuild_hash(dic_engine* e) {
+    ht_clear_kernel<<<nblk(e->hcap), 256, 0, e->s>>>(e->ht, e->hcap);
+    ::dic::note_launch();
+    ht_insert_records_kernel<<<sm_count() * 8, 256, 0, e->s>>>(e->ht, (uint64_t)e->hcap - 1, e->R,
+                                                               e->d_stat + S_NREC);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("rehash");
     return DIC_OK;
 }
 
@@ -1173,12 +1420,7 @@ int ensure_hash(dic_engine* e, int64_t nrec_after) {
     int rc = dalloc(&e->ht, nc, e->s);
     if (rc) return rc;
     e->hcap = nc;
-    ht_clear_kernel<<<nblk(nc), 256, 0, e->s>>>(e->ht, nc);
-    ::dic::note_launch();
-    ht_insert_records_kernel<<<sm_count() * 8, 256, 0, e->s>>>(e->ht, (uint64_t)nc - 1, e->R, e->d_stat + S_NREC);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("rehash");
-    return DIC_OK;
+    return rebuild_hash(e);
 }
 
 // Push the bucket tables (record / item arrays, capacities) the device has
@@ -1344,16 +1586,9 @@ int grow_bucket(dic_engine* e, int k, int64_t need_cap, bool* changed) {
 int ensure_tmp(dic_engine* e, int64_t want) {
     if (want <= e->tmp_cap) return DIC_OK;
     const int64_t nc = std::max<int64_t>(want, e->tmp_cap * 2);
-    dfree(e->tmp_mask, e->s);
-    dfree(e->tmp_hash, e->s);
-    dfree(e->tmp_size, e->s);
-    dfree(e->tmp_slot, e->s);
-    dfree(e->tmp_keys, e->s);
+    dfree(e->joins, e->s);
     int rc;
-    if ((rc = dalloc(&e->tmp_mask, nc * e->W, e->s)) || (rc = dalloc(&e->tmp_hash, nc, e->s)) ||
-        (rc = dalloc(&e->tmp_size, nc, e->s)) || (rc = dalloc(&e->tmp_slot, nc, e->s)) ||
-        (rc = dalloc(&e->tmp_keys, nc, e->s)))
-        return rc;
+    if ((rc = dalloc(&e->joins, nc, e->s))) return rc;
     e->tmp_cap = nc;
     return DIC_OK;
 }
@@ -1384,50 +1619,67 @@ int ensure_headroom(dic_engine* e) {
     return DIC_OK;
 }
 
-// CTAs per SM of the join evaluation and dedup kernels (DIC_CAND_GRID; the
-// layout-determinism tests vary it: the committed layout must not change)
-static int cand_grid_per_sm() {
-    const char* env = getenv("DIC_CAND_GRID");
-    const int v = env && *env ? atoi(env) : 4;
-    return std::min(64, std::max(1, v));
+// CTAs of the checkpoint kernel: one per SM.  DIC_CKPT_CTAS overrides it (the
+// layout-determinism tests vary it: the work split and the timing of every
+// atomic change, the committed layout must not).
+static int ckpt_ctas() {
+    const char* env = getenv("DIC_CKPT_CTAS");
+    const int v = env && *env ? atoi(env) : 0;
+    return v > 0 ? std::min(v, sm_count()) : sm_count();
 }
 
-int candidate_step(dic_engine* e, cudaStream_t s) {
-    const int G = sm_count() * cand_grid_per_sm();
-    unsigned long long* st = e->d_stat;
-    eval_candidates_kernel<<<G, 256, 0, s>>>(e->frontier, e->level1, e->nL1, e->W, e->R, e->ht,
-                                                 (uint64_t)e->hcap - 1, e->tmp_mask, e->tmp_hash, e->tmp_size,
-                                                 e->tmp_cap, st, e->KS, e->R.cap, e->hcap, e->d_bcap, e->rank,
-                                                 (int64_t)e->m);
+// The checkpoint half of a stop as one cooperative launch (every CTA is
+// resident, so the grid-wide barriers cannot deadlock): apply + prune +
+// finalize over every slot, compaction of the flagged buckets,
+// make_candidates (device-sized, all-or-nothing), status.  replay: the
+// candidate step alone (overflow recovery).
+int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
+    CkptArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rec_tab = e->d_brec;
+    a.items_tab = e->d_bitems;
+    a.bcap = e->d_bcap;
+    a.doff = e->d_doff;
+    a.delta = e->delta;
+    a.R = e->R;
+    a.need = e->need;
+    a.interval = e->interval;
+    a.stop_max = e->stop_max;
+    a.frontier = e->frontier;
+    a.keep = e->keep;
+    a.stat = e->d_stat;
+    a.pa = PairArgs{e->tri, e->rank, e->nL1, e->tri ? e->tri_len : 0, (int64_t)e->m};
+    a.level1 = e->level1;
+    a.ht = e->ht;
+    a.hmask = (uint64_t)e->hcap - 1;
+    a.joins = e->joins;
+    a.tmp_cap = e->tmp_cap;
+    a.rec_cap = e->R.cap;
+    a.hcap = e->hcap;
+    a.ins_k = e->ins_k;
+    a.ring = e->ring_dev;
+    a.ring_words = e->ring_words;
+    a.sync = e->d_sync;
+    a.W = e->W;
+    a.KS = e->KS;
+    a.kuse_issue = replay ? e->kuse : e->kuse_issue;
+    a.kuse = e->kuse;
+    a.bound = e->bound;
+    a.replay = replay ? 1 : 0;
+    void* params[] = {&a};
+    static const bool coop = [] {
+        const char* env = getenv("DIC_CKPT_COOP");
+        return !(env && atoi(env) == 0);
+    }();
+    if (coop) {
+        DIC_CUDA(cudaLaunchCooperativeKernel((const void*)checkpoint_kernel, dim3((unsigned)ckpt_ctas()),
+                                             dim3(kCkptThreads), params, 0, s));
+    } else {
+        checkpoint_kernel<<<ckpt_ctas(), kCkptThreads, 0, s>>>(a);
+        DIC_CHECK_LAUNCH("checkpoint_kernel");
+    }
     ::dic::note_launch();
-    dedup_kernel<<<G, 256, 0, s>>>(e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->R, e->ht, (uint64_t)e->hcap - 1, st,
-                                   e->tmp_slot, e->tmp_keys, e->ins_k);
-    ::dic::note_launch();
-    // the canonical commit (one warp per new candidate) and the stop's status
-    rank_commit_status_kernel<<<sm_count(), kCommitThreads, 0, s>>>(
-        e->W, e->tmp_mask, e->tmp_hash, e->tmp_size, e->tmp_slot, e->tmp_keys, e->R, e->ht, st, e->KS, e->kuse,
-        e->ins_k, e->d_brec, e->d_bitems, e->ring_dev, e->ring_words, e->d_doff);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("candidate_step");
     return DIC_OK;
-}
-
-
-// the checkpoint half of a stop: apply + prune + finalize over every slot,
-// compaction of the flagged buckets, make_candidates (device-sized,
-// all-or-nothing), status
-int launch_checkpoint(dic_engine* e, cudaStream_t s) {
-    PairArgs pa{e->tri, e->rank, e->d_bitems, e->nL1, e->tri ? e->tri_len : 0, e->m};
-    apply_prune_finalize_kernel<<<sm_count() * 8, 256, 0, s>>>(
-        e->d_brec, e->d_doff, e->kuse_issue, e->delta, e->R, e->need, e->interval, e->stop_max, e->bound, e->frontier,
-        e->keep, e->d_stat, pa, e->KS);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("apply_prune_finalize_kernel");
-    compact_flagged_kernel<<<(unsigned)std::min(e->kuse_issue, e->KS), kCompactThreads, 0, s>>>(
-        e->d_brec, e->d_bitems, e->d_doff, e->keep, e->d_stat, e->KS);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("compact_flagged_kernel");
-    return candidate_step(e, s);  // eval, dedup, commit + status
 }
 
 // Fused reduction of a stop's counts over NVLink peer memory (SURVEY 8(f)
@@ -1540,7 +1792,7 @@ GraphKey graph_key(const dic_engine* e, bool with_sched) {
     k.pair_live = e->tri && e->tri_live;
     k.keep = e->keep;
     k.frontier = e->frontier;
-    k.tmp_mask = e->tmp_mask;
+    k.joins = e->joins;
     k.tmp_cap = e->tmp_cap;
     k.kuse_status = e->kuse;
     if (with_sched) {
@@ -1636,7 +1888,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
         (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s)) ||
-        (rc = dalloc(&e->ins_k, kDoffMax + 2, e->s))) {
+        (rc = dalloc(&e->ins_k, kDoffMax + 2, e->s)) || (rc = dalloc(&e->d_sync, 4, e->s))) {
         delete e;
         return rc;
     }
@@ -1655,6 +1907,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->ins_k, 0, (kDoffMax + 2) * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->d_sync, 0, 4 * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
     cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
     cudaMemsetAsync(e->d_bcap, 0, KS * sizeof(int64_t), e->s);
@@ -1668,15 +1921,14 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     cudaStreamSynchronize(s);
     Records& R = e->R;
     dfree(R.mask, s); dfree(R.hash, s); dfree(R.support, s); dfree(R.intervals, s); dfree(R.size, s);
-    dfree(R.shape, s);
+    dfree(R.shape, s); dfree(R.items, s);
     dfree(e->ht, s);
     for (Bucket& b : e->buckets) { dfree(b.rec, s); dfree(b.items, s); }
     dfree(e->d_brec, s); dfree(e->d_bitems, s); dfree(e->d_bcap, s); dfree(e->d_doff, s); dfree(e->d_stat, s);
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s);
     if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
-    dfree(e->tmp_mask, s); dfree(e->tmp_hash, s); dfree(e->tmp_size, s); dfree(e->tmp_slot, s);
-    dfree(e->tmp_keys, s); dfree(e->ins_k, s);
+    dfree(e->joins, s); dfree(e->ins_k, s); dfree(e->d_sync, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
     if (!e->fused) dfree(e->tri, s);
     if (e->fused) {
@@ -2074,7 +2326,13 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         e->nrec = (int64_t)h[S_NREC];
         if ((rc = ensure_tmp(e, na))) return rc;
         if ((rc = grow_records(e, e->nrec + na))) return rc;
-        if ((rc = ensure_hash(e, e->nrec + na))) return rc;
+        // the aborted candidate step left its joins' temporary entries in the
+        // index: rebuild it from the records (none of that stop was committed)
+        {
+            const int64_t hc0 = e->hcap;
+            if ((rc = ensure_hash(e, e->nrec + na))) return rc;
+            if (e->hcap == hc0 && (rc = rebuild_hash(e))) return rc;
+        }
         bool changed = false;
         for (int k = 0; k < KS; ++k) {
             if (!adm[k]) continue;
@@ -2087,7 +2345,8 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_ABORT, 0, u, e->s));
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
-        if ((rc = candidate_step(e, e->s))) return rc;  // ends with the stop's status
+        DIC_CUDA(cudaMemsetAsync(e->ins_k, 0, kDoffMax * u, e->s));
+        if ((rc = launch_checkpoint(e, e->s, true))) return rc;  // ends with the stop's status
         e->kuse_at[slot] = e->kuse;
         DIC_CUDA(cudaStreamSynchronize(e->s));
         ku = e->kuse_at[slot];

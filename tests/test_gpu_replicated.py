@@ -4,10 +4,10 @@ A sharded run reduces every stop's counts SLOT BY SLOT across ranks
 (DESIGN.md §9), so every rank must give the same itemset the same bucket
 slot.  Two properties are checked on one GPU:
 
-1. Layout determinism: the same run with different grid sizes for the join
-   evaluation / dedup kernels (DIC_CAND_GRID) — i.e. different thread timing
-   in every atomic — leaves byte-identical buckets (record ids and item lists)
-   after every stop.
+1. Layout determinism: the same run with different grid sizes for the
+   checkpoint kernel (DIC_CKPT_CTAS) — i.e. a different work split and
+   different thread timing in every atomic — leaves byte-identical buckets
+   (record ids and item lists) after every stop.
 2. Lockstep emulation of G ranks (lockstep.py): G engines over the
    chunk-sliced shards of one database, their delta buffers and pair
    triangles summed slot by slot between the count and checkpoint halves,
@@ -69,8 +69,8 @@ def test_layout_independent_of_grid(monkeypatch, idx, n, interval):
     db = dic.BitDatabase.from_csr(indptr, indices, cfg.m)
     params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
     runs = []
-    for grid in ("1", "4", "29"):
-        monkeypatch.setenv("DIC_CAND_GRID", grid)
+    for grid in ("7", "148", "61"):
+        monkeypatch.setenv("DIC_CKPT_CTAS", grid)
         runs.append(_step_dumps(db, params))
     assert len(runs[0]) == len(runs[1]) == len(runs[2])
     new = 0
@@ -165,8 +165,8 @@ def test_large_stop_multi_run_commit_is_canonical_and_exact(monkeypatch):
     assert _stats(res.stats) == _oracle_tuple(want)
     db = dic.BitDatabase(ints, m=m)
     runs = []
-    for grid in ("1", "16"):
-        monkeypatch.setenv("DIC_CAND_GRID", grid)
+    for grid in ("3", "148"):
+        monkeypatch.setenv("DIC_CKPT_CTAS", grid)
         runs.append(_step_dumps(db, params, kmax=8))
     for a, b in zip(*runs):
         for (ra, ia), (rb, ib) in zip(a, b):

@@ -1,4 +1,4 @@
-"""Phase timeline of the per-stop commit_status kernel over a cfg4 run (lab
+"""Phase timeline of the per-stop checkpoint kernel (CTA 0) over a cfg4 run (lab
 build: python tools/lab/build_variant.py TIMING -DDIC_LAB_TIMING, then
 DIC_LIB=tools/lab/libs/lib_TIMING.so python tools/lab/commit_phases.py)."""
 
@@ -27,16 +27,29 @@ def main() -> None:
     buf = (C.c_ulonglong * (512 * 8))()
     _abi.load().dic_lab_commit_stamps(buf)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 8).astype(np.int64)
-    names = ["scan", "rank+commit", "last-out"]
-    for s in list(range(60, 100, 3)) + [100, 101, 150]:
-        r = a[s]
+    # stamps of CTA 0: 0 start, 1 after apply (+ barrier), 2 after compaction / joins (+ barrier),
+    # 3 after the commit, 4 last CTA out (before the status), 5 after the status; [6] = mode
+    # (0 grid, 1 small stop that called the grid in, 2 CTA 0 alone).  4 and 5 exist only when CTA 0 left last.
+    names = ["apply", "joins", "commit", "last-out", "status"]
+    tot = np.zeros(3)
+    modes = [0, 0, 0]
+    for s in range(326):
+        r = a[s].copy()
         if r[0] == 0:
             continue
-        if r[1] == 0:
-            print(s, "no commit")
-            continue
+        if r[2] < r[1]:
+            r[2] = r[1]
         d = np.diff(r[:4]) / 1e3
-        print(s, " ".join(f"{n}={x:.1f}" for n, x in zip(names, d)), "us")
+        tot += d
+        tail = np.diff(r[3:6]) / 1e3 if r[4] > r[3] and r[5] > r[4] else None
+        if tail is not None:
+            modes[int(r[6])] += 1
+        if s % 10 == 0 or s in (101, 102, 103, 104, 105):
+            extra = " ".join(f"{n}={x:.1f}" for n, x in zip(names[3:], tail)) + f" mode={r[6]}" if tail is not None else ""
+            ev = f"(eval {(r[7] - r[1]) / 1e3:.1f})" if a[s][7] > r[1] else ""
+            print(s, " ".join(f"{n}={x:.1f}" for n, x in zip(names, d)), ev, extra, f"sum={d.sum():.1f} us")
+    print("totals ms:", " ".join(f"{n}={x / 1e3:.2f}" for n, x in zip(names, tot)), f"sum={tot.sum() / 1e3:.2f}",
+          "stops seen to the end by CTA 0 per mode:", modes)
 
 
 if __name__ == "__main__":

@@ -69,7 +69,7 @@ def main() -> None:
     # per-launch duration series of the per-stop kernels (stop order)
     series = defaultdict(list)
     for s0, e0, n0 in acts:
-        for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "pair_tc", "dedup", "commit_status",
+        for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "pair_tc", "dedup", "commit_status", "checkpoint_kernel",
                     "compact", "status_kernel"):
             if key in n0:
                 series[key].append(round(e0 - s0, 1))
