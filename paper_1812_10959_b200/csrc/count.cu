@@ -61,7 +61,15 @@ __global__ void __launch_bounds__(256) item_support_kernel(const uint32_t* __res
 // ---------------------------------------------------------------------------
 // the streaming support count
 // ---------------------------------------------------------------------------
-constexpr int kStreamThreads = 512;
+// Threads per CTA (one CTA per SM).  TW = 32 tiles (m <= 768): 512 threads x 128
+// registers, as many candidates per thread as fit.  TW = 16 tiles (wider
+// universes, e.g. cfg4's m = 1000): 1,024 threads x 64 registers — the unit is
+// bound by shared-memory load latency, and eight warps per scheduler hide it
+// where four did not (ncu: short-scoreboard stalls 5.6 per issue at 512).
+#ifndef DIC_TW16_THREADS
+#define DIC_TW16_THREADS 512
+#endif
+__host__ __device__ constexpr int stream_threads(int TW) { return TW == 16 ? DIC_TW16_THREADS : 512; }
 constexpr int kMaxBuckets = 16;
 
 struct BucketDesc {
@@ -75,7 +83,6 @@ struct BucketDesc {
 struct StreamArgs {
     const uint32_t* tids;
     int32_t m, TW;
-    int32_t rowlanes;  // use the row-lane units for sizes <= 8
     uint32_t tile_bytes;
     int64_t t_first, t_last;  // inclusive tile range of the chunk
     int64_t row_splits;
@@ -111,7 +118,8 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     constexpr int RB = (TW + 4) * 4;  // row stride in bytes
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
-    const int64_t cbase = blk * (int64_t)kStreamThreads * R;
+    constexpr int NT = stream_threads(TW);
+    const int64_t cbase = blk * (int64_t)NT * R;
     const int k = K > 0 ? K : kdyn;
 
     if (threadIdx.x == 0) {
@@ -123,7 +131,7 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     uint32_t cnt[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
+        int64_t c = cbase + (int64_t)r * NT + threadIdx.x;
         int64_t cc = c < C ? c : C - 1;
         cnt[r] = 0;
         if constexpr (K > 0) {
@@ -142,7 +150,7 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
         // tiles holding a chunk edge: zero the rows outside [first, last]
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
-            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += kStreamThreads) {
+            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += NT) {
                 int item = idx / (TW + 4), slot = idx - item * (TW + 4);
                 if (slot < TW) w[idx] &= group_mask(geom, t * TW + slot);
             }
@@ -179,7 +187,7 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        int64_t c = cbase + (int64_t)r * kStreamThreads + threadIdx.x;
+        int64_t c = cbase + (int64_t)r * NT + threadIdx.x;
         if (c < C && cnt[r]) atomicAdd(out + c, (unsigned long long)cnt[r]);
     }
 }
@@ -217,7 +225,8 @@ __device__ __forceinline__ uint32_t popc4_csa(uint4 v) {
 // lanes once per unit.
 __host__ __device__ constexpr int rl_regs(int K, int TW) {
     return TW == 32 ? (K <= 4 ? 32 : (K == 5 ? 20 : (K == 6 ? 24 : 12)))   // cfg5-shaped (m <= 768)
-                    : (K <= 2 ? 32 : (K <= 4 ? 28 : (K <= 6 ? 20 : 12)));  // cfg4's m = 1000 stops
+           : DIC_TW16_THREADS == 1024 ? (K <= 2 ? 16 : (K <= 4 ? 12 : (K <= 6 ? 8 : 4)))  // cfg4's m = 1000 stops
+                                      : (K <= 2 ? 32 : (K <= 4 ? 28 : (K <= 6 ? 20 : 12)));
 }
 // (tuned per size on cfg5 with tools/lab/count_ab.sh; register allocation
 // across the per-size instantiations does not make this monotone)
@@ -225,7 +234,7 @@ static_assert(rl_regs(1, 32) % 4 == 0 && rl_regs(5, 32) % 4 == 0 && rl_regs(6, 3
                   rl_regs(7, 32) % 4 == 0 && rl_regs(3, 16) % 4 == 0 && rl_regs(5, 16) % 4 == 0 &&
                   rl_regs(7, 16) % 4 == 0,
               "row-lane id spans are loaded 8 bytes at a time");
-__host__ __device__ constexpr int rl_slots(int TW) { return kStreamThreads / (TW / 4); }  // candidate slots per CTA row
+__host__ __device__ constexpr int rl_slots(int TW) { return stream_threads(TW) / (TW / 4); }  // candidate slots per CTA
 
 template <int K, int TW>
 __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids, int m, uint32_t tb,
@@ -248,6 +257,8 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
     const int64_t cbase = blk * per + (int64_t)slot * R;
     // slots past the share re-count the block's last candidate (all lanes of
     // such a warp read the same rows: broadcasts) and add nothing
+    // a warp whose slots all lie past the share only keeps the barriers
+    const bool warp_live = __any_sync(0xFFFFFFFFu, cbase < bend);
     lab_stamp(0);
     if (threadIdx.x == 0) {
         fence_proxy_async();
@@ -301,7 +312,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         uint8_t* base = bufs + (size_t)s * tb;
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
-            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += kStreamThreads) {
+            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += stream_threads(TW)) {
                 int item = idx / (TW + 4), sl = idx - item * (TW + 4);
                 if (sl < TW) w[idx] &= group_mask(geom, t * TW + sl);
             }
@@ -316,6 +327,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
             for (int j = 0; j < KP; ++j) asm volatile("" : "+r"(it[r][j]));
         uint32_t prev0 = 0xFFFFFFFFu;
         uint4 v0 = make_uint4(0u, 0u, 0u, 0u);
+        if (warp_live)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t i0 = it[r][0] & 0xFFFFu;
@@ -367,27 +379,18 @@ __device__ __forceinline__ void dispatch_unit_rl(int k, const uint32_t* tids, in
 }
 
 // candidates per block of the unit kind used for (TW, k)
-__host__ __device__ inline int64_t cands_per_block(int TW, int k, bool rowlanes) {
-    if (rowlanes && k <= 8) return (int64_t)rl_slots(TW) * rl_regs(k, TW);
-    return (int64_t)kStreamThreads * regs_per_thread(k <= 8 ? k : 0);
+__host__ __device__ inline int64_t cands_per_block(int TW, int k) {
+    if (k <= 8) return (int64_t)rl_slots(TW) * rl_regs(k, TW);
+    return (int64_t)stream_threads(TW) * regs_per_thread(0);
 }
 
+// itemsets of more than 8 items: one candidate per thread, ids read per use
 template <int TW>
 __device__ __forceinline__ void dispatch_unit(int k, const uint32_t* tids, int m, uint32_t tb, const ChunkGeom& geom,
                                               const uint16_t* items, int64_t C, unsigned long long* out,
                                               int64_t blk, int64_t t0, int64_t t1, uint8_t* smem,
                                               uint32_t (&uses)[2]) {
-    switch (k) {
-        case 1: stream_unit<1, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 2: stream_unit<2, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 3: stream_unit<3, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 4: stream_unit<4, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 5: stream_unit<5, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 6: stream_unit<6, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 7: stream_unit<7, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        case 8: stream_unit<8, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-        default: stream_unit<0, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses); break;
-    }
+    stream_unit<0, TW>(tids, m, tb, geom, items, k, C, out, blk, t0, t1, smem, uses);
 }
 
 __device__ __forceinline__ void init_barriers(uint8_t* smem) {
@@ -402,7 +405,7 @@ __device__ __forceinline__ void init_barriers(uint8_t* smem) {
 
 // Host-sized launch (the dic_count_support API): grid = (row splits, blocks).
 template <int TW>
-__global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const __grid_constant__ StreamArgs a) {
+__global__ void __launch_bounds__(stream_threads(TW), 1) count_stream_kernel(const __grid_constant__ StreamArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     int64_t blk = blockIdx.y;
     int j = 0;
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) count_stream_kernel(const _
     if (t0 >= t1) return;
     init_barriers(smem);
     uint32_t uses[2] = {0u, 0u};
-    if (a.rowlanes && B.k <= 8)
+    if (B.k <= 8)
         dispatch_unit_rl<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
     else
         dispatch_unit<TW>(B.k, a.tids, a.m, a.tile_bytes, a.geom, B.items, B.C, B.out, blk, t0, t1, smem, uses);
@@ -512,60 +515,88 @@ __device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const Chu
 }
 
 template <int TW>
-__global__ void __launch_bounds__(kStreamThreads, 1) count_dev_kernel(const __grid_constant__ DevCountArgs a) {
+__global__ void __launch_bounds__(stream_threads(TW), 1) count_dev_kernel(const __grid_constant__ DevCountArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ int64_t pref[kDevMaxK + 1];
-    __shared__ int64_t cpref[kDevMaxK + 1];
+    __shared__ int64_t upref[kDevMaxK + 1];  // units before bucket k
+    __shared__ int64_t cpref[kDevMaxK + 1];  // candidates before bucket k
+    __shared__ int32_t srs[kDevMaxK];        // row splits of bucket k's blocks
     if (*a.abort) return;
     ChunkGeom geom;
     int64_t t_first, t_last;
     if (!dev_chunk(a, geom, t_first, t_last)) return;
+    const int64_t nt = t_last - t_first + 1;
     // bucket fills loaded in parallel (a loop of dependent-latency loads in
     // one thread would cost one L2 round trip per size)
     if (threadIdx.x < a.kuse) cpref[threadIdx.x + 1] = (int64_t)a.bn[threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {
         const bool dense = a.tri_len > 0 && 2 * cpref[3] >= a.tri_len;
-        int64_t acc = 0, cacc = 0;
-        pref[0] = 0;
+        // Row splits per bucket, weighted by what a block costs per tile: the
+        // tile's arrival is a floor (1.6 us with every SM streaming: tools/lab/
+        // count_fill.py), a full block's AND/POPC work takes 3.7 us and hides
+        // it.  A bucket holding a few hundred candidates then takes fewer CTAs
+        // with longer tile ranges instead of as many CTAs as a full block,
+        // which stretched every other block's range (cfg4's middle stops hold
+        // ~9k 3-item and a few hundred 4-item candidates).
+        constexpr float kFloor = 0.45f;
+        float wsum = 0.f;
+        int64_t cacc = 0, nblocks = 0;
         cpref[0] = 0;
         for (int k = 1; k < a.kuse; ++k) {
             int64_t C = cpref[k + 1];
             if (k == 2 && dense) C = 0;
-            const int64_t per = cands_per_block(TW, k, true);
-            pref[k] = acc;
+            const int64_t per = cands_per_block(TW, k);
+            const int64_t nb = (C + per - 1) / per;
             cpref[k] = cacc;
-            acc += (C + per - 1) / per;
             cacc += C;
+            nblocks += nb;
+            upref[k] = nb;  // (blocks, for now)
+            if (nb) wsum += (float)nb * fmaxf(kFloor, (float)C / (float)(nb * per));
         }
-        pref[a.kuse] = acc;
         cpref[a.kuse] = cacc;
+        int64_t uacc = 0;
+        for (int k = 1; k < a.kuse; ++k) {
+            const int64_t nb = upref[k];
+            int64_t rs = 1;
+            if (nb && nblocks < (int64_t)gridDim.x) {
+                const int64_t C = cpref[k + 1] - cpref[k];
+                const float w = fmaxf(kFloor, (float)C / (float)(nb * cands_per_block(TW, k)));
+                rs = (int64_t)((float)gridDim.x * w / wsum);
+#ifdef DIC_COUNT_UNIFORM_SPLITS
+                rs = (int64_t)gridDim.x / nblocks;
+#endif
+                rs = max((int64_t)1, min(rs, nt));
+            }
+            srs[k] = (int32_t)rs;
+            upref[k] = uacc;
+            uacc += nb * rs;
+        }
+        upref[a.kuse] = uacc;
+        upref[0] = 0;
     }
     __syncthreads();
-    const int64_t B = pref[a.kuse];
-    if (B == 0) return;
+    const int64_t U = upref[a.kuse];
+    if (U == 0) return;
     if (cpref[a.kuse] <= a.small_max) {
-        count_dev_small<TW>(a, geom, t_first, t_last - t_first + 1, cpref, a.kuse);
+        count_dev_small<TW>(a, geom, t_first, nt, cpref, a.kuse);
         return;
     }
-    const int64_t nt = t_last - t_first + 1;
-    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)gridDim.x / B));
-    const int64_t U = B * rs;
     if ((int64_t)blockIdx.x >= U) return;
     init_barriers(smem);
     uint32_t uses[2] = {0u, 0u};
     for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
-        const int64_t gb = u / rs, r = u - gb * rs;
         int k = 1;
-        while (pref[k + 1] <= gb) ++k;
+        while (upref[k + 1] <= u) ++k;
+        const int64_t rs = srs[k];
+        const int64_t gb = (u - upref[k]) / rs, r = (u - upref[k]) - gb * rs;
         const int64_t t0 = t_first + nt * r / rs, t1 = t_first + nt * (r + 1) / rs;
         if (t0 < t1) {
             if (k <= 8)
                 dispatch_unit_rl<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
-                                     a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+                                     a.delta + a.doff[k], gb, t0, t1, smem, uses);
             else
                 dispatch_unit<TW>(k, a.tids, a.m, a.tile_bytes, geom, a.items_tab[k], (int64_t)a.bn[k],
-                                  a.delta + a.doff[k], gb - pref[k], t0, t1, smem, uses);
+                                  a.delta + a.doff[k], gb, t0, t1, smem, uses);
         }
         __syncthreads();
     }
@@ -657,7 +688,7 @@ struct BucketIn {
 
 // Count every bucket over rows [first, last] in as few launches as possible.
 int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
-                         const BucketIn* bk, int nbk, cudaStream_t s, bool rowlanes = true) {
+                         const BucketIn* bk, int nbk, cudaStream_t s) {
     if (last < first) return DIC_OK;
     const int TW = tile_groups(m);
     const ChunkGeom geom = chunk_geom(first, last);
@@ -699,10 +730,9 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
         a.t_last = t_last;
         a.geom = geom;
         int64_t blocks = 0;
-        a.rowlanes = rowlanes ? 1 : 0;
         for (; i < nbk && a.nb < kMaxBuckets; ++i) {
             if (bk[i].C <= 0) continue;
-            const int64_t per = cands_per_block(TW, bk[i].k, rowlanes);
+            const int64_t per = cands_per_block(TW, bk[i].k);
             BucketDesc& d = a.b[a.nb++];
             d.items = bk[i].items;
             d.out = bk[i].out;
@@ -722,9 +752,9 @@ int count_buckets_launch(const uint32_t* tids, int64_t n, int m, int64_t first, 
         a.row_splits = rs;
         dim3 grid((unsigned)rs, (unsigned)blocks);
         if (TW == 32)
-            count_stream_kernel<32><<<grid, kStreamThreads, smem, s>>>(a);
+            count_stream_kernel<32><<<grid, stream_threads(32), smem, s>>>(a);
         else
-            count_stream_kernel<16><<<grid, kStreamThreads, smem, s>>>(a);
+            count_stream_kernel<16><<<grid, stream_threads(16), smem, s>>>(a);
         ::dic::note_launch();
         DIC_CHECK_LAUNCH("count_stream_kernel");
     }
@@ -790,9 +820,9 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
         attr16 = true;
     }
     if (a.TW == 32)
-        count_dev_kernel<32><<<sm_count(), kStreamThreads, smem, s>>>(a);
+        count_dev_kernel<32><<<sm_count(), stream_threads(32), smem, s>>>(a);
     else
-        count_dev_kernel<16><<<sm_count(), kStreamThreads, smem, s>>>(a);
+        count_dev_kernel<16><<<sm_count(), stream_threads(16), smem, s>>>(a);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("count_dev_kernel");
     return DIC_OK;

@@ -721,10 +721,51 @@ __device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, in
             if (!ok) continue;
             const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
             if (!(ks == 2 && prank)) {
-                for (int q = 0; q < ks && ok; ++q) {
-                    const int d = its[q];
-                    const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, ks, l, d, ks);
-                    ok = e >= 0 && is_box(R.shape[e]);
+                if (ks <= 4) {
+                    // the (up to four) subset probes side by side: their index
+                    // slots in one round of loads, the records they name in a
+                    // second, instead of a chain of 4 dependent loads per subset
+                    int32_t eq[4];
+                    unsigned slow = 0;  // probes that met a collision: sequential path below
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        eq[q] = -1;
+                        if (q < ks) {
+                            const uint64_t hq = hc ^ zob((uint32_t)its[q]);
+                            const hent_t x = ht[mix64(hq) & hmask];
+                            const int32_t e = hent_id(x);
+                            if (x == kEmptyEnt) ok = false;  // not known
+                            else if (hent_tag(x) == (uint32_t)(hq >> 32) && !(e & kTempFlag)) eq[q] = e;
+                            else slow |= 1u << q;
+                        }
+                    }
+                    if (!ok) continue;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (q < ks && eq[q] >= 0) {
+                            const unsigned long long* rm = R.mask + (int64_t)eq[q] * W;
+                            bool match = R.size[eq[q]] == ks;
+                            match &= ((rm[l >> 6] >> (l & 63)) & 1ull) != 0;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+                                if (p < ks && p != q) match &= ((rm[its[p] >> 6] >> (its[p] & 63)) & 1ull) != 0;
+                            const bool box = is_box(R.shape[eq[q]]);
+                            if (!match) slow |= 1u << q;
+                            else ok &= box;
+                        }
+                    }
+                    for (int q = 0; q < ks && ok; ++q) {
+                        if (!((slow >> q) & 1u)) continue;
+                        const int d = its[q];
+                        const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, ks, l, d, ks);
+                        ok = e >= 0 && is_box(R.shape[e]);
+                    }
+                } else {
+                    for (int q = 0; q < ks && ok; ++q) {
+                        const int d = its[q];
+                        const int32_t e = ht_find_items(ht, hmask, R, W, hc ^ zob((uint32_t)d), its, ks, l, d, ks);
+                        ok = e >= 0 && is_box(R.shape[e]);
+                    }
                 }
                 if (!ok) continue;
             }
@@ -866,11 +907,22 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
         const JoinRec je = a.joins[e];
         if (je.hi == ~0ull) continue;  // duplicate
         unsigned cnt = 0;
-        for (int64_t j = lane; j < na; j += 32) {
-            const unsigned long long hj = a.joins[j].hi, lj = a.joins[j].lo;
-            bool less = hj != je.hi ? hj < je.hi : lj < je.lo;  // (~0 is never smaller)
-            if (hj == je.hi && lj == je.lo && j != e) less = join_less_slow(a, a.joins[j], je);
-            cnt += less ? 1u : 0u;
+        for (int64_t j0 = lane; j0 < na; j0 += 128) {
+            // four keys per lane and round: their loads go out together
+            unsigned long long hj[4], lj[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t j = j0 + 32 * u;
+                hj[u] = j < na ? a.joins[j].hi : ~0ull;
+                lj[u] = j < na ? a.joins[j].lo : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t j = j0 + 32 * u;
+                bool less = hj[u] != je.hi ? hj[u] < je.hi : lj[u] < je.lo;  // (~0 is never smaller)
+                if (hj[u] == je.hi && lj[u] == je.lo && j != e && j < na) less = join_less_slow(a, a.joins[j], je);
+                cnt += less ? 1u : 0u;
+            }
         }
         cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
         // record nrec0 + rank at bucket slot bn0[sz] + rank - start[sz]; its
@@ -1143,6 +1195,64 @@ __global__ void gather_frequent_kernel(Records R, int W, const int32_t* __restri
     for (int w = 0; w < W; ++w) masks[i * W + w] = R.mask[(int64_t)r * W + w];
     sizes[i] = R.size[r];
     supports[i] = R.support[r];
+}
+
+// Canonical order of the result (engine.py:446-455): by size, then by the
+// mask as an integer — for masks of equal size, the lexicographic order of
+// their item ids listed from the highest down.  Key of a frequent record of
+// at most 8 items: (size, ids descending), 16 bits each; *big is raised when a
+// larger itemset is met (the host then sorts instead).
+struct ResKey {
+    unsigned long long k0, k1, k2;
+};
+
+__global__ void result_keys_kernel(Records R, const int32_t* __restrict__ ids, int64_t F, ResKey* __restrict__ keys,
+                                   unsigned long long* big) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F) return;
+    const int32_t r = ids[i];
+    const int sz = R.size[r];
+    ResKey k{(unsigned long long)(uint32_t)sz << 48, 0ull, 0ull};
+    if (sz > 8) {
+        *big = 1ull;
+    } else {
+        const uint4 iv = *reinterpret_cast<const uint4*>(R.items + (int64_t)r * 8);
+        const uint32_t w[4] = {iv.x, iv.y, iv.z, iv.w};
+        for (int q = 0; q < sz; ++q) {
+            const int a = sz - 1 - q;  // q-th highest id
+            const unsigned long long it = (w[a >> 1] >> ((a & 1) * 16)) & 0xFFFFu;
+            if (q < 3) k.k0 |= it << (32 - 16 * q);
+            else if (q < 7) k.k1 |= it << (48 - 16 * (q - 3));
+            else k.k2 |= it << 48;
+        }
+    }
+    keys[i] = k;
+}
+
+// One warp per frequent record: its position is the number of smaller keys
+// (distinct itemsets have distinct keys); the warp then writes the record's
+// mask, size and support to that position.
+__global__ void result_rank_gather_kernel(Records R, int W, const int32_t* __restrict__ ids, int64_t F,
+                                          const ResKey* __restrict__ keys, unsigned long long* __restrict__ masks,
+                                          int32_t* __restrict__ sizes, int64_t* __restrict__ supports) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < F; i += warps) {
+        const ResKey me = keys[i];
+        unsigned cnt = 0;
+        for (int64_t j = lane; j < F; j += 32) {
+            const ResKey o = keys[j];
+            const bool less = o.k0 != me.k0 ? o.k0 < me.k0 : (o.k1 != me.k1 ? o.k1 < me.k1 : o.k2 < me.k2);
+            cnt += less ? 1u : 0u;
+        }
+        const int64_t pos = (int64_t)__reduce_add_sync(0xFFFFFFFFu, cnt);
+        const int32_t r = ids[i];
+        for (int w = lane; w < W; w += 32) masks[pos * W + w] = R.mask[(int64_t)r * W + w];
+        if (lane == 0) {
+            sizes[pos] = R.size[r];
+            supports[pos] = R.support[r];
+        }
+    }
 }
 
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
@@ -2523,17 +2633,35 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
     e->res_F = -1;  // ids consumed
     const int W = e->W;
     if (F == 0) return DIC_OK;
-    // one device buffer and one pinned staging buffer: masks | sizes | supports
-    const size_t mb = (size_t)F * W * 8, sb = (size_t)F * 4, pb = (size_t)F * 8;
-    const size_t total = mb + pb + sb;
+    // one device buffer and one pinned staging buffer: masks | supports | sizes | flag
+    const size_t mb = (size_t)F * W * 8, sb = ((size_t)F * 4 + 7) & ~(size_t)7, pb = (size_t)F * 8;
+    const size_t total = mb + pb + sb + 8;
     uint8_t* dbuf = nullptr;
     if ((rc = dalloc(&dbuf, (int64_t)total, e->s))) return rc;
     auto* dm = reinterpret_cast<unsigned long long*>(dbuf);
     auto* dsu = reinterpret_cast<int64_t*>(dbuf + mb);
     auto* dsz = reinterpret_cast<int32_t*>(dbuf + mb + pb);
-    gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, W, e->res_ids, F, dm, dsz, dsu);
-    ::dic::note_launch();
-    DIC_CHECK_LAUNCH("gather_frequent_kernel");
+    auto* dflag = reinterpret_cast<unsigned long long*>(dbuf + mb + pb + sb);
+    // up to kDevSortMax itemsets (of at most 8 items each) are put in the
+    // result's canonical order on the device: rank by counting, F^2 / 32 warp
+    // steps, a few microseconds for the thousands of itemsets a run finds
+    constexpr int64_t kDevSortMax = 24576;
+    bool dev_sorted = F <= kDevSortMax;
+    DIC_CUDA(cudaMemsetAsync(dflag, 0, 8, e->s));
+    if (dev_sorted) {
+        ResKey* keys = nullptr;
+        if ((rc = dalloc(&keys, F, e->s))) return rc;
+        result_keys_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, e->res_ids, F, keys, dflag);
+        ::dic::note_launch();
+        result_rank_gather_kernel<<<sm_count() * 4, 256, 0, e->s>>>(e->R, W, e->res_ids, F, keys, dm, dsz, dsu);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("result_rank_gather_kernel");
+        dfree(keys, e->s);
+    } else {
+        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, W, e->res_ids, F, dm, dsz, dsu);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("gather_frequent_kernel");
+    }
     HostRes& hr = e->hres;
     if (hr.stage_bytes < total) {
         if (hr.stage) cudaFreeHost(hr.stage);
@@ -2544,11 +2672,26 @@ extern "C" int dic_engine_frequent(dic_engine* e, uint64_t* masks_host, int32_t*
         hr.stage_bytes = want;
     }
     DIC_CUDA(cudaMemcpyAsync(hr.stage, dbuf, total, cudaMemcpyDeviceToHost, e->s));
-    dfree(dbuf, e->s);
     DIC_CUDA(cudaStreamSynchronize(e->s));
+    if (dev_sorted && *reinterpret_cast<const unsigned long long*>(hr.stage + mb + pb + sb) != 0) {
+        // an itemset of more than 8 items: gather unordered, sort on the host
+        dev_sorted = false;
+        gather_frequent_kernel<<<nblk(F), 256, 0, e->s>>>(e->R, W, e->res_ids, F, dm, dsz, dsu);
+        ::dic::note_launch();
+        DIC_CHECK_LAUNCH("gather_frequent_kernel");
+        DIC_CUDA(cudaMemcpyAsync(hr.stage, dbuf, total, cudaMemcpyDeviceToHost, e->s));
+        DIC_CUDA(cudaStreamSynchronize(e->s));
+    }
+    dfree(dbuf, e->s);
     const uint64_t* m1 = reinterpret_cast<const uint64_t*>(hr.stage);
     const int64_t* p1 = reinterpret_cast<const int64_t*>(hr.stage + mb);
     const int32_t* s1 = reinterpret_cast<const int32_t*>(hr.stage + mb + pb);
+    if (dev_sorted) {
+        memcpy(masks_host, m1, mb);
+        memcpy(sizes_host, s1, (size_t)F * 4);
+        memcpy(supports_host, p1, pb);
+        return DIC_OK;
+    }
     // canonical order of the reference's result (engine.py:446-455): by size,
     // then by the mask as an integer.  For masks of equal size that order is
     // the lexicographic order of their item ids listed from the highest down,
