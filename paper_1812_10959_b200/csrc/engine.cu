@@ -77,17 +77,29 @@ __host__ __device__ inline uint64_t zob(uint32_t item) {
     return mix64(0x5A0B1157ull + (uint64_t)item * 0x9E3779B97F4A7C15ull);
 }
 
-constexpr int32_t kEmpty = -1;
-constexpr int32_t kTempFlag = 0x40000000;
-// Hash-index entries: (upper 32 bits of the mask's hash) << 32 | record id, so
-// a probe reads one word and only a tag match touches the record's mask.
+// Hash-index entries, one 64-bit word each, so a probe reads one word and only
+// a tag match touches a record:
+//   record     bit 63 = 0 | 31-bit tag (bits 32.. of the mask's hash) | record id
+//   temporary  bit 63 = 1 | joined item l (16) | source record (31) | 16 tag bits
+//              a join of the current stop, cand = source's itemset + {l}, not
+//              yet a record (checkpoint kernel); self-describing, so a thread
+//              that meets it needs nothing but the records of earlier stops
+//   empty      all ones (no temporary entry looks like it: record ids stay
+//              far below 2^31 - 1)
 typedef unsigned long long hent_t;
 constexpr hent_t kEmptyEnt = ~0ull;
+__host__ __device__ __forceinline__ uint32_t htag(uint64_t h) { return (uint32_t)(h >> 32) & 0x7FFFFFFFu; }
 __host__ __device__ __forceinline__ hent_t hent(uint64_t h, int32_t id) {
-    return ((hent_t)(uint32_t)(h >> 32) << 32) | (uint32_t)id;
+    return ((hent_t)htag(h) << 32) | (uint32_t)id;
 }
 __host__ __device__ __forceinline__ int32_t hent_id(hent_t x) { return (int32_t)(uint32_t)x; }
 __host__ __device__ __forceinline__ uint32_t hent_tag(hent_t x) { return (uint32_t)(x >> 32); }
+__host__ __device__ __forceinline__ bool hent_temp(hent_t x) { return (x >> 63) != 0; }  // (after the empty test)
+__host__ __device__ __forceinline__ hent_t hent_join(uint64_t h, int32_t src, int l) {
+    return (1ull << 63) | ((hent_t)(uint32_t)l << 47) | ((hent_t)(uint32_t)src << 16) | ((h >> 32) & 0xFFFFull);
+}
+__host__ __device__ __forceinline__ int32_t hent_join_src(hent_t x) { return (int32_t)((x >> 16) & 0x7FFFFFFFull); }
+__host__ __device__ __forceinline__ int hent_join_item(hent_t x) { return (int)((x >> 47) & 0xFFFFull); }
 
 // Status words (device, one contiguous u64 array).
 enum : int {
@@ -144,13 +156,13 @@ __device__ __forceinline__ bool mask_eq(const unsigned long long* a, const MaskV
 __device__ __forceinline__ int32_t ht_lookup(const hent_t* __restrict__ ht, uint64_t hmask, const Records& R,
                                              int W, uint64_t h, const MaskView& v) {
     uint64_t slot = mix64(h) & hmask;
-    const uint32_t tag = (uint32_t)(h >> 32);
+    const uint32_t tag = htag(h);
     while (true) {
         const hent_t x = ht[slot];
         const int32_t e = hent_id(x);
-        if (e == kEmpty) return -1;
-        // (temporary entries: this stop's unpublished joins, never a record)
-        if (hent_tag(x) == tag && !(e & kTempFlag) && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
+        if (x == kEmptyEnt) return -1;
+        // (a temporary entry — an unpublished join of this stop, never a record — has bit 63 set: no tag match)
+        if (hent_tag(x) == tag && mask_eq(R.mask + (int64_t)e * W, v, W)) return e;
         slot = (slot + 1) & hmask;
     }
 }
@@ -164,12 +176,12 @@ __device__ __forceinline__ int32_t ht_find_items(const hent_t* __restrict__ ht, 
                                                  int W, uint64_t h, const int* its, int k, int add, int drop,
                                                  int size) {
     uint64_t slot = mix64(h) & hmask;
-    const uint32_t tag = (uint32_t)(h >> 32);
+    const uint32_t tag = htag(h);
     while (true) {
         const hent_t x = ht[slot];
         const int32_t e = hent_id(x);
-        if (e == kEmpty) return -1;
-        if (hent_tag(x) == tag && !(e & kTempFlag) && R.size[e] == size) {
+        if (x == kEmptyEnt) return -1;
+        if (hent_tag(x) == tag && R.size[e] == size) {
             const unsigned long long* rm = R.mask + (int64_t)e * W;
             bool ok = add < 0 || ((rm[add >> 6] >> (add & 63)) & 1ull);
             for (int q = 0; q < k; ++q) {
@@ -307,7 +319,6 @@ struct CkptArgs {
     uint64_t hmask;
     JoinRec* joins;               // this stop's admitted joins (eval -> commit)
     int64_t tmp_cap, rec_cap, hcap;
-    unsigned long long* ins_k;    // [kDoffMax] new candidates by size (eval -> commit)
     unsigned long long* ring;     // host-mapped status ring
     int64_t ring_words;
     unsigned long long* sync;     // [0] grid-barrier arrivals, [1] CTAs out (both zero between launches),
@@ -331,7 +342,7 @@ struct CkptSmem {
 
 #ifdef DIC_LAB_TIMING
 // lab build: per-stop phase stamps of CTA 0 (globaltimer ns), slot S_SEQ % 512
-__device__ unsigned long long g_lab_commit[512][8];
+__device__ unsigned long long g_lab_commit[512][12];
 #define CKPT_STAMP(i)                                                                        \
     do {                                                                                     \
         if (threadIdx.x == 0 && blockIdx.x == 0) {                                           \
@@ -572,19 +583,19 @@ __device__ __forceinline__ void compact_bucket(const CkptArgs& a, CkptSmem& sm, 
 // same in either order.
 //
 // A join that passes walks cand's probe chain once: an existing record with
-// cand's mask -> already known, drop; a temporary entry (kTempFlag | join
-// index) with cand's mask -> another source produced the same candidate at
-// this stop, drop (all duplicates carry the same mask, so which join wins
-// does not matter); an empty slot -> allocate a join record, publish it
-// (fence) and CAS the slot: the winner owns the candidate.  No record is
-// published before the commit, so a non-temporary entry always names a record
-// of an earlier stop, and a subset lookup that meets a temporary entry just
-// keeps probing (a fresh candidate is no box: the join fails either way, as
-// in the reference, where it is a DASHED_CIRCLE).  The all-or-nothing
-// capacity check follows the phase; if it fails the host rebuilds the index
-// from the records (dropping the temporary entries) and replays.
+// cand's mask -> already known, drop; a temporary entry with cand's mask ->
+// another source produced the same candidate at this stop, drop (all
+// duplicates carry the same mask, so which join wins does not matter); an
+// empty slot -> CAS a temporary entry into it: the winner owns the candidate
+// and takes a join record.  No record is published before the commit, so a
+// non-temporary entry always names a record of an earlier stop, and a subset
+// lookup that meets a temporary entry just keeps probing (a fresh candidate is
+// no box: the join fails either way, as in the reference, where it is a
+// DASHED_CIRCLE).  The all-or-nothing capacity check follows the phase; if it
+// fails the host rebuilds the index from the records (dropping the temporary
+// entries) and replays.
 struct JoinRec {
-    unsigned long long hi, lo;  // sort key (size, first seven ids, 16 bits each); hi == ~0: duplicate, no candidate
+    unsigned long long hi, lo;  // sort key (size, first seven ids, 16 bits each)
     uint64_t hash;
     int64_t slot;  // hash slot the owner claimed
     int32_t src;   // source record: the candidate is src's itemset + {l}
@@ -620,47 +631,50 @@ __device__ __noinline__ void claim_join(const CkptArgs& a, int32_t src, int l, u
     unsigned long long* stat = a.stat;
     const Records& R = a.R;
     const int W = a.W;
-    const uint32_t tag = (uint32_t)(hc >> 32);
+    const uint32_t tag = htag(hc);
     const MaskView cand{R.mask + (int64_t)src * W, l, -1};
+#ifdef DIC_LAB_TIMING
+    struct LabT {
+        unsigned long long t0, seq;
+        __device__ LabT(unsigned long long s) : seq(s) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0)); }
+        __device__ ~LabT() {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            atomicMax(&g_lab_commit[seq % 512][8], t1 - t0);
+            atomicAdd(&g_lab_commit[seq % 512][10], 1ull);
+        }
+    } lab_t(stat[S_SEQ]);
+#endif
     uint64_t slot = mix64(hc) & a.hmask;
-    int64_t t = -1;
     hent_t x = ldv(a.ht + slot);
     while (true) {
         if (x == kEmptyEnt) {
-            if (t < 0) {
-                t = (int64_t)atomicAdd(&stat[S_NADM], 1ull);
-                atomicAdd(&stat[S_HEAD + a.KS + sz], 1ull);  // adm[sz]
-                if (t >= a.tmp_cap) return;                  // the capacity check will see NADM
-                JoinRec* j = a.joins + t;
-                j->hi = hi;
-                j->lo = lo;
-                j->hash = hc;
-                j->src = src;
-                j->l = (uint16_t)l;
-                j->size = (uint16_t)sz;
-                __threadfence();  // the record before the entry that names it
-            }
-            x = atomicCAS(a.ht + slot, kEmptyEnt, hent(hc, kTempFlag | (int32_t)t));
-            if (x == kEmptyEnt) {  // owner
-                a.joins[t].slot = (int64_t)slot;
+            x = atomicCAS(a.ht + slot, kEmptyEnt, hent_join(hc, src, l));
+            if (x == kEmptyEnt) {  // owner: the stop's next join record
+                const int64_t t = (int64_t)atomicAdd(&stat[S_NADM], 1ull);
                 atomicAdd(&stat[S_NINS], 1ull);
-                atomicAdd(&a.ins_k[sz], 1ull);
+                atomicAdd(&stat[S_HEAD + a.KS + sz], 1ull);  // adm[sz]
+                if (t < a.tmp_cap) {                          // (else: the capacity check sees NADM)
+                    JoinRec* j = a.joins + t;
+                    j->hi = hi;
+                    j->lo = lo;
+                    j->hash = hc;
+                    j->slot = (int64_t)slot;
+                    j->src = src;
+                    j->l = (uint16_t)l;
+                    j->size = (uint16_t)sz;
+                }
                 return;
             }
             // another thread took the slot first: examine its entry
         }
-        if (hent_tag(x) == tag) {
+        bool same = false;
+        if (hent_temp(x)) {
+            if ((x & 0xFFFFull) == ((hc >> 32) & 0xFFFFull))
+                same = views_same(MaskView{R.mask + (int64_t)hent_join_src(x) * W, hent_join_item(x), -1}, cand, W);
+        } else if (hent_tag(x) == tag) {
             const int32_t e = hent_id(x);
-            bool same;
-            if (e & kTempFlag) {
-                const JoinRec* o = a.joins + (e & ~kTempFlag);
-                // (L2 loads: the record was published by another SM during this phase)
-                const uint64_t oh = ldv(reinterpret_cast<const unsigned long long*>(&o->hash));
-                const unsigned long long ow = ldv(reinterpret_cast<const unsigned long long*>(&o->src));
-                same = oh == hc && (int)((ow >> 48) & 0xFFFFu) == sz &&
-                       views_same(MaskView{R.mask + (int64_t)(int32_t)(uint32_t)ow * W, (int)((ow >> 32) & 0xFFFFu), -1},
-                                  cand, W);
-            } else if (its) {
+            if (its) {
                 // a record of the same size holding every item of cand IS cand
                 same = R.size[e] == sz;
                 if (same) {
@@ -672,11 +686,8 @@ __device__ __noinline__ void claim_join(const CkptArgs& a, int32_t src, int l, u
             } else {
                 same = mask_eq(R.mask + (int64_t)e * W, cand, W);
             }
-            if (same) {
-                if (t >= 0) a.joins[t].hi = ~0ull;  // the join slot stays unused
-                return;
-            }
         }
+        if (same) return;  // known, or another join's candidate
         slot = (slot + 1) & a.hmask;
         x = ldv(a.ht + slot);
     }
@@ -735,7 +746,7 @@ __device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, in
                             const hent_t x = ht[mix64(hq) & hmask];
                             const int32_t e = hent_id(x);
                             if (x == kEmptyEnt) ok = false;  // not known
-                            else if (hent_tag(x) == (uint32_t)(hq >> 32) && !(e & kTempFlag)) eq[q] = e;
+                            else if (hent_tag(x) == htag(hq)) eq[q] = e;
                             else slow |= 1u << q;
                         }
                     }
@@ -882,7 +893,7 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
         int64_t carry = 0;
         for (int k0 = 0; k0 < top; k0 += 32) {
             const int k = k0 + lane;
-            const int64_t v = k < top ? (int64_t)ldv(a.ins_k + k) : 0;
+            const int64_t v = k < top ? (int64_t)ldv(stat + S_HEAD + a.KS + k) : 0;  // adm[k]
             int64_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -905,7 +916,6 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
     // the stop commits only a few)
     for (int64_t e = (int64_t)wid * nctas + cta; e < na; e += warps) {
         const JoinRec je = a.joins[e];
-        if (je.hi == ~0ull) continue;  // duplicate
         unsigned cnt = 0;
         for (int64_t j0 = lane; j0 < na; j0 += 128) {
             // four keys per lane and round: their loads go out together
@@ -919,7 +929,7 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int64_t j = j0 + 32 * u;
-                bool less = hj[u] != je.hi ? hj[u] < je.hi : lj[u] < je.lo;  // (~0 is never smaller)
+                bool less = hj[u] != je.hi ? hj[u] < je.hi : lj[u] < je.lo;  // (the ~0 filler is never smaller)
                 if (hj[u] == je.hi && lj[u] == je.lo && j != e && j < na) less = join_less_slow(a, a.joins[j], je);
                 cnt += less ? 1u : 0u;
             }
@@ -1109,6 +1119,13 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
     if (nfront > 0) {
         eval_phase(a, nfront, cta, nctas);
         CKPT_STAMP(7);
+#ifdef DIC_LAB_TIMING
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(&g_lab_commit[stat[S_SEQ] % 512][9], t);
+        }
+#endif
         if (solo) {
             __syncthreads();
         } else {
@@ -1137,9 +1154,8 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
         unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
         const int top = a.kuse < kDoffMax ? a.kuse : kDoffMax;
         for (int k = threadIdx.x; k < top; k += blockDim.x) {
-            const unsigned long long n = ldv(a.ins_k + k);
+            const unsigned long long n = ldv(stat + S_HEAD + a.KS + k);  // adm[k]
             if (n) bn[k] = ldv(bn + k) + n;
-            a.ins_k[k] = 0;
         }
         if (threadIdx.x == 0) stat[S_NREC] = ldv(stat + S_NREC) + (unsigned long long)N;
     }
@@ -1339,7 +1355,6 @@ struct dic_engine {
 
     JoinRec* joins = nullptr;             // the stop's admitted joins (checkpoint kernel: eval -> commit)
     int64_t tmp_cap = 0;
-    unsigned long long* ins_k = nullptr;  // [kDoffMax + 2] new candidates by size (dedup -> commit_status)
 
     // the pair bucket as a dense triangle over the frequent items (pairs.cu)
     const uint32_t* pair_tids = nullptr;  // tids restricted to level1 (or tids itself)
@@ -1766,7 +1781,6 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
     a.tmp_cap = e->tmp_cap;
     a.rec_cap = e->R.cap;
     a.hcap = e->hcap;
-    a.ins_k = e->ins_k;
     a.ring = e->ring_dev;
     a.ring_words = e->ring_words;
     a.sync = e->d_sync;
@@ -1998,7 +2012,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
         (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s)) ||
-        (rc = dalloc(&e->ins_k, kDoffMax + 2, e->s)) || (rc = dalloc(&e->d_sync, 4, e->s))) {
+        (rc = dalloc(&e->d_sync, 4, e->s))) {
         delete e;
         return rc;
     }
@@ -2016,7 +2030,6 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
-    cudaMemsetAsync(e->ins_k, 0, (kDoffMax + 2) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_sync, 0, 4 * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
     cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
@@ -2038,7 +2051,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s);
     if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
-    dfree(e->joins, s); dfree(e->ins_k, s); dfree(e->d_sync, s);
+    dfree(e->joins, s); dfree(e->d_sync, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
     if (!e->fused) dfree(e->tri, s);
     if (e->fused) {
@@ -2455,7 +2468,6 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_NADM, 0, 3 * u, e->s));  // NADM, NINS, OVERFLOW
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_ABORT, 0, u, e->s));
         DIC_CUDA(cudaMemsetAsync(e->d_stat + S_HEAD + KS, 0, (size_t)KS * u, e->s));
-        DIC_CUDA(cudaMemsetAsync(e->ins_k, 0, kDoffMax * u, e->s));
         if ((rc = launch_checkpoint(e, e->s, true))) return rc;  // ends with the stop's status
         e->kuse_at[slot] = e->kuse;
         DIC_CUDA(cudaStreamSynchronize(e->s));

@@ -24,9 +24,9 @@ def main() -> None:
     db = dic.BitDatabase.from_csr(ip, ix, cfg.m)
     params = dic.MiningParams.create(cfg.n, cfg.minsup, interval=cfg.interval)
     run_engine(db.device_tids(), cfg.n, cfg.m, params)
-    buf = (C.c_ulonglong * (512 * 8))()
+    buf = (C.c_ulonglong * (512 * 12))()
     _abi.load().dic_lab_commit_stamps(buf)
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 8).astype(np.int64)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 12).astype(np.int64)
     # stamps of CTA 0: 0 start, 1 after apply (+ barrier), 2 after compaction / joins (+ barrier),
     # 3 after the commit, 4 last CTA out (before the status), 5 after the status; [6] = mode
     # (0 grid, 1 small stop that called the grid in, 2 CTA 0 alone).  4 and 5 exist only when CTA 0 left last.
@@ -46,7 +46,8 @@ def main() -> None:
             modes[int(r[6])] += 1
         if s % 10 == 0 or s in (101, 102, 103, 104, 105):
             extra = " ".join(f"{n}={x:.1f}" for n, x in zip(names[3:], tail)) + f" mode={r[6]}" if tail is not None else ""
-            ev = f"(eval {(r[7] - r[1]) / 1e3:.1f})" if a[s][7] > r[1] else ""
+            ev = (f"(eval cta0 {(r[7] - r[1]) / 1e3:.1f}, last cta {(r[9] - r[1]) / 1e3:.1f}, {r[10]} claims, "
+                  f"slowest {r[8] / 1e3:.1f})") if a[s][7] > r[1] else ""
             print(s, " ".join(f"{n}={x:.1f}" for n, x in zip(names, d)), ev, extra, f"sum={d.sum():.1f} us")
     print("totals ms:", " ".join(f"{n}={x / 1e3:.2f}" for n, x in zip(names, tot)), f"sum={tot.sum() / 1e3:.2f}",
           "stops seen to the end by CTA 0 per mode:", modes)
