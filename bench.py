@@ -200,7 +200,7 @@ def kernel_microbench(peaks: dict, reps: int = 3) -> dict:
         hb.append(e0.elapsed_time(e1))
     hbm_gbs, hbm_src = measured_hbm()
     t_hbm = min(hb)
-    moved = tids.numel() * tids.element_size()  # tiles incl. 4 pad words per item row
+    moved = tids.numel() * tids.element_size()  # whole tiles (dense rows: the bitmap rounded up to tiles)
     hbm = {"kernel": "item_support_kernel", "ms": t_hbm, "bytes_read": moved,
            "algorithmic_bytes": n * words_for(m) * 8, "achieved_gbs": moved / (t_hbm * 1e-3) / 1e9,
            "peak_gbs": hbm_gbs, "frac": moved / (t_hbm * 1e-3) / 1e9 / hbm_gbs, "peak_source": hbm_src}

@@ -26,19 +26,18 @@
  *   rows   : uint64 [n][W], W = ceil(m/64); item p of row j is bit (p & 63)
  *            of word (p >> 6) — the reference's single-word layout
  *            (bitops.py:36) extended LSW-first to W words.
- *   tids   : the tiled, padded bit-sliced ("vertical") copy, uint32 words.
- *            Rows are grouped 32 per word (group g = rows 32g..32g+31, bit
- *            b <-> row 32g+b).  A tile holds TW groups of all m items,
+ *   tids   : the tiled bit-sliced ("vertical") copy, uint32 words.  Rows are
+ *            grouped 32 per word (group g = rows 32g..32g+31, bit b <-> row
+ *            32g+b).  A tile holds TW groups of all m items,
  *            TW = dic_tids_tile_groups(m) = 32 (m <= 768) or 16.  Item i's TW
- *            words of tile t form one row padded by 4 zero words, so the row
- *            stride is RW = TW + 4 words (an odd number of 16-byte chunks: the
- *            shared-memory copy of a tile reads conflict-free) and there is
- *            no swizzle:
- *              word(i, g) = tids[t*m*RW + i*RW + (g - t*TW)],  t = g / TW,
+ *            words of tile t form one dense row of 128 or 64 bytes — no pad
+ *            words, no swizzle:
+ *              word(i, g) = tids[t*m*TW + i*TW + (g - t*TW)],  t = g / TW,
  *            i.e. dic_tids_index(m, i, g).  A tile's global image equals its
  *            shared-memory image, so one bulk copy (TMA engine) stages it.
- *            Rows past n and the pad words read as zero; the buffer holds
- *            dic_tids_words(n, m) = ceil(ceil(n/32)/TW) * m * RW words.
+ *            Rows past n read as zero; the buffer holds
+ *            dic_tids_words(n, m) = ceil(ceil(n/32)/TW) * m * TW words —
+ *            exactly the bitmap's bits, rounded up to whole tiles.
  *   items  : uint16 [C][k], the k ascending item ids of each candidate of a
  *            size-k bucket (candidates of one launch share k).
  */

@@ -78,16 +78,18 @@ __device__ __forceinline__ uint32_t group_mask(const ChunkGeom& c, int64_t g) {
 }
 
 // ----------------------------------------------------------------------------
-// Tiled, padded bit-sliced layout ("tids"; include/dic_b200.h).  A tile holds
-// TW row-groups (TW*32 rows) of all m items: item i's TW words form one row,
-// padded by 4 zero words, so the row stride RW = TW + 4 words is 4 mod 8
-// banks-of-16-bytes... i.e. 16-byte chunk q of item i sits in bank group
-// (i * RW/4 + q) mod 8 with RW/4 odd: 8 lanes reading the same chunk of 8
-// items that differ mod 8 hit 8 different bank groups, and every chunk
-// address is a compile-time offset from the row base.  The tile's global
-// image equals its shared-memory image, so one bulk copy stages it.
-__host__ __device__ inline int tile_groups(int m) { return m <= 768 ? 32 : 16; }
-__host__ __device__ inline int row_words(int TW) { return TW + 4; }
+// Tiled bit-sliced layout ("tids"; include/dic_b200.h).  A tile holds TW
+// row-groups (TW*32 rows) of all m items: item i's TW words form one dense row
+// (64 or 128 bytes, no pad, no swizzle), so HBM holds exactly the bitmap's
+// bits.  The tile's global image equals its shared-memory image: one bulk copy
+// stages it.  Readers keep shared-memory accesses conflict-free by how lanes
+// are assigned, not by padding: the row-lane count units give the TW/4 chunks
+// of one row to adjacent lanes (a contiguous 64/128-byte segment), and the
+// AND/POPC pair kernel and the one-candidate-per-lane unit walk a row's chunks
+// in an order rotated by the lane.
+constexpr int kRowPad = 0;
+__host__ __device__ constexpr int tile_groups(int m) { return m <= 768 ? 32 : 16; }
+__host__ __device__ constexpr int row_words(int TW) { return TW + kRowPad; }
 __host__ __device__ inline int64_t tile_count(int64_t n, int m) {
     int64_t groups = (n + 31) / 32;
     int TW = tile_groups(m);

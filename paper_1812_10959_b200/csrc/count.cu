@@ -27,34 +27,63 @@ namespace dic {
 // ---------------------------------------------------------------------------
 // item support (first pass)
 // ---------------------------------------------------------------------------
-// grid.x = tile splits; thread = item (strided); each thread sums its item
-// row over the split's tiles (rows of adjacent items are adjacent in memory).
+// grid.x = tile splits.  The TW/4 lanes of a group take the 16-byte chunks of
+// one item row, so a warp reads 512 contiguous bytes (4 or 8 adjacent item
+// rows) per load; a lane sums its chunk over the split's tiles, four tiles in
+// flight, and the group's lanes are added up once at the end.
 __global__ void __launch_bounds__(256) item_support_kernel(const uint32_t* __restrict__ tids, int m, int TW,
                                                            ChunkGeom geom, int64_t t_first, int64_t t_last,
                                                            unsigned long long* __restrict__ counts) {
     const int64_t nt = t_last - t_first + 1;
     const int64_t ta = t_first + nt * blockIdx.x / gridDim.x;
     const int64_t tb = t_first + nt * (blockIdx.x + 1) / gridDim.x;
-    const int RW = row_words(TW);
+    const int RW = row_words(TW), CH = TW / 4;
     const int64_t tw_words = (int64_t)m * RW;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        unsigned long long acc = 0;
-        for (int64_t t = ta; t < tb; ++t) {
-            const uint4* row = reinterpret_cast<const uint4*>(tids + t * tw_words + (int64_t)i * RW);
-            const bool edge = (t * TW <= geom.g_first) || (t * TW + TW - 1 >= geom.g_last);
-            for (int q = 0; q < TW / 4; ++q) {
-                uint4 v = __ldg(row + q);
-                if (edge) {
-                    int64_t g = t * TW + (int64_t)(q * 4);
-                    v.x &= group_mask(geom, g);
-                    v.y &= group_mask(geom, g + 1);
-                    v.z &= group_mask(geom, g + 2);
-                    v.w &= group_mask(geom, g + 3);
+    const int q = threadIdx.x & (CH - 1), per = blockDim.x / CH;
+    const unsigned gmask = CH == 8 ? 0xFFu << (threadIdx.x & 24) : 0xFu << (threadIdx.x & 28);
+    for (int i0 = 0; i0 < m; i0 += per) {
+        const int i = i0 + (int)threadIdx.x / CH;
+        const bool live = i < m;
+        const uint4* row = reinterpret_cast<const uint4*>(tids + (int64_t)(live ? i : 0) * RW) + q;
+        uint32_t acc = 0;  // <= 128 bits per tile: 2^25 tiles before it could wrap (splits hold far fewer)
+        unsigned long long total = 0;
+        int64_t t = ta;
+        for (; t + 4 <= tb; t += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(row + (t + u) * (tw_words / 4));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t tt = t + u;
+                if ((tt * TW <= geom.g_first) || (tt * TW + TW - 1 >= geom.g_last)) {
+                    const int64_t g = tt * TW + (int64_t)(q * 4);
+                    v[u].x &= group_mask(geom, g);
+                    v[u].y &= group_mask(geom, g + 1);
+                    v[u].z &= group_mask(geom, g + 2);
+                    v[u].w &= group_mask(geom, g + 3);
                 }
-                acc += popc4(v);
+                acc += popc4(v[u]);
+            }
+            if (acc > 0xF0000000u) {
+                total += acc;
+                acc = 0;
             }
         }
-        if (acc) atomicAdd(counts + i, acc);
+        for (; t < tb; ++t) {
+            uint4 v = __ldg(row + t * (tw_words / 4));
+            if ((t * TW <= geom.g_first) || (t * TW + TW - 1 >= geom.g_last)) {
+                const int64_t g = t * TW + (int64_t)(q * 4);
+                v.x &= group_mask(geom, g);
+                v.y &= group_mask(geom, g + 1);
+                v.z &= group_mask(geom, g + 2);
+                v.w &= group_mask(geom, g + 3);
+            }
+            acc += popc4(v);
+        }
+        total += acc;
+        if (!live) total = 0;
+        for (int o = 1; o < CH; o <<= 1) total += __shfl_xor_sync(gmask, total, o);
+        if (q == 0 && live && total) atomicAdd(counts + i, total);
     }
 }
 
@@ -115,7 +144,7 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
     constexpr int R = regs_per_thread(K);
     constexpr int KK = K > 0 ? K : 1;
     constexpr int CH = TW / 4;        // 16-byte chunks per item row
-    constexpr int RB = (TW + 4) * 4;  // row stride in bytes
+    constexpr int RB = row_words(TW) * 4;  // row stride in bytes
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
     constexpr int NT = stream_threads(TW);
@@ -150,8 +179,8 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
         // tiles holding a chunk edge: zero the rows outside [first, last]
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
-            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += NT) {
-                int item = idx / (TW + 4), slot = idx - item * (TW + 4);
+            for (int idx = threadIdx.x; idx < m * row_words(TW); idx += NT) {
+                int item = idx / row_words(TW), slot = idx - item * row_words(TW);
                 if (slot < TW) w[idx] &= group_mask(geom, t * TW + slot);
             }
             __syncthreads();
@@ -170,10 +199,13 @@ __device__ __forceinline__ void stream_unit(const uint32_t* __restrict__ tids, i
             } else {
                 const uint16_t* it = items + (int64_t)off[r][0] * k;
                 for (int q = 0; q < CH; ++q) {
+                    // the lanes of a warp read different rows: each starts at
+                    // another chunk, so they spread over the bank groups
+                    const int qq = (q + (int)threadIdx.x) & (CH - 1);
                     uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
                     for (int j = 0; j < k; ++j) {
                         uint32_t o = (uint32_t)__ldg(it + j) * RB;
-                        v = and4(v, *reinterpret_cast<const uint4*>(base + o + q * 16));
+                        v = and4(v, *reinterpret_cast<const uint4*>(base + o + qq * 16));
                     }
                     cnt[r] += popc4(v);
                 }
@@ -241,7 +273,7 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
                                                const ChunkGeom& geom, const uint16_t* __restrict__ items, int64_t C,
                                                unsigned long long* __restrict__ out, int64_t blk, int64_t t0,
                                                int64_t t1, uint8_t* smem, uint32_t (&uses)[2]) {
-    constexpr int RB = (TW + 4) * 4, R = rl_regs(K, TW), KP = (K + 1) / 2, SUB = TW / 4;
+    constexpr int RB = row_words(TW) * 4, R = rl_regs(K, TW), KP = (K + 1) / 2, SUB = TW / 4;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* bufs = smem + 128;
     const int sub = threadIdx.x & (SUB - 1), slot = threadIdx.x / SUB;
@@ -312,13 +344,18 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         uint8_t* base = bufs + (size_t)s * tb;
         if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
             uint32_t* w = reinterpret_cast<uint32_t*>(base);
-            for (int idx = threadIdx.x; idx < m * (TW + 4); idx += stream_threads(TW)) {
-                int item = idx / (TW + 4), sl = idx - item * (TW + 4);
+            for (int idx = threadIdx.x; idx < m * row_words(TW); idx += stream_threads(TW)) {
+                int item = idx / row_words(TW), sl = idx - item * row_words(TW);
                 if (sl < TW) w[idx] &= group_mask(geom, t * TW + sl);
             }
             __syncthreads();
         }
         const uint8_t* bs = base + sub * 16;
+        // the row stride as an opaque value: item * stride stays an IMAD (the
+        // FMA pipe, idle here) instead of becoming a shift on the ALU pipe the
+        // ANDs saturate (the stride is a power of two since the rows are dense)
+        uint32_t rbv = RB;
+        asm volatile("" : "+r"(rbv));
         // keep the row offsets derived per tile (one IMAD each) instead of
         // letting the compiler hoist R*K of them into registers
 #pragma unroll
@@ -332,14 +369,14 @@ __device__ __forceinline__ void stream_unit_rl(const uint32_t* __restrict__ tids
         for (int r = 0; r < R; ++r) {
             const uint32_t i0 = it[r][0] & 0xFFFFu;
             if (i0 != prev0) {
-                v0 = *reinterpret_cast<const uint4*>(bs + i0 * RB);
+                v0 = *reinterpret_cast<const uint4*>(bs + i0 * rbv);
                 prev0 = i0;
             }
             uint4 v = v0;
 #pragma unroll
             for (int j = 1; j < K; ++j) {
                 const uint32_t item = (j & 1) ? (it[r][j >> 1] >> 16) : (it[r][j >> 1] & 0xFFFFu);
-                v = and4(v, *reinterpret_cast<const uint4*>(bs + item * RB));
+                v = and4(v, *reinterpret_cast<const uint4*>(bs + item * rbv));
             }
             cnt[r] += K <= 4 ? popc4_csa(v) : popc4(v);  // sizes 5+: shared memory binds, not POPC
         }
@@ -477,7 +514,7 @@ __device__ __forceinline__ bool dev_chunk(const DevCountArgs& a, ChunkGeom& geom
 template <int TW>
 __device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const ChunkGeom& geom, int64_t t_first,
                                                 int64_t nt, const int64_t* cpref, int kuse) {
-    constexpr int SUB = TW / 4, RW = TW + 4;
+    constexpr int SUB = TW / 4, RW = row_words(TW);
     const int64_t tile_words = (int64_t)a.m * RW;
     const int lane = threadIdx.x & 31, sub = lane & (SUB - 1);
     const unsigned gmask = ((1u << SUB) - 1u) << (lane & ~(SUB - 1));

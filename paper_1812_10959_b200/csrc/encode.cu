@@ -110,7 +110,7 @@ __global__ void finish_status_kernel(const int64_t* __restrict__ indptr, int64_t
 // rows) and one 64-item word column at a time: warp w transposes groups
 // w, w+8, ... with 64 ballots per group (bit b of lane l's word -> bit l of
 // column b), stages the 64 x TW result in shared memory and writes the 64
-// item rows of the tile (with their zero pad words) with consecutive
+// item rows of the tile with consecutive
 // threads on consecutive words.
 __global__ void __launch_bounds__(256) rows_to_tids_kernel(
     const unsigned long long* __restrict__ rows, int64_t n, int32_t m, int W, int TW,
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) rows_to_tids_kernel(
 // A CTA builds one tile image at a time in shared memory (zeroed, then one
 // warp per row OR-ing the row's bit into each item's group word with a
 // shared-memory atomic — the returned old word flags duplicates), then
-// streams the image (pad words included) to HBM with 16-byte stores.  Tiles
+// streams the image to HBM with 16-byte stores.  Tiles
 // too large for shared memory are built in place with global atomics.
 // Ids are uint16 or int32 (IDX); the first out-of-range id in row-major order
 // is recorded as in encode_csr_kernel.

@@ -64,19 +64,26 @@ constexpr int kPairStages = 3;
 // are not emitted — 6 of 16 and_popc8 per step.  NJ: register columns
 // j >= NJ lie past the last item of a partial B block (nb <= 16 NJ) and are
 // not emitted either (cfg4: the 40-item last block, 15 of 136 block pairs).
-template <bool DIAG, int NJ = 4>
+template <bool DIAG, int CH, int NJ = 4>
 __device__ __forceinline__ void pair_step(const uint8_t* A, const uint8_t* B, int RB, int ta, int tb, int q,
                                           uint32_t (&cnt)[4][4], uint32_t one) {
+    // Item rows are dense (64 or 128 bytes): the 16 lanes of a half-warp read
+    // 16 different A rows, so each walks the row's CH chunks from another
+    // start (a pair's AND may take its row groups in any order): a
+    // quarter-warp then covers 8 distinct bank groups with its A loads and
+    // one contiguous B row segment.
+    const int rot = CH == 8 ? ta : (ta >> 1);
+    const int c0 = ((q + rot) & (CH - 1)) * 16, c1 = ((q + 1 + rot) & (CH - 1)) * 16;
     uint4 av0[4], av1[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16);
-        av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + q * 16 + 16);
+        av0[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + c0);
+        av1[i] = *reinterpret_cast<const uint4*>(A + (ta + 16 * i) * RB + c1);
     }
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-        const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16);
-        const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + q * 16 + 16);
+        const uint4 bv0 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + c0);
+        const uint4 bv1 = *reinterpret_cast<const uint4*>(B + (tb + 16 * j) * RB + c1);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if (DIAG && i > j) continue;
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
         t_first = geom.g_first / TW;
         t_last = geom.g_last / TW;
     }
-    constexpr int RW = TW + 4;
+    constexpr int RW = row_words(TW);
     constexpr int RB = RW * 4;
     constexpr uint32_t BLK = kPairBlock * RB;
     constexpr int NW = kPairThreads / 32;
@@ -245,13 +252,13 @@ __global__ void __launch_bounds__(kPairThreads, MINB) pair_tri_kernel(const uint
         // which balances the ALU (64 lanes/SM/clk) and POPC (16) pipes
         if (diag) {
 #pragma unroll
-            for (int q = 0; q < TW / 4; q += 2) pair_step<true>(A, B, RB, ta, tb, q, cnt, one);
+            for (int q = 0; q < TW / 4; q += 2) pair_step<true, TW / 4>(A, B, RB, ta, tb, q, cnt, one);
         } else if (d.nb <= 48) {
 #pragma unroll
-            for (int q = 0; q < TW / 4; q += 2) pair_step<false, 3>(A, B, RB, ta, tb, q, cnt, one);
+            for (int q = 0; q < TW / 4; q += 2) pair_step<false, TW / 4, 3>(A, B, RB, ta, tb, q, cnt, one);
         } else {
 #pragma unroll
-            for (int q = 0; q < TW / 4; q += 2) pair_step<false>(A, B, RB, ta, tb, q, cnt, one);
+            for (int q = 0; q < TW / 4; q += 2) pair_step<false, TW / 4>(A, B, RB, ta, tb, q, cnt, one);
         }
         // stage s consumed by this warp; the last warp refills it
         __syncwarp();

@@ -483,7 +483,7 @@ static int make_map(CUtensorMap* map, const uint32_t* tids, int L, int64_t tiles
         set_error("pair_tc: cuTensorMapEncodeTiled unavailable");
         return DIC_ECUDA;
     }
-    const int RW = TW + 4;
+    const int RW = row_words(TW);
     cuuint64_t dims[3] = {(cuuint64_t)RW, (cuuint64_t)L, (cuuint64_t)tiles};
     cuuint64_t strides[2] = {(cuuint64_t)RW * 4, (cuuint64_t)L * RW * 4};
     cuuint32_t box[3] = {(cuuint32_t)kTcKW, (cuuint32_t)box_items, 1};

@@ -195,9 +195,8 @@ def test_result_builder_matches_python_construction():
 def header_tids_index(m: int, item: int, g: int) -> int:
     """The tids layout exactly as include/dic_b200.h documents it."""
     TW = 32 if m <= 768 else 16
-    RW = TW + 4
     t = g // TW
-    return t * m * RW + item * RW + (g - t * TW)
+    return t * m * TW + item * TW + (g - t * TW)
 
 
 @pytest.mark.parametrize("m", [1, 64, 128, 700, 768, 769, 1000, 4096])
@@ -213,4 +212,4 @@ def test_tids_layout_matches_header_formula(m):
         assert _abi.call("dic_tids_index", m, item, g) == header_tids_index(m, item, g)
     for n in (1, 31, 32, 33, TW * 32, TW * 32 + 1, 10_000_000):
         groups = -(-n // 32)
-        assert lib.dic_tids_words(n, m) == -(-groups // TW) * m * (TW + 4)
+        assert lib.dic_tids_words(n, m) == -(-groups // TW) * m * TW
