@@ -135,6 +135,11 @@ struct Records {
     int64_t cap = 0;
 };
 
+// L2 load (words other CTAs update during a kernel: the L1 copy may be stale)
+__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
 // Mask view: words of src with bit `add` set and bit `drop` cleared (-1 = none).
 struct MaskView {
     const unsigned long long* src;
@@ -322,7 +327,8 @@ struct CkptArgs {
     unsigned long long* ring;     // host-mapped status ring
     int64_t ring_words;
     unsigned long long* sync;     // [0] grid-barrier arrivals, [1] CTAs out (both zero between launches),
-                                  // [2] CTA 0's verdict of a small stop, tagged with the stop's sequence number
+                                  // [2] CTA 0's verdict of a small stop, tagged with the stop's sequence number,
+                                  // [4 + 1024 p + g] kept entries of CTA g in a grid compaction round of parity p
     int32_t W, KS, kuse_issue, kuse, bound, replay;
 };
 
@@ -572,6 +578,89 @@ __device__ __forceinline__ void compact_bucket(const CkptArgs& a, CkptSmem& sm, 
     }
 }
 
+// P2a, large buckets: the same compaction by the whole grid (the pair bucket
+// leaves its dense phase with ~500k slots to drop: 860 us on one CTA).  A
+// round covers G x S slots: CTA g stages the kept entries of its S slots in
+// shared memory and publishes their number; after a grid barrier every CTA
+// knows its output offset (the kept entries of the rounds before, plus those
+// of the CTAs below it) and writes its staged entries there.  In place and
+// safe: a round's writes end at or before the next round's first slot, and
+// every slot a write can reach was staged before the barrier.
+constexpr int64_t kCoopCompact = 16384;  // bucket fill above which the grid compacts together
+constexpr int kStageBytes = 96 * 1024;   // dynamic shared memory of the checkpoint kernel
+
+__device__ __forceinline__ void coop_compact(const CkptArgs& a, CkptSmem& sm, uint8_t* stage, int k, int64_t n,
+                                             unsigned long long& nbar) {
+    unsigned long long* stat = a.stat;
+    const int64_t G = gridDim.x;
+    const int64_t smax = (kStageBytes / (4 + 2 * k)) & ~(int64_t)(kCkptThreads - 1);
+    const int64_t S = min((((n + G - 1) / G) + kCkptThreads - 1) & ~(int64_t)(kCkptThreads - 1), smax);
+    int32_t* srec = reinterpret_cast<int32_t*>(stage);
+    uint16_t* sit = reinterpret_cast<uint16_t*>(stage + S * 4);
+    const int32_t* keep = a.keep + a.doff[k];
+    int32_t* rec = a.rec_tab[k];
+    uint16_t* items = a.items_tab[k];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t carry = 0;
+    for (int64_t base = 0, round = 0; base < n; base += G * S, ++round) {
+        const int64_t lo = min(n, base + (int64_t)blockIdx.x * S), hi = min(n, lo + S);
+        int cnt = 0;
+        for (int64_t c0 = lo; c0 < hi; c0 += kCkptThreads) {
+            const int64_t c = c0 + threadIdx.x;
+            const bool valid = c < hi;
+            const int kp = valid ? keep[c] : 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, kp);
+            if (lane == 0) sm.wsum[wid] = __popc(bal);
+            __syncthreads();
+            if (wid == 0) {
+                const int v = sm.wsum[lane];
+                int x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                    if (lane >= o) x += y;
+                }
+                sm.wsum[lane] = x - v;  // exclusive
+                if (lane == 31) sm.ctotal = x;
+            }
+            __syncthreads();
+            if (kp) {
+                const int p = cnt + sm.wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+                srec[p] = rec[c];
+                for (int q = 0; q < k; ++q) sit[(int64_t)p * k + q] = items[c * k + q];
+            }
+            cnt += sm.ctotal;
+            __syncthreads();
+        }
+        unsigned long long* ccnt = a.sync + 4 + (round & 1) * 1024;
+        if (threadIdx.x == 0) {
+            ccnt[blockIdx.x] = (unsigned long long)cnt;
+            sm.nrec0 = 0;  // (kept entries of the CTAs below this one)
+            sm.flag = 0;   // (kept entries of the round)
+        }
+        grid_barrier(a.sync, (unsigned long long)G * ++nbar);
+        if (threadIdx.x < G) {
+            const int c = (int)ldv(ccnt + threadIdx.x);
+            if (c) {
+                atomicAdd(&sm.flag, c);
+                if ((int)threadIdx.x < (int)blockIdx.x) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.nrec0),
+                                                                  (unsigned long long)c);
+            }
+        }
+        __syncthreads();
+        const int64_t off = carry + sm.nrec0;
+        for (int i = threadIdx.x; i < cnt; i += kCkptThreads) rec[off + i] = srec[i];
+        for (int j = threadIdx.x; j < cnt * k; j += kCkptThreads) items[off * k + j] = sit[j];
+        carry += sm.flag;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        stat[S_HEAD + 2 * a.KS + k] = (unsigned long long)carry;  // bn[k]
+        stat[S_HEAD + k] = 0;                                     // removed: none left
+        stat[S_HEAD + 3 * a.KS + k] = 0;                          // cflag
+    }
+}
+
 // P2b.  make_candidates (engine.py:320-369): evaluation of the
 // (frontier f, level1 item j) joins, and — in the same pass — the claim of
 // every admitted join in the hash index.
@@ -601,10 +690,6 @@ struct JoinRec {
     int32_t src;   // source record: the candidate is src's itemset + {l}
     uint16_t l, size;
 };
-
-__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
-    return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
 
 __device__ __forceinline__ bool views_same(const MaskView& x, const MaskView& y, int W) {
     unsigned long long d = 0;
@@ -1055,6 +1140,7 @@ constexpr int64_t kSoloJoins = 2048;   // <= 2 joins per thread of one CTA
 
 __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __grid_constant__ CkptArgs a) {
     __shared__ CkptSmem sm;
+    extern __shared__ __align__(16) uint8_t dyn_smem[];  // kStageBytes: coop_compact's staging
     unsigned long long* stat = a.stat;
     // a stop skipped by the overflow recovery: only its (unchanged) status
     if (stat[S_ABORT]) {
@@ -1102,17 +1188,21 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
     const int cta = solo ? 0 : (int)blockIdx.x, nctas = solo ? 1 : (int)gridDim.x;
     const int64_t nfront = (int64_t)ldv(stat + S_NFRONT);
     if (!a.replay) {
+        // the flagged buckets' fills, every one loaded at once (a loop of
+        // dependent-latency loads otherwise) and before any compaction of this
+        // launch changes them: large buckets are compacted by the whole grid
+        // (every CTA must take the same decisions), the others by one CTA each
         const unsigned long long* cflag = stat + S_HEAD + 3 * a.KS;
+        const unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
         const int kc = min(a.kuse_issue, a.KS);
-        if (solo) {
-            // every flag loaded at once (a loop of dependent-latency loads otherwise)
-            if (threadIdx.x < kc) sm.pos[threadIdx.x] = cflag[threadIdx.x] != 0;
-            __syncthreads();
-            for (int k = 1; k < kc; ++k)
-                if (sm.pos[k]) compact_bucket(a, sm, k);
-        } else {
-            for (int k = 1 + cta; k < kc; k += nctas)
-                if (cflag[k]) compact_bucket(a, sm, k);
+        __syncthreads();
+        if (threadIdx.x < kc) sm.bn0[threadIdx.x] = cflag[threadIdx.x] ? (int64_t)bn[threadIdx.x] : 0;
+        __syncthreads();
+        for (int k = 1; k < kc; ++k) {
+            const int64_t n = sm.bn0[k];
+            if (n == 0) continue;
+            if (!solo && n > kCoopCompact) coop_compact(a, sm, dyn_smem, k, n, nbar);
+            else if ((k - 1) % nctas == cta) compact_bucket(a, sm, k);
         }
     }
     int64_t N = 0;
@@ -1795,11 +1885,16 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
         const char* env = getenv("DIC_CKPT_COOP");
         return !(env && atoi(env) == 0);
     }();
+    static bool attr = false;
+    if (!attr) {
+        DIC_CUDA(cudaFuncSetAttribute(checkpoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes));
+        attr = true;
+    }
     if (coop) {
         DIC_CUDA(cudaLaunchCooperativeKernel((const void*)checkpoint_kernel, dim3((unsigned)ckpt_ctas()),
-                                             dim3(kCkptThreads), params, 0, s));
+                                             dim3(kCkptThreads), params, kStageBytes, s));
     } else {
-        checkpoint_kernel<<<ckpt_ctas(), kCkptThreads, 0, s>>>(a);
+        checkpoint_kernel<<<ckpt_ctas(), kCkptThreads, kStageBytes, s>>>(a);
         DIC_CHECK_LAUNCH("checkpoint_kernel");
     }
     ::dic::note_launch();
@@ -2012,7 +2107,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
         (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s)) ||
-        (rc = dalloc(&e->d_sync, 4, e->s))) {
+        (rc = dalloc(&e->d_sync, 4 + 2048, e->s))) {
         delete e;
         return rc;
     }
@@ -2030,7 +2125,7 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
-    cudaMemsetAsync(e->d_sync, 0, 4 * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->d_sync, 0, (4 + 2048) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
     cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
     cudaMemsetAsync(e->d_bcap, 0, KS * sizeof(int64_t), e->s);
