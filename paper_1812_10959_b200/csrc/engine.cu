@@ -407,13 +407,19 @@ __device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int
     const int64_t nth = (int64_t)nctas * blockDim.x;
     const int64_t tid = (int64_t)cta * blockDim.x + threadIdx.x;
     const int64_t iters = (total + nth * B - 1) / (nth * B);  // uniform trip count for the warp votes
+    const int64_t wtid = tid & ~(int64_t)31;  // the warp's first slot of a round
     for (int64_t it = 0; it < iters; ++it) {
+        // a warp with no slot left is done (slots only grow with it and i):
+        // few live slots then cost a few warps' time, not the whole CTA's
+        if (it * B * nth + wtid >= total) break;
         int64_t g[B], c[B];
         int bk[B];
         int32_t r[B];
+        bool wlive[B];  // warp-uniform: some lane of the warp holds a slot
 #pragma unroll
         for (int i = 0; i < B; ++i) {
             g[i] = (it * B + i) * nth + tid;
+            wlive[i] = (it * B + i) * nth + wtid < total;
             bk[i] = 0;
             c[i] = 0;
             r[i] = -1;
@@ -455,6 +461,7 @@ __device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int
         }
 #pragma unroll
         for (int i = 0; i < B; ++i) {
+            if (!wlive[i]) continue;
             bool gone = false;
             if (r[i] >= 0) {
                 // the count buffers are zero again for the next stop's count
@@ -1071,27 +1078,28 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
 // next stop (dead slots >= a quarter), reset the per-stop counters and
 // compute the next stop's delta offsets from the bucket fill.
 // ring == nullptr: reset only (engine seeding).
-__device__ void status_body(unsigned long long* __restrict__ stat, int KS, int kuse,
+// (The status words are read from L2: atomics of this launch updated them there.)
+__device__ void status_body(unsigned long long* stat, int KS, int kuse,
                             unsigned long long* __restrict__ ring, int64_t ring_words, int64_t* __restrict__ doff) {
     __shared__ int64_t sh[1];
     if (ring) {
-        unsigned long long* slot = ring + (int64_t)(stat[S_SEQ] % kRing) * ring_words;
-        for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = stat[i];
+        unsigned long long* slot = ring + (int64_t)(ldv(stat + S_SEQ) % kRing) * ring_words;
+        for (int i = threadIdx.x; i < S_HEAD; i += blockDim.x) slot[i] = ldv(stat + i);
         for (int k = threadIdx.x; k < kuse; k += blockDim.x) {
-            slot[S_HEAD + 3 * k] = stat[S_HEAD + k];
-            slot[S_HEAD + 3 * k + 1] = stat[S_HEAD + KS + k];
-            slot[S_HEAD + 3 * k + 2] = stat[S_HEAD + 2 * KS + k];
+            slot[S_HEAD + 3 * k] = ldv(stat + S_HEAD + k);
+            slot[S_HEAD + 3 * k + 1] = ldv(stat + S_HEAD + KS + k);
+            slot[S_HEAD + 3 * k + 2] = ldv(stat + S_HEAD + 2 * KS + k);
         }
     }
     __syncthreads();
-    if (stat[S_ABORT]) return;
-    if (ring && threadIdx.x == 0) stat[S_SEQ] += 1;
+    if (ldv(stat + S_ABORT)) return;
+    if (ring && threadIdx.x == 0) stat[S_SEQ] = ldv(stat + S_SEQ) + 1;
     for (int i = threadIdx.x; i < S_NREC; i += blockDim.x) stat[i] = 0;
     // per-size words: only sizes <= kuse can be non-zero (a stop's joins are
     // one item larger than its largest live itemset, which is < kuse)
     const int lim = min(min(KS, kDoffMax), kuse + 1);
     for (int k = threadIdx.x; k < lim; k += blockDim.x) {
-        const unsigned long long rem = stat[S_HEAD + k], fill = stat[S_HEAD + 2 * KS + k];
+        const unsigned long long rem = ldv(stat + S_HEAD + k), fill = ldv(stat + S_HEAD + 2 * KS + k);
         stat[S_HEAD + 3 * KS + k] = (rem > 0 && (rem * 4 >= fill || rem == fill)) ? 1ull : 0ull;  // cflag
         stat[S_HEAD + k] = 0;       // removed
         stat[S_HEAD + KS + k] = 0;  // adm
@@ -1106,7 +1114,7 @@ __device__ void status_body(unsigned long long* __restrict__ stat, int KS, int k
         int64_t carry = 0;
         for (int k0 = 0; k0 < use; k0 += 32) {
             const int k = k0 + lane;
-            const int64_t v = k < use ? (int64_t)stat[S_HEAD + 2 * KS + k] : 0;
+            const int64_t v = k < use ? (int64_t)ldv(stat + S_HEAD + 2 * KS + k) : 0;
             int64_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1167,9 +1175,11 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
         if (blockIdx.x == 0) {
             if (threadIdx.x == 0) {
                 sm.flag = (int64_t)ldv(stat + S_NFRONT) * a.pa.L <= kSoloJoins;
-                // release: the apply's writes before the verdict
+                // "join in" is a release (the apply's writes before the verdict);
+                // "done without you" carries no data
                 const unsigned long long v = tag | (sm.flag ? 1ull : 2ull);
-                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sync + 2), "l"(v) : "memory");
+                if (sm.flag) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a.sync + 2), "l"(v) : "memory");
+                else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sync + 2), "l"(v) : "memory");
             }
             __syncthreads();
             solo = sm.flag != 0;
@@ -1249,10 +1259,9 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
         }
         if (threadIdx.x == 0) stat[S_NREC] = ldv(stat + S_NREC) + (unsigned long long)N;
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !solo) {
         a.sync[0] = 0;
         a.sync[1] = 0;
-        __threadfence();  // also drops this SM's L1 copies of the status words (updated by atomics at L2)
     }
     __syncthreads();
     CKPT_STAMP(4);
