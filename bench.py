@@ -659,6 +659,14 @@ def main() -> None:
                        "db_passes": s.db_passes, "candidates_generated": s.candidates_generated,
                        "peak_dashed": s.peak_dashed, "interval_counts": s.interval_counts},
             "step_ms": [round(x, 3) for x in step_ms], "host_loop": trace.native,
+            # the per-stop cost that does not shard: the step minus its count halves (pair triangle +
+            # support count, timed per stop in the instrumented run), i.e. the checkpoint kernel, the
+            # launch gaps, the first pass and the result collection
+            "step_split_ms": {"count_halves": round(tot_ms, 3), "replicated": round(ms - tot_ms, 3),
+                              "stops": len(count_ms),
+                              "projected_8gpu_ms": round(tot_ms / 8 + (ms - tot_ms) + 0.007 * len(count_ms), 3),
+                              "projection": "count/8 + replicated + 7 us per stop for the fused reduction "
+                                            "(not measured: one GPU per call)"},
             "host_phases_ms": {k: round(v, 3) for k, v in trace.phases.items()},
             **({"step_diag": step_diag} if step_diag else {}),
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": launches, "e2e": e2e,
