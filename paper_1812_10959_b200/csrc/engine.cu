@@ -798,10 +798,13 @@ __device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, in
         const int64_t f = t / L, j = t - f * L;
         const int32_t src = a.frontier[f];
         const int l = a.level1[j];
+        // everything the join needs of src in one round of loads (its item
+        // list is only meaningful for ks <= 8, but always addressable)
         const int ks = R.size[src];
+        const uint4 iv = *reinterpret_cast<const uint4*>(R.items + (int64_t)src * 8);
+        const uint64_t hsrc = R.hash[src];
         if (ks <= 7) {
-            // item-list path: src's ascending ids in one 16-byte load
-            const uint4 iv = *reinterpret_cast<const uint4*>(R.items + (int64_t)src * 8);
+            // item-list path: src's ascending ids came in one 16-byte load
             int its[8] = {(int)(iv.x & 0xFFFFu), (int)(iv.x >> 16), (int)(iv.y & 0xFFFFu), (int)(iv.y >> 16),
                           (int)(iv.z & 0xFFFFu), (int)(iv.z >> 16), (int)(iv.w & 0xFFFFu), (int)(iv.w >> 16)};
             bool in = false;
@@ -822,7 +825,7 @@ __device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, in
                 ok = is_box(sb) & is_box(sa);
             }
             if (!ok) continue;
-            const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
+            const uint64_t hc = hsrc ^ zob((uint32_t)l);
             if (!(ks == 2 && prank)) {
                 if (ks <= 4) {
                     // the (up to four) subset probes side by side: their index
@@ -890,7 +893,7 @@ __device__ __forceinline__ void eval_phase(const CkptArgs& a, int64_t nfront, in
             // large itemsets: masks all the way
             const unsigned long long* sm = R.mask + (int64_t)src * W;
             if ((sm[l >> 6] >> (l & 63)) & 1ull) continue;  // cand == base
-            const uint64_t hc = R.hash[src] ^ zob((uint32_t)l);
+            const uint64_t hc = hsrc ^ zob((uint32_t)l);
             const MaskView cand{sm, l, -1};
             bool ok = true;
             for (int w = 0; w < W && ok; ++w) {
@@ -1008,6 +1011,14 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
     // the stop commits only a few)
     for (int64_t e = (int64_t)wid * nctas + cta; e < na; e += warps) {
         const JoinRec je = a.joins[e];
+        // what the commit needs of the source record and the bucket tables,
+        // loaded before the ranking rounds instead of after them
+        const int sz = je.size;
+        const unsigned long long* smk = R.mask + (int64_t)je.src * W;
+        unsigned long long mw = lane < W ? smk[lane] : 0ull;  // (masks of up to 32 words: one load per lane)
+        const int mine = (sz <= 8 && lane < sz - 1) ? (int)R.items[(int64_t)je.src * 8 + lane] : 0x10000;
+        int32_t* const brec = a.rec_tab[sz];
+        uint16_t* const bits = a.items_tab[sz];
         unsigned cnt = 0;
         for (int64_t j0 = lane; j0 < na; j0 += 128) {
             // four keys per lane and round: their loads go out together
@@ -1029,20 +1040,20 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
         cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
         // record nrec0 + rank at bucket slot bn0[sz] + rank - start[sz]; its
         // record id replaces the temporary entry in the hash slot it claimed
-        const int sz = je.size;
         const int64_t r = sm.nrec0 + cnt;
         const int64_t pos = sm.bn0[sz] + ((int64_t)cnt - start[sz]);
-        const unsigned long long* smk = R.mask + (int64_t)je.src * W;
-        for (int w = lane; w < W; w += 32) {
+        if (lane < W) {
+            if (lane == (je.l >> 6)) mw |= 1ull << (je.l & 63);
+            R.mask[r * W + lane] = mw;
+        }
+        for (int w = 32 + lane; w < W; w += 32) {
             unsigned long long x = smk[w];
             if (w == (je.l >> 6)) x |= 1ull << (je.l & 63);
             R.mask[r * W + w] = x;
         }
-        uint16_t* bit = a.items_tab[sz] + pos * sz;
+        uint16_t* bit = bits + pos * sz;
         if (sz <= 8) {
             // the ascending ids: src's list with l merged in; lane q holds item q
-            const uint16_t* si = R.items + (int64_t)je.src * 8;
-            const int mine = lane < sz - 1 ? (int)si[lane] : 0x10000;
             const int p = __popc(__ballot_sync(0xFFFFFFFFu, mine < (int)je.l));
             const int up = __shfl_up_sync(0xFFFFFFFFu, mine, 1);
             const int it = lane < p ? mine : (lane == p ? (int)je.l : up);
@@ -1065,7 +1076,7 @@ __device__ __forceinline__ void commit_phase(const CkptArgs& a, CkptSmem& sm, in
             R.support[r] = 0;
             R.intervals[r] = 0;
             R.shape[r] = DASHED_CIRCLE;
-            a.rec_tab[sz][pos] = (int32_t)r;
+            brec[pos] = (int32_t)r;
             a.ht[je.slot] = hent(je.hash, (int32_t)r);
         }
     }
