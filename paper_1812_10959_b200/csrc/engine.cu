@@ -1208,27 +1208,32 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
         }
     }
     const int cta = solo ? 0 : (int)blockIdx.x, nctas = solo ? 1 : (int)gridDim.x;
-    const int64_t nfront = (int64_t)ldv(stat + S_NFRONT);
-    if (!a.replay) {
-        // the flagged buckets' fills, every one loaded at once (a loop of
-        // dependent-latency loads otherwise) and before any compaction of this
-        // launch changes them: large buckets are compacted by the whole grid
-        // (every CTA must take the same decisions), the others by one CTA each
+    // The frontier size and the flagged buckets' fills in ONE round of loads (a
+    // loop of dependent-latency loads otherwise), before any compaction of this
+    // launch changes the fills: large buckets are compacted by the whole grid
+    // (every CTA must take the same decisions), the others by one CTA each.
+    const int kc = a.replay ? 0 : min(a.kuse_issue, a.KS);
+    __syncthreads();
+    if ((int)threadIdx.x < kc) {
         const unsigned long long* cflag = stat + S_HEAD + 3 * a.KS;
         const unsigned long long* bn = stat + S_HEAD + 2 * a.KS;
-        const int kc = min(a.kuse_issue, a.KS);
-        __syncthreads();
-        if (threadIdx.x < kc) sm.bn0[threadIdx.x] = cflag[threadIdx.x] ? (int64_t)bn[threadIdx.x] : 0;
-        __syncthreads();
-        for (int k = 1; k < kc; ++k) {
-            const int64_t n = sm.bn0[k];
-            if (n == 0) continue;
-            if (!solo && n > kCoopCompact) coop_compact(a, sm, dyn_smem, k, n, nbar);
-            else if ((k - 1) % nctas == cta) compact_bucket(a, sm, k);
-        }
+        // flag and fill loaded side by side
+        const unsigned long long fl = cflag[threadIdx.x], fill = bn[threadIdx.x];
+        sm.bn0[threadIdx.x] = fl ? (int64_t)fill : 0;
+    } else if (threadIdx.x == kCkptThreads - 1) {
+        sm.nrec0 = (int64_t)ldv(stat + S_NFRONT);
+    }
+    __syncthreads();
+    const int64_t nfront = sm.nrec0;
+    for (int k = 1; k < kc; ++k) {
+        const int64_t n = sm.bn0[k];
+        if (n == 0) continue;
+        if (!solo && n > kCoopCompact) coop_compact(a, sm, dyn_smem, k, n, nbar);
+        else if ((k - 1) % nctas == cta) compact_bucket(a, sm, k);
     }
     int64_t N = 0;
     if (nfront > 0) {
+        CKPT_STAMP(11);
         eval_phase(a, nfront, cta, nctas);
         CKPT_STAMP(7);
 #ifdef DIC_LAB_TIMING

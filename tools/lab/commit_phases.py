@@ -46,7 +46,7 @@ def main() -> None:
             modes[int(r[6])] += 1
         if s % 10 == 0 or s in (101, 102, 103, 104, 105):
             extra = " ".join(f"{n}={x:.1f}" for n, x in zip(names[3:], tail)) + f" mode={r[6]}" if tail is not None else ""
-            ev = (f"(eval cta0 {(r[7] - r[1]) / 1e3:.1f}, last cta {(r[9] - r[1]) / 1e3:.1f}, {r[10]} claims, "
+            ev = (f"(pre-eval {(r[11] - r[1]) / 1e3:.1f}, eval cta0 {(r[7] - r[11]) / 1e3:.1f}, last cta {(r[9] - r[1]) / 1e3:.1f}, {r[10]} claims, "
                   f"slowest {r[8] / 1e3:.1f})") if a[s][7] > r[1] else ""
             print(s, " ".join(f"{n}={x:.1f}" for n, x in zip(names, d)), ev, extra, f"sum={d.sum():.1f} us")
     print("totals ms:", " ".join(f"{n}={x / 1e3:.2f}" for n, x in zip(names, tot)), f"sum={tot.sum() / 1e3:.2f}",
