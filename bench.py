@@ -51,7 +51,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-bench", action="store_true")
     ap.add_argument("--no-config-sweep", action="store_true", help="skip the cfg1-3 GPU vs CPU-oracle sweep")
-    ap.add_argument("--clock-ms", type=int, default=500, help="nvidia-smi sampling period in the timed region")
+    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period in the timed region")
     ap.add_argument("--profile", action="store_true", help="one short run for ncu (no JSON contract)")
     ap.add_argument("--step-trace", action="store_true", help="per-step host phase / loop diagnostics in the JSON")
     return ap.parse_args()
