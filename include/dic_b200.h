@@ -293,6 +293,8 @@ typedef struct dic_run_stats {
     double issue_us;     /* host time spent enqueuing stops (diagnostic)       */
     double poll_us;      /* host time spent waiting for / reading statuses     */
     int64_t graphs_captured;  /* stop graphs (re-)captured during the run        */
+    int64_t batches;          /* launches that ran several quiet stops at once   */
+    int64_t batched_stops;    /* stops run by those launches                     */
 } dic_run_stats;
 int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_t* llast,
                    const int64_t* rows, int64_t stop_max, int32_t depth,

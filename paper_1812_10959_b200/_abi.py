@@ -48,6 +48,8 @@ class RunStats(C.Structure):
         ("issue_us", dbl),
         ("poll_us", dbl),
         ("graphs_captured", i64),
+        ("batches", i64),
+        ("batched_stops", i64),
     ]
 
 

@@ -487,7 +487,15 @@ struct DevCountArgs {
     const unsigned long long* seq;
     int32_t ring;
     int64_t small_max;  // at most this many sparse candidates: the unstaged path
+    // batch of quiet stops (engine): the next `batch` chunks of the stop
+    // counter are counted in one launch, chunk b into delta + b * batch_stride
+    // (refused — nothing counted — unless the live slots fit a block and no
+    // bucket is dense: the batch checkpoint kernel applies the same test)
+    int32_t batch;
+    int64_t batch_stride;
 };
+
+constexpr int kCountBatchMax = 8;
 
 // The chunk geometry of this launch (host-given, or read from the ring).
 __device__ __forceinline__ bool dev_chunk(const DevCountArgs& a, ChunkGeom& geom, int64_t& t_first,
@@ -512,8 +520,8 @@ __device__ __forceinline__ bool dev_chunk(const DevCountArgs& a, ChunkGeom& geom
 // contiguous row segment per lane group; the chunk is L2-resident), AND them,
 // and popcount; partial counts are reduced over the group once.
 template <int TW>
-__device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const ChunkGeom& geom, int64_t t_first,
-                                                int64_t nt, const int64_t* cpref, int kuse) {
+__device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const ChunkGeom* geoms, int nb,
+                                                int64_t nt_max, const int64_t* cpref, int kuse) {
     constexpr int SUB = TW / 4, RW = row_words(TW);
     const int64_t tile_words = (int64_t)a.m * RW;
     const int lane = threadIdx.x & 31, sub = lane & (SUB - 1);
@@ -521,33 +529,55 @@ __device__ __forceinline__ void count_dev_small(const DevCountArgs& a, const Chu
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SUB;
     const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / SUB;
     const int64_t Ctot = cpref[kuse];
-    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(nt, ngroups / std::max<int64_t>(Ctot, 1)));
-    const int64_t W = Ctot * rs;
+    // work item = (chunk b, candidate, row split): every chunk of a batch in one pass
+    const int64_t rs =
+        std::max<int64_t>(1, std::min<int64_t>(nt_max, ngroups / std::max<int64_t>(Ctot * nb, 1)));
+    const int64_t W = Ctot * rs * nb;
     for (int64_t w = gid; w < W; w += ngroups) {
-        const int64_t cg = w / rs, r = w - cg * rs;
+        const int64_t b = w / (Ctot * rs), w1 = w - b * Ctot * rs;
+        const int64_t cg = w1 / rs, r = w1 - cg * rs;
+        const ChunkGeom geom = geoms[b];
+        if (geom.g_last < geom.g_first) continue;  // (an empty chunk)
+        const int64_t t_first = geom.g_first / TW, nt = geom.g_last / TW - t_first + 1;
         int k = 1;
         while (cpref[k + 1] <= cg) ++k;
         const int64_t c = cg - cpref[k];
         const uint16_t* it = a.items_tab[k] + c * k;
         const int64_t t0 = t_first + nt * r / rs, t1 = t_first + nt * (r + 1) / rs;
         uint32_t cnt = 0;
-        for (int64_t t = t0; t < t1; ++t) {
-            const uint32_t* base = a.tids + t * tile_words + sub * 4;
-            uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)__ldg(it) * RW));
-            for (int j = 1; j < k; ++j)
-                v = and4(v, __ldg(reinterpret_cast<const uint4*>(base + (int64_t)__ldg(it + j) * RW)));
-            if (t * TW <= geom.g_first || t * TW + TW - 1 >= geom.g_last) {
-                const int64_t g = t * TW + sub * 4;
-                v.x &= group_mask(geom, g);
-                v.y &= group_mask(geom, g + 1);
-                v.z &= group_mask(geom, g + 2);
-                v.w &= group_mask(geom, g + 3);
+        // four tiles per round: the item rows of all four are requested before
+        // any is used (the loop is bound by L2 latency, not by its few ANDs)
+        for (int64_t t = t0; t < t1; t += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+            for (int j = 0; j < k; ++j) {
+                const int64_t row = (int64_t)__ldg(it + j) * RW + sub * 4;
+                uint4 x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    x[u] = t + u < t1 ? __ldg(reinterpret_cast<const uint4*>(a.tids + (t + u) * tile_words + row))
+                                      : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = and4(v[u], x[u]);
             }
-            cnt += popc4(v);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t tt = t + u;
+                if (tt < t1 && (tt * TW <= geom.g_first || tt * TW + TW - 1 >= geom.g_last)) {
+                    const int64_t g = tt * TW + sub * 4;
+                    v[u].x &= group_mask(geom, g);
+                    v[u].y &= group_mask(geom, g + 1);
+                    v[u].z &= group_mask(geom, g + 2);
+                    v[u].w &= group_mask(geom, g + 3);
+                }
+                cnt += popc4(v[u]);
+            }
         }
 #pragma unroll
         for (int o = 1; o < SUB; o <<= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
-        if (sub == 0 && cnt) atomicAdd(a.delta + a.doff[k] + c, (unsigned long long)cnt);
+        if (sub == 0 && cnt)
+            atomicAdd(a.delta + b * a.batch_stride + a.doff[k] + c, (unsigned long long)cnt);
     }
 }
 
@@ -557,10 +587,27 @@ __global__ void __launch_bounds__(stream_threads(TW), 1) count_dev_kernel(const 
     __shared__ int64_t upref[kDevMaxK + 1];  // units before bucket k
     __shared__ int64_t cpref[kDevMaxK + 1];  // candidates before bucket k
     __shared__ int32_t srs[kDevMaxK];        // row splits of bucket k's blocks
+    __shared__ ChunkGeom sgeom[kCountBatchMax];
     if (*a.abort) return;
     ChunkGeom geom;
     int64_t t_first, t_last;
-    if (!dev_chunk(a, geom, t_first, t_last)) return;
+    if (a.batch > 1) {
+        // a batch of stops: chunk b is the schedule slot of stop counter + b
+        if (a.doff[a.kuse] > a.batch_stride) return;
+        if ((int)threadIdx.x < a.batch) {
+            const int64_t sl = (int64_t)((*a.seq + threadIdx.x) % (unsigned long long)a.ring);
+            const int64_t f = a.chunk_ring[2 * sl], l = a.chunk_ring[2 * sl + 1];
+            ChunkGeom g = chunk_geom(0, 0);
+            g.g_first = 1;
+            g.g_last = 0;  // empty
+            if (l >= f) g = chunk_geom(f, l);
+            sgeom[threadIdx.x] = g;
+        }
+        geom = chunk_geom(0, 0);
+        t_first = t_last = 0;
+    } else if (!dev_chunk(a, geom, t_first, t_last)) {
+        return;
+    }
     const int64_t nt = t_last - t_first + 1;
     // bucket fills loaded in parallel (a loop of dependent-latency loads in
     // one thread would cost one L2 round trip per size)
@@ -614,8 +661,18 @@ __global__ void __launch_bounds__(stream_threads(TW), 1) count_dev_kernel(const 
     __syncthreads();
     const int64_t U = upref[a.kuse];
     if (U == 0) return;
+    if (a.batch > 1) {
+        // (the engine batches stops only after the pair bucket left its dense phase for good)
+        int64_t nt_max = 1;
+        for (int b = 0; b < a.batch; ++b)
+            nt_max = max(nt_max, sgeom[b].g_last / TW - sgeom[b].g_first / TW + 1);
+        count_dev_small<TW>(a, sgeom, a.batch, nt_max, cpref, a.kuse);
+        return;
+    }
     if (cpref[a.kuse] <= a.small_max) {
-        count_dev_small<TW>(a, geom, t_first, nt, cpref, a.kuse);
+        sgeom[0] = geom;
+        __syncthreads();
+        count_dev_small<TW>(a, sgeom, 1, nt, cpref, a.kuse);
         return;
     }
     if ((int64_t)blockIdx.x >= U) return;
@@ -803,8 +860,10 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
                      uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
                      unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
                      cudaStream_t s, const int64_t* chunk_ring = nullptr, const unsigned long long* seq = nullptr,
-                     int ring = 0) {
+                     int ring = 0, int batch = 1, int64_t batch_stride = 0) {
     if (!chunk_ring && last < first) return DIC_OK;
+    DIC_REQUIRE(batch >= 1 && batch <= kCountBatchMax && (batch == 1 || (chunk_ring && batch_stride > 0)),
+                "count_dev_launch: bad batch");
     DevCountArgs a;
     memset(&a, 0, sizeof(a));
     a.tids = tids;
@@ -824,6 +883,8 @@ int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int6
     a.chunk_ring = chunk_ring;
     a.seq = seq;
     a.ring = ring;
+    a.batch = batch;
+    a.batch_stride = batch_stride;
     static int64_t small_max = -1;
     if (small_max < 0) {
         const char* e = getenv("DIC_COUNT_SMALL_MAX");

@@ -58,7 +58,8 @@ constexpr int kFusedMaxPeers = 72;  // LSA team size it supports (one NVLink dom
 int count_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last, int kuse,
                      uint16_t* const* items_tab, const unsigned long long* bn, const int64_t* doff,
                      unsigned long long* delta, const unsigned long long* abort_flag, int64_t tri_len,
-                     cudaStream_t s, const int64_t* chunk_ring, const unsigned long long* seq, int ring);
+                     cudaStream_t s, const int64_t* chunk_ring, const unsigned long long* seq, int ring,
+                     int batch = 1, int64_t batch_stride = 0);
 int item_support_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
                         unsigned long long* counts, cudaStream_t s);
 int count_pairs_dev_launch(const uint32_t* tids, int64_t n, int m, int64_t first, int64_t last,
@@ -388,7 +389,8 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned l
 // pending) are only marked not-kept.  keep[g] = still dashed.  A thread takes
 // four slots at a time and issues each level of their dependent loads
 // (record id -> record fields and count) together.
-__device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int cta, int nctas) {
+__device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int cta, int nctas,
+                                            unsigned long long* delta) {
     unsigned long long* stat = a.stat;
     const int kuse = a.kuse_issue;
     const Records& R = a.R;
@@ -444,7 +446,7 @@ __device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int
                 iv[i] = R.intervals[r[i]];
                 if (!(bk[i] == 2 && dense)) {
                     // (dense pairs are counted into the triangle: their delta slots stay zero)
-                    dg[i] = (int64_t)a.delta[g[i]];
+                    dg[i] = (int64_t)delta[g[i]];
                 } else {
                     // until the bucket is first compacted, slot c still holds the
                     // seeded pair c (record rec0 + c, triangle slot c): no item /
@@ -467,7 +469,7 @@ __device__ __forceinline__ void apply_phase(const CkptArgs& a, CkptSmem& sm, int
                 // the count buffers are zero again for the next stop's count
                 if (dg[i]) {
                     if (tp[i] >= 0) a.pa.tri[tp[i]] = 0;
-                    else a.delta[g[i]] = 0;
+                    else delta[g[i]] = 0;
                 }
                 uint8_t s = sh[i];
                 bool kept = false;
@@ -1175,10 +1177,10 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
     CKPT_STAMP(0);
     if (!a.replay) {
         if (!small) {
-            apply_phase(a, sm, blockIdx.x, gridDim.x);
+            apply_phase(a, sm, blockIdx.x, gridDim.x, a.delta);
             grid_barrier(a.sync, G * ++nbar);
         } else if (blockIdx.x == 0) {
-            apply_phase(a, sm, 0, 1);
+            apply_phase(a, sm, 0, 1, a.delta);
             __syncthreads();
         }
     }
@@ -1294,6 +1296,73 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
         g_lab_commit[lab_seq % 512][6] = (unsigned long long)(small ? (solo ? 2 : 1) : 0);
     }
 #endif
+}
+
+// The quiet tail of a run — a few hundred live itemsets or fewer, most stops
+// without a promotion — costs a launch gap, a count kernel and a checkpoint
+// kernel per stop for microseconds of work.  dic_engine_run therefore issues
+// such stops in BATCHES: one count launch fills a delta block per chunk for the
+// next `nstops` chunks (count.cu, DevCountArgs::batch), and this kernel — one
+// CTA, CTA-level barriers only — runs their checkpoints one after the other.
+// The counts of the later chunks hold only while the dashed vector keeps its
+// slots: nothing is compacted inside a batch (flagged buckets keep their dead
+// slots until the next single stop; the blocks are small), and the batch ends
+// after a stop that inserted candidates (they were not counted in the later
+// chunks) or that overflowed; the stops not run leave no status, and the host
+// issues them again.
+constexpr int64_t kBatchSlots = 2048;  // live slots of a batched stop (one delta block)
+constexpr int kBatchStops = 8;
+
+__global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_batch_kernel(const __grid_constant__ CkptArgs a,
+                                                                       int nstops, unsigned long long* bdelta) {
+    __shared__ CkptSmem sm;
+    unsigned long long* stat = a.stat;
+    const int64_t total0 = a.doff[a.kuse_issue];
+    if (stat[S_ABORT] || total0 > kBatchSlots) {
+        // skipped by the overflow recovery (its unchanged status), or refused:
+        // the count launch made the same test and counted nothing
+        if (stat[S_ABORT]) status_body(stat, a.KS, a.kuse, a.ring, a.ring_words, a.doff);
+        return;
+    }
+    int b = 0;
+    for (; b < nstops; ++b) {
+        apply_phase(a, sm, 0, 1, bdelta + (int64_t)b * kBatchSlots);
+        __syncthreads();
+        const int64_t nfront = (int64_t)ldv(stat + S_NFRONT);
+        int64_t N = 0;
+        bool over = false;
+        if (nfront > 0) {
+            eval_phase(a, nfront, 0, 1);
+            __syncthreads();
+            over = capacity_over(a, sm);
+            if (!over) {
+                N = (int64_t)ldv(stat + S_NINS);
+                if (N > 0) commit_phase(a, sm, (int64_t)ldv(stat + S_NADM), 0, 1);
+            }
+        }
+        __syncthreads();
+        if (N > 0) {
+            unsigned long long* bnw = stat + S_HEAD + 2 * a.KS;
+            const int top = a.kuse < kDoffMax ? a.kuse : kDoffMax;
+            for (int k = threadIdx.x; k < top; k += blockDim.x) {
+                const unsigned long long n = ldv(stat + S_HEAD + a.KS + k);  // adm[k]
+                if (n) bnw[k] = ldv(bnw + k) + n;
+            }
+            if (threadIdx.x == 0) stat[S_NREC] = ldv(stat + S_NREC) + (unsigned long long)N;
+        }
+        __syncthreads();
+        status_body(stat, a.KS, a.kuse, a.ring, a.ring_words, a.doff);
+        __syncthreads();
+        // may the next chunk's counts be applied to the same slots?
+        if (over || N > 0) {  // (uniform)
+            ++b;
+            break;
+        }
+    }
+    // the delta blocks of the stops not run go back to zero (a run stop's block
+    // was re-zeroed by its apply)
+    for (int64_t i = (int64_t)b * kBatchSlots + threadIdx.x; i < (int64_t)nstops * kBatchSlots; i += blockDim.x)
+        if ((i % kBatchSlots) < total0) bdelta[i] = 0;
 }
 
 struct TableUpdate {
@@ -1437,7 +1506,7 @@ struct HostRes {
     cudaStream_t cap = nullptr;
     uint8_t* stage = nullptr;  // pinned staging for the result copies (grown on demand)
     size_t stage_bytes = 0;
-    cudaGraphExec_t gx[3] = {nullptr, nullptr, nullptr};  // stop graphs, updated in place by the next engine
+    cudaGraphExec_t gx[4] = {nullptr, nullptr, nullptr, nullptr};  // stop graphs, updated in place by the next engine
 };
 
 struct dic_engine {
@@ -1511,6 +1580,14 @@ struct dic_engine {
     GraphKey key_stop{};
     int64_t graphs_captured = 0, graph_launches = 0;
     bool count_graphed = false;          // the pending count went through the graph
+
+    // batches of quiet stops (dic_engine_run): kBatchStops delta blocks of kBatchSlots
+    unsigned long long* bdelta = nullptr;
+    cudaGraphExec_t gx_batch = nullptr;
+    long long nk_batch = 0;
+    GraphKey key_batch{};
+    int gx_batch_n = 0;
+    bool status_ready = false;  // dic_engine_poll: the stop's status is already on the host (batches)
 
     int32_t* res_ids = nullptr;          // result collection (dic_engine_num_frequent)
     int64_t res_cap = 0, res_F = -1;
@@ -1874,7 +1951,7 @@ static int ckpt_ctas() {
 // finalize over every slot, compaction of the flagged buckets,
 // make_candidates (device-sized, all-or-nothing), status.  replay: the
 // candidate step alone (overflow recovery).
-int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
+CkptArgs checkpoint_args(dic_engine* e, bool replay) {
     CkptArgs a;
     memset(&a, 0, sizeof(a));
     a.rec_tab = e->d_brec;
@@ -1906,6 +1983,11 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
     a.kuse = e->kuse;
     a.bound = e->bound;
     a.replay = replay ? 1 : 0;
+    return a;
+}
+
+int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
+    CkptArgs a = checkpoint_args(e, replay);
     void* params[] = {&a};
     static const bool coop = [] {
         const char* env = getenv("DIC_CKPT_COOP");
@@ -1924,6 +2006,23 @@ int launch_checkpoint(dic_engine* e, cudaStream_t s, bool replay = false) {
         DIC_CHECK_LAUNCH("checkpoint_kernel");
     }
     ::dic::note_launch();
+    return DIC_OK;
+}
+
+// A batch of quiet stops (checkpoint_batch_kernel): one count launch over the
+// next n chunks into the batch's delta blocks, then their checkpoints on one CTA.
+int launch_batch(dic_engine* e, int n, cudaStream_t s) {
+    const unsigned long long* bn = e->d_stat + S_HEAD + 2 * e->KS;
+    int rc;
+    if ((rc = count_dev_launch(e->tids, e->n_local, e->m, 0, e->n_local > 0 ? e->n_local - 1 : 0, e->kuse_issue,
+                               e->d_bitems, bn, e->d_doff, e->bdelta, e->d_stat + S_ABORT,
+                               e->tri ? e->tri_len : 0, s, e->d_sched, e->d_stat + S_SEQ, (int)e->nsched, n,
+                               kBatchSlots)))
+        return rc;
+    const CkptArgs a = checkpoint_args(e, false);
+    checkpoint_batch_kernel<<<1, kCkptThreads, 0, s>>>(a, n, e->bdelta);
+    ::dic::note_launch();
+    DIC_CHECK_LAUNCH("checkpoint_batch_kernel");
     return DIC_OK;
 }
 
@@ -2133,7 +2232,8 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     if ((rc = dalloc(&e->d_brec, KS, e->s)) || (rc = dalloc(&e->d_bitems, KS, e->s)) ||
         (rc = dalloc(&e->d_bcap, KS, e->s)) || (rc = dalloc(&e->d_doff, KS + 1, e->s)) ||
         (rc = dalloc(&e->d_stat, e->ring_words + KS, e->s)) || (rc = dalloc(&e->level1, m, e->s)) ||
-        (rc = dalloc(&e->d_sync, 4 + 2048, e->s))) {
+        (rc = dalloc(&e->d_sync, 4 + 2048, e->s)) ||
+        (rc = dalloc(&e->bdelta, (int64_t)kBatchStops * kBatchSlots, e->s))) {
         delete e;
         return rc;
     }
@@ -2148,10 +2248,12 @@ extern "C" int dic_engine_create(const uint32_t* tids, int64_t n_local, int32_t 
     e->gx_count = e->hres.gx[0];  // stale until the first capture updates them
     e->gx_ckpt = e->hres.gx[1];
     e->gx_stop = e->hres.gx[2];
-    e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = nullptr;
+    e->gx_batch = e->hres.gx[3];
+    e->hres.gx[0] = e->hres.gx[1] = e->hres.gx[2] = e->hres.gx[3] = nullptr;
     for (int i = 0; i < kRing; ++i) e->kuse_at[i] = 0;
     cudaMemsetAsync(e->d_stat, 0, (e->ring_words + KS) * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_sync, 0, (4 + 2048) * sizeof(unsigned long long), e->s);
+    cudaMemsetAsync(e->bdelta, 0, (size_t)kBatchStops * kBatchSlots * sizeof(unsigned long long), e->s);
     cudaMemsetAsync(e->d_brec, 0, KS * sizeof(int32_t*), e->s);
     cudaMemsetAsync(e->d_bitems, 0, KS * sizeof(uint16_t*), e->s);
     cudaMemsetAsync(e->d_bcap, 0, KS * sizeof(int64_t), e->s);
@@ -2172,7 +2274,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     dfree(e->level1, s); dfree(e->frontier, s); dfree(e->keep, s);
     if (!e->fused) dfree(e->delta, s);
     dfree(e->d_sched, s);
-    dfree(e->joins, s); dfree(e->d_sync, s);
+    dfree(e->joins, s); dfree(e->d_sync, s); dfree(e->bdelta, s);
     dfree(e->pair_tids_own, s); dfree(e->rank, s); dfree(e->res_ids, s);
     if (!e->fused) dfree(e->tri, s);
     if (e->fused) {
@@ -2184,6 +2286,7 @@ extern "C" int dic_engine_destroy(dic_engine* e) {
     e->hres.gx[0] = e->gx_count;  // pooled with the host resources
     e->hres.gx[1] = e->gx_ckpt;
     e->hres.gx[2] = e->gx_stop;
+    e->hres.gx[3] = e->gx_batch;
     release_host_res(e->hres);  // the stream was synchronised above: no stop reads the ring any more
     delete e;
     return DIC_OK;
@@ -2549,7 +2652,7 @@ extern "C" int dic_engine_poll(dic_engine* e, int64_t seq, dic_stop_status* st, 
     const int KS = e->KS;
     const size_t u = sizeof(unsigned long long);
     const int slot = (int)(seq % kRing);
-    DIC_CUDA(cudaEventSynchronize(e->ev[slot]));
+    if (!e->status_ready) DIC_CUDA(cudaEventSynchronize(e->ev[slot]));
     unsigned long long* h = e->ring + (int64_t)slot * e->ring_words;
     int ku = e->kuse_at[slot];
     *replayed = 0;
@@ -2676,9 +2779,92 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     auto us_since = [](clk::time_point t) {
         return std::chrono::duration<double, std::micro>(clk::now() - t).count();
     };
+    // one stop's status into the run's totals; returns false once the run is over
+    auto account = [&](const Flight& f, const dic_stop_status& st, int32_t replayed) {
+        out->replays += replayed;
+        const int64_t i = out->stops;
+        if (i < max_stops) {
+            if (timed) cudaEventElapsedTime(&count_ms[i], t0[f.seq % kRing], t1[f.seq % kRing]);
+            if (dashed) dashed[i] = st.dashed_at_start;
+        }
+        out->stops++;
+        out->interval_counts += st.dashed_at_start;
+        out->scanned += rows[f.stop - 1];
+        out->candidates_generated += st.inserted;
+        out->candidates_pruned += st.pruned;
+        out->peak_dashed = std::max<int64_t>(out->peak_dashed, st.dashed_peak);
+        if (st.dashed_at_end == 0) done = true;
+    };
+    // Batches of quiet stops (checkpoint_batch_kernel): with the pipeline
+    // drained the host knows the dashed vector exactly; once it is small and
+    // the pair bucket has left its dense phase, the next stops go out
+    // kBatchStops at a time (DIC_BATCH_STOPS: 0 or 1 disables).
+    int batch_n = kBatchStops;
+    {
+        const char* env = getenv("DIC_BATCH_STOPS");
+        if (env && *env) batch_n = std::max(0, std::min(atoi(env), (int)kBatchStops));
+    }
+    const bool batch_ok = e->in_run && !e->comm && depth > 1 && batch_n > 1 && stop_max == e->nsched;
+    // (as of the last polled stop; exact once nothing is in flight)
+    auto batch_wanted = [&]() {
+        if (!batch_ok || done || e->live <= 0 || e->live > kBatchSlots / 2) return false;
+        if (e->tri && e->tri_live) return false;
+        int64_t fill = 0;
+        for (const Bucket& b : e->buckets) fill += b.n;
+        return fill <= kBatchSlots;
+    };
     while (rc == DIC_OK) {
+        if (inflight.empty() && batch_wanted()) {
+            const clk::time_point tb = clk::now();
+            e->kuse_issue = e->kuse;
+            const GraphKey k = graph_key(e, true);
+            if (!e->gx_batch || e->gx_batch_n != batch_n || !(k == e->key_batch)) {
+                if ((rc = capture_graph(e, &e->gx_batch, &e->nk_batch,
+                                        [&](cudaStream_t cs) { return launch_batch(e, batch_n, cs); })))
+                    break;
+                e->key_batch = k;
+                e->gx_batch_n = batch_n;
+            }
+            // the batch's ring slots must not pass for written (the pooled ring
+            // keeps the statuses of earlier runs; nothing is in flight now)
+            for (int i = 0; i < batch_n; ++i)
+                e->ring[(int64_t)((e->issued + i) % kRing) * e->ring_words + S_SEQ] = ~0ull;
+            if ((rc = launch_graph(e, e->gx_batch, e->nk_batch))) break;
+            out->issue_us += us_since(tb);
+            const clk::time_point tp = clk::now();
+            DIC_CUDA(cudaStreamSynchronize(e->s));
+            ++out->batches;
+            for (int i = 0; i < batch_n && rc == DIC_OK && !done; ++i) {
+                // the stops of the batch that ran left their status in the ring
+                const int64_t seq = e->issued;
+                const int slot = (int)(seq % kRing);
+                const unsigned long long* h = e->ring + (int64_t)slot * e->ring_words;
+                if (h[S_SEQ] != (unsigned long long)seq) {
+                    if (i == 0) {
+                        set_error("dic_engine_run: a batch of stops left no status");
+                        rc = DIC_ESTATE;
+                    }
+                    break;  // the batch ended before this stop: it is issued again
+                }
+                e->kuse_at[slot] = e->kuse;
+                ++e->issued;
+                stop = stop < stop_max ? stop + 1 : 1;
+                dic_stop_status st;
+                int32_t replayed = 0;
+                e->status_ready = true;  // (the stream is idle: no event to wait for)
+                rc = dic_engine_poll(e, seq, &st, &replayed);
+                e->status_ready = false;
+                if (rc) break;
+                ++out->batched_stops;
+                account(Flight{seq, stop}, st, replayed);
+                if (replayed) break;  // (the batch ended at this stop: it overflowed)
+            }
+            out->poll_us += us_since(tp);
+            continue;
+        }
         const clk::time_point ti = clk::now();
-        while (!done && (int64_t)inflight.size() < depth) {
+        // (no new single stops once a batch is wanted: the pipeline drains first)
+        while (!done && (int64_t)inflight.size() < depth && !batch_wanted()) {
             stop = stop < stop_max ? stop + 1 : 1;
             const int slot = (int)(e->issued % kRing);
             if (timed) cudaEventRecord(t0[slot], e->s);
@@ -2697,24 +2883,15 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
         const clk::time_point tp = clk::now();
         if ((rc = dic_engine_poll(e, f.seq, &st, &replayed))) break;
         out->poll_us += us_since(tp);
-        out->replays += replayed;
-        if (done) continue;  // a no-op stop issued after the last live one
-        const int64_t i = out->stops;
-        if (i < max_stops) {
-            if (timed) cudaEventElapsedTime(&count_ms[i], t0[f.seq % kRing], t1[f.seq % kRing]);
-            if (dashed) dashed[i] = st.dashed_at_start;
+        if (done) {  // a no-op stop issued after the last live one
+            out->replays += replayed;
+            continue;
         }
-        out->stops++;
-        out->interval_counts += st.dashed_at_start;
-        out->scanned += rows[f.stop - 1];
-        out->candidates_generated += st.inserted;
-        out->candidates_pruned += st.pruned;
-        out->peak_dashed = std::max<int64_t>(out->peak_dashed, st.dashed_peak);
+        account(f, st, replayed);
         if (replayed) {  // stops after f.seq were skipped on the device: re-issue them
             inflight.clear();
             stop = f.stop;
         }
-        if (st.dashed_at_end == 0) done = true;
     }
     out->graphs_captured = e->graphs_captured - captured0;
     e->in_run = false;

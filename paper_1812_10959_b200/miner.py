@@ -309,6 +309,7 @@ def run_engine(tids, n_local: int, m: int, params: MiningParams, *, prune_bound:
             if trace is not None:
                 trace.native = {"stops": out.stops, "replays": out.replays, "issue_ms": out.issue_us / 1e3,
                                 "poll_ms": out.poll_us / 1e3, "graphs_captured": out.graphs_captured,
+                                "batches": out.batches, "batched_stops": out.batched_stops,
                                 "collective": eng.collective_mode() if hasattr(eng, "collective_mode") else "none"}
             stats.interval_counts += out.interval_counts
             stats.candidates_pruned += out.candidates_pruned

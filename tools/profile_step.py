@@ -70,7 +70,7 @@ def main() -> None:
     series = defaultdict(list)
     for s0, e0, n0 in acts:
         for key in ("count_dev", "eval_cand", "apply_prune", "pair_tri", "pair_tc", "dedup", "commit_status", "checkpoint_kernel",
-                    "compact", "status_kernel"):
+                    "compact", "status_kernel", "checkpoint_batch"):
             if key in n0:
                 series[key].append(round(e0 - s0, 1))
     for key, v in series.items():
