@@ -105,3 +105,28 @@ def test_grid_compaction_of_a_large_triple_bucket():
     bits[:1500] |= rng.random((1500, m)) < 0.5
     trace = _check(_rows(bits), m, 0.13, 500)
     assert max(st["dashed_at_start"] for st in trace.stops) > 16384
+
+
+@pytest.mark.parametrize("batch", ["0", "3", "8"])
+def test_batches_of_quiet_stops(monkeypatch, batch):
+    """The tail of a run goes out in batches of stops (one count launch over the
+    next chunks, one single-CTA kernel for their checkpoints); a batch ends
+    early when a stop inserts candidates.  Same result for every batch size,
+    and batches really are used."""
+    monkeypatch.setenv("DIC_BATCH_STOPS", batch)
+    rng = np.random.default_rng(29)
+    n, m = 20000, 48
+    p = rng.beta(2, 6, size=m)
+    bits = rng.random((n, m)) < p
+    # groups planted in the second half only: their itemsets are promoted (and
+    # their supersets inserted) late, in the middle of otherwise quiet stops
+    for g in range(5):
+        items = rng.choice(m, 4, replace=False)
+        on = np.zeros(n, dtype=bool)
+        on[n // 2:] = rng.random(n - n // 2) < 0.5
+        bits[np.ix_(on, items)] = True
+    trace = _check(_rows(bits), m, 0.12, 250)
+    if batch == "0":
+        assert trace.native["batches"] == 0
+    else:
+        assert trace.native["batches"] > 0 and trace.native["batched_stops"] > trace.native["batches"]
