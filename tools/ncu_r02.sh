@@ -9,4 +9,5 @@ $F -k regex:checkpoint_kernel -s 150 -c 1 -o gpurun_out/r02_checkpoint_s150 $T >
 $F -k regex:count_dev_kernel -s 150 -c 1 -o gpurun_out/r02_count_dev_s150_v2 $T > gpurun_out/ncu3.log 2>&1
 $F -k regex:pair_tc_kernel -s 10 -c 1 -o gpurun_out/r02_pair_tc_v8 $T > gpurun_out/ncu4.log 2>&1
 $F -k regex:item_support_kernel -c 1 -o gpurun_out/r02_item_support $T > gpurun_out/ncu5.log 2>&1
+$F -k regex:checkpoint_batch_kernel -s 5 -c 1 -o gpurun_out/r02_checkpoint_batch $T > gpurun_out/ncu6.log 2>&1
 ls -la gpurun_out/*.ncu-rep
