@@ -1313,15 +1313,25 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_kernel(const __gri
 constexpr int64_t kBatchSlots = 2048;  // live slots of a batched stop (one delta block)
 constexpr int kBatchStops = 8;
 
+// The kernel reports what it ran in a host-mapped word — (first sequence number
+// + 1) << 8 | stops run — of the parity of its launch number (a.sync[3]), so the
+// host can keep two batches in flight and still read exactly the ring slots a
+// finished batch wrote.
 __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_batch_kernel(const __grid_constant__ CkptArgs a,
-                                                                       int nstops, unsigned long long* bdelta) {
+                                                                       int nstops, unsigned long long* bdelta,
+                                                                       unsigned long long* report) {
     __shared__ CkptSmem sm;
     unsigned long long* stat = a.stat;
     const int64_t total0 = a.doff[a.kuse_issue];
+    const unsigned long long seq0 = stat[S_SEQ], launch_no = a.sync[3];
     if (stat[S_ABORT] || total0 > kBatchSlots) {
         // skipped by the overflow recovery (its unchanged status), or refused:
         // the count launch made the same test and counted nothing
         if (stat[S_ABORT]) status_body(stat, a.KS, a.kuse, a.ring, a.ring_words, a.doff);
+        if (threadIdx.x == 0) {
+            report[launch_no & 1] = (seq0 + 1) << 8;
+            a.sync[3] = launch_no + 1;
+        }
         return;
     }
     int b = 0;
@@ -1363,6 +1373,10 @@ __global__ void __launch_bounds__(kCkptThreads, 1) checkpoint_batch_kernel(const
     // was re-zeroed by its apply)
     for (int64_t i = (int64_t)b * kBatchSlots + threadIdx.x; i < (int64_t)nstops * kBatchSlots; i += blockDim.x)
         if ((i % kBatchSlots) < total0) bdelta[i] = 0;
+    if (threadIdx.x == 0) {
+        report[launch_no & 1] = ((seq0 + 1) << 8) | (unsigned long long)b;
+        a.sync[3] = launch_no + 1;
+    }
 }
 
 struct TableUpdate {
@@ -1588,6 +1602,7 @@ struct dic_engine {
     GraphKey key_batch{};
     int gx_batch_n = 0;
     bool status_ready = false;  // dic_engine_poll: the stop's status is already on the host (batches)
+    int64_t batch_launches = 0;  // = the device's launch number (a.sync[3])
 
     int32_t* res_ids = nullptr;          // result collection (dic_engine_num_frequent)
     int64_t res_cap = 0, res_F = -1;
@@ -2020,7 +2035,8 @@ int launch_batch(dic_engine* e, int n, cudaStream_t s) {
                                kBatchSlots)))
         return rc;
     const CkptArgs a = checkpoint_args(e, false);
-    checkpoint_batch_kernel<<<1, kCkptThreads, 0, s>>>(a, n, e->bdelta);
+    // (the report words: two of the pinned scratch words past the status ring)
+    checkpoint_batch_kernel<<<1, kCkptThreads, 0, s>>>(a, n, e->bdelta, e->ring_dev + kRing * e->hres.words + 2);
     ::dic::note_launch();
     DIC_CHECK_LAUNCH("checkpoint_batch_kernel");
     return DIC_OK;
@@ -2815,52 +2831,85 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
     };
     while (rc == DIC_OK) {
         if (inflight.empty() && batch_wanted()) {
-            const clk::time_point tb = clk::now();
-            e->kuse_issue = e->kuse;
-            const GraphKey k = graph_key(e, true);
-            if (!e->gx_batch || e->gx_batch_n != batch_n || !(k == e->key_batch)) {
-                if ((rc = capture_graph(e, &e->gx_batch, &e->nk_batch,
-                                        [&](cudaStream_t cs) { return launch_batch(e, batch_n, cs); })))
-                    break;
-                e->key_batch = k;
-                e->gx_batch_n = batch_n;
-            }
-            // the batch's ring slots must not pass for written (the pooled ring
-            // keeps the statuses of earlier runs; nothing is in flight now)
-            for (int i = 0; i < batch_n; ++i)
-                e->ring[(int64_t)((e->issued + i) % kRing) * e->ring_words + S_SEQ] = ~0ull;
-            if ((rc = launch_graph(e, e->gx_batch, e->nk_batch))) break;
-            out->issue_us += us_since(tb);
-            const clk::time_point tp = clk::now();
-            DIC_CUDA(cudaStreamSynchronize(e->s));
-            ++out->batches;
-            for (int i = 0; i < batch_n && rc == DIC_OK && !done; ++i) {
-                // the stops of the batch that ran left their status in the ring
-                const int64_t seq = e->issued;
-                const int slot = (int)(seq % kRing);
-                const unsigned long long* h = e->ring + (int64_t)slot * e->ring_words;
-                if (h[S_SEQ] != (unsigned long long)seq) {
-                    if (i == 0) {
-                        set_error("dic_engine_run: a batch of stops left no status");
-                        rc = DIC_ESTATE;
+            // Batch mode, up to two batches in flight: the second is launched
+            // before the first one's statuses are read, so the GPU does not wait
+            // for the host between batches.  The device keeps its own stop
+            // counter, so the second batch simply continues where the first one
+            // ended (a batch may end early); each reports how many stops it ran.
+            struct InBatch { int par; int kuse; };
+            std::deque<InBatch> bq;
+            bool more = true;
+            volatile unsigned long long* report = e->hres.ring + kRing * e->hres.words + 2;
+            while (rc == DIC_OK && (more || !bq.empty())) {
+                const clk::time_point tb = clk::now();
+                while (rc == DIC_OK && more && (int)bq.size() < 2) {
+                    e->kuse_issue = e->kuse;
+                    const GraphKey k = graph_key(e, true);
+                    if (!e->gx_batch || e->gx_batch_n != batch_n || !(k == e->key_batch)) {
+                        if ((rc = capture_graph(e, &e->gx_batch, &e->nk_batch,
+                                                [&](cudaStream_t cs) { return launch_batch(e, batch_n, cs); })))
+                            break;
+                        e->key_batch = k;
+                        e->gx_batch_n = batch_n;
                     }
-                    break;  // the batch ended before this stop: it is issued again
+                    const int par = (int)(e->batch_launches & 1);
+                    report[par] = 0;
+                    if ((rc = launch_graph(e, e->gx_batch, e->nk_batch))) break;
+                    DIC_CUDA(cudaEventRecord(e->ev[par], e->s));
+                    ++e->batch_launches;
+                    bq.push_back({par, e->kuse});
+                    ++out->batches;
                 }
-                e->kuse_at[slot] = e->kuse;
-                ++e->issued;
-                stop = stop < stop_max ? stop + 1 : 1;
-                dic_stop_status st;
-                int32_t replayed = 0;
-                e->status_ready = true;  // (the stream is idle: no event to wait for)
-                rc = dic_engine_poll(e, seq, &st, &replayed);
-                e->status_ready = false;
-                if (rc) break;
-                ++out->batched_stops;
-                account(Flight{seq, stop}, st, replayed);
-                if (replayed) break;  // (the batch ended at this stop: it overflowed)
+                out->issue_us += us_since(tb);
+                if (rc || bq.empty()) break;
+                const clk::time_point tp = clk::now();
+                const InBatch ib = bq.front();
+                bq.pop_front();
+                DIC_CUDA(cudaEventSynchronize(e->ev[ib.par]));
+                const unsigned long long rep = report[ib.par];
+                const int nrun = (int)(rep & 0xFF);
+                if (nrun > 0 && (rep >> 8) != (unsigned long long)e->issued + 1) {
+                    set_error("dic_engine_run: a batch reports stop %lld, expected %lld", (long long)(rep >> 8) - 1,
+                              (long long)e->issued);
+                    rc = DIC_ESTATE;
+                    break;
+                }
+                if (nrun == 0) more = false;  // refused or skipped: back to single stops
+                for (int i = 0; i < nrun && rc == DIC_OK; ++i) {
+                    const int64_t seq = e->issued;
+                    const int slot = (int)(seq % kRing);
+                    e->kuse_at[slot] = ib.kuse;
+                    ++e->issued;
+                    stop = stop < stop_max ? stop + 1 : 1;
+                    dic_stop_status st;
+                    int32_t replayed = 0;
+                    e->status_ready = true;  // (its kernel has finished: no event to wait for)
+                    rc = dic_engine_poll(e, seq, &st, &replayed);
+                    e->status_ready = false;
+                    if (rc) break;
+                    if (done) {  // (a stop run past the last live one)
+                        out->replays += replayed;
+                        continue;
+                    }
+                    ++out->batched_stops;
+                    account(Flight{seq, stop}, st, replayed);
+                    if (replayed) more = false;  // (it overflowed: a later batch in flight was skipped)
+                }
+                if (done || !batch_wanted()) more = false;
+                out->poll_us += us_since(tp);
             }
-            out->poll_us += us_since(tp);
-            continue;
+            if (rc) break;
+            if (!done && batch_wanted()) {
+                // (refused although wanted: cannot happen with an exact view of the
+                // dashed vector; one single stop guarantees progress anyway)
+                stop = stop < stop_max ? stop + 1 : 1;
+                if ((rc = dic_engine_issue_count(e, lfirst[stop - 1], llast[stop - 1]))) break;
+                int64_t seq = 0;
+                if ((rc = dic_engine_issue_checkpoint(e, &seq))) break;
+                inflight.push_back({seq, stop});
+            } else {
+                continue;
+            }
         }
         const clk::time_point ti = clk::now();
         // (no new single stops once a batch is wanted: the pipeline drains first)
