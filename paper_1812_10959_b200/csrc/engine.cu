@@ -1455,10 +1455,17 @@ __global__ void result_rank_gather_kernel(Records R, int W, const int32_t* __res
     for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < F; i += warps) {
         const ResKey me = keys[i];
         unsigned cnt = 0;
-        for (int64_t j = lane; j < F; j += 32) {
-            const ResKey o = keys[j];
-            const bool less = o.k0 != me.k0 ? o.k0 < me.k0 : (o.k1 != me.k1 ? o.k1 < me.k1 : o.k2 < me.k2);
-            cnt += less ? 1u : 0u;
+        for (int64_t j0 = lane; j0 < F; j0 += 128) {
+            // four keys per lane and round: their loads go out together
+            ResKey o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = j0 + 32 * u < F ? keys[j0 + 32 * u] : ResKey{~0ull, ~0ull, ~0ull};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool less =
+                    o[u].k0 != me.k0 ? o[u].k0 < me.k0 : (o[u].k1 != me.k1 ? o[u].k1 < me.k1 : o[u].k2 < me.k2);
+                cnt += less ? 1u : 0u;
+            }
         }
         const int64_t pos = (int64_t)__reduce_add_sync(0xFFFFFFFFu, cnt);
         const int32_t r = ids[i];
@@ -2855,7 +2862,10 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
                     const int par = (int)(e->batch_launches & 1);
                     report[par] = 0;
                     if ((rc = launch_graph(e, e->gx_batch, e->nk_batch))) break;
-                    DIC_CUDA(cudaEventRecord(e->ev[par], e->s));
+                    if (const cudaError_t ce = cudaEventRecord(e->ev[par], e->s)) {
+                        rc = cuda_fail(ce, "cudaEventRecord(batch)");
+                        break;
+                    }
                     ++e->batch_launches;
                     bq.push_back({par, e->kuse});
                     ++out->batches;
@@ -2865,7 +2875,10 @@ extern "C" int dic_engine_run(dic_engine* e, const int64_t* lfirst, const int64_
                 const clk::time_point tp = clk::now();
                 const InBatch ib = bq.front();
                 bq.pop_front();
-                DIC_CUDA(cudaEventSynchronize(e->ev[ib.par]));
+                if (const cudaError_t ce = cudaEventSynchronize(e->ev[ib.par])) {
+                    rc = cuda_fail(ce, "cudaEventSynchronize(batch)");
+                    break;
+                }
                 const unsigned long long rep = report[ib.par];
                 const int nrun = (int)(rep & 0xFF);
                 if (nrun > 0 && (rep >> 8) != (unsigned long long)e->issued + 1) {
