@@ -13,6 +13,29 @@
 #include <Python.h>
 #include <stdint.h>
 
+/* An arbitrary-precision int from `top` little-endian 64-bit words: the
+ * interpreter's 30-bit digits cut out of the words directly
+ * (_PyLong_FromDigits, CPython >= 3.12), instead of _PyLong_FromByteArray's
+ * byte-by-byte loop (8 x top iterations; three times slower on a 16-word mask). */
+static PyObject* mask_to_long(const uint64_t* w, Py_ssize_t top) {
+#if PY_VERSION_HEX >= 0x030C0000 && PyLong_SHIFT == 30
+    digit d[(64 * 64 + 29) / 30 + 1];
+    if (top <= 64) {
+        const Py_ssize_t bits = top * 64;
+        Py_ssize_t nd = 0;
+        for (Py_ssize_t b = 0; b < bits; b += 30) {
+            const Py_ssize_t i = b >> 6, o = b & 63;
+            uint64_t x = w[i] >> o;
+            if (o > 34 && i + 1 < top) x |= w[i + 1] << (64 - o);
+            d[nd++] = (digit)(x & 0x3FFFFFFFu);
+        }
+        while (nd > 0 && d[nd - 1] == 0) --nd;
+        return (PyObject*)_PyLong_FromDigits(0, nd, d);
+    }
+#endif
+    return _PyLong_FromByteArray((const unsigned char*)w, (size_t)top * 8u, 1, 0);
+}
+
 static PyObject* frequent_tuple(PyObject* self, PyObject* args) {
     PyObject* cls;
     Py_buffer masks, sizes, sups;
@@ -42,7 +65,7 @@ static PyObject* frequent_tuple(PyObject* self, PyObject* args) {
         const uint64_t* row = (const uint64_t*)(mb + (size_t)i * (size_t)W * 8u);
         Py_ssize_t top = W;
         while (top > 1 && row[top - 1] == 0) --top;
-        PyObject* mask = _PyLong_FromByteArray((const unsigned char*)row, (size_t)top * 8u, 1, 0);
+        PyObject* mask = mask_to_long(row, top);
         PyObject* size = PyLong_FromLong(sz[i]);
         PyObject* sup = PyLong_FromLongLong(sp[i]);
         PyObject* item = tp->tp_alloc(tp, 3);
